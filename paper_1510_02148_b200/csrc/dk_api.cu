@@ -1,0 +1,916 @@
+// dk_api.cu — the C ABI (include/dk.h): handles, buffers, the GMRES(m) cycle driver.
+//
+// The driver issues one restart cycle (restart residual, m Arnoldi steps, cycle end) as a
+// fixed kernel sequence; every kernel is gated by a device flag, so the sequence is captured
+// once into a CUDA graph and replayed per cycle.  The host reads one int per cycle to decide
+// whether another cycle is needed — the reference's per-iteration Python control flow
+// (krylov.py:127-212) runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dk_launch.h"
+
+using namespace dk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return DK_ECUDA;
+}
+
+#define DK_TRY(x)                                        \
+  do {                                                   \
+    cudaError_t _e = (x);                                \
+    if (_e != cudaSuccess) return cuda_fail(_e, #x);     \
+  } while (0)
+
+long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+
+// ---- profiling classes ---------------------------------------------------------------
+enum ProfClass {
+  PC_STENCIL = 0,
+  PC_RESTRICT,
+  PC_GEMV,
+  PC_PROJECT,
+  PC_GS,
+  PC_REORTH,
+  PC_CYCLE,
+  PC_XUPDATE,
+  PC_RESTART,
+  PC_COUNT
+};
+const char* kProfNames[PC_COUNT] = {"stencil_restrict", "restrict_final", "coarse_gemv",
+                                    "prolong_dots",     "gs_update",      "gs_reorth",
+                                    "cycle_end",        "x_update",       "restart"};
+
+unsigned long long g_ctx_serial = 0;
+
+}  // namespace
+
+struct dk_defl;
+
+struct dk_op {
+  int dev = 0;
+  long long n = 0, n_pad = 0, guard = 0, vlen = 0;
+  int ndiag = 0, center = -1;
+  long long off[kMaxDiag] = {0};
+  double* dia = nullptr;
+  double* inv_base = nullptr;
+  double* inv = nullptr;
+  cudaStream_t own = nullptr, stream = nullptr;
+  int G = 1;
+  // vectors (guarded)
+  double *w_base = nullptr, *x_base = nullptr, *b_base = nullptr, *x0_base = nullptr,
+         *t_base = nullptr;
+  double *w = nullptr, *x = nullptr, *b = nullptr, *x0 = nullptr, *t = nullptr;
+  double* V_base = nullptr;
+  long long vstride = 0;
+  int v_rows = 0;
+  double* part = nullptr;
+  int part_q = 0;
+  double* nrm = nullptr;  // [4] device norms
+  unsigned int* tickets = nullptr;
+  int* one = nullptr;  // device constant 1 (gate of ungated launches)
+  // solver state
+  State* st = nullptr;
+  State* st_host = nullptr;  // pinned
+  double* scal = nullptr;
+  int scal_m = 0;
+  double* hist = nullptr;
+  int* rof = nullptr;
+  int hist_cap = 0;
+  Scal sc{};
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  unsigned long long g_ctx = ~0ull;
+  int g_m = -1;
+  // profiling
+  bool prof = false;
+  double prof_ms[PC_COUNT] = {0};
+  long long prof_n[PC_COUNT] = {0};
+  double prof_bytes[PC_COUNT] = {0};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> ev_marks;  // (class, index of start event)
+  std::vector<double> ev_bytes;
+  int launches = 0;
+  bool has_last = false;
+};
+
+struct dk_defl {
+  dk_op* op = nullptr;
+  unsigned long long serial = 0;
+  int d = 0, ld = 0, ap = DK_AP_A;
+  int* lab_base = nullptr;
+  int* lab = nullptr;
+  int* tile_run_off = nullptr;
+  double* run_part = nullptr;
+  int* lab_run_ptr = nullptr;
+  int* lab_runs = nullptr;
+  long long nruns = 0, nlabelled = 0;
+  double* E = nullptr;
+  double* Einv = nullptr;
+  int* piv = nullptr;
+  double* xs_base = nullptr;
+  double* xs = nullptr;
+  double* s = nullptr;
+  double* y = nullptr;
+  double* qv_base = nullptr;
+  float ms[4] = {0, 0, 0, 0};
+  RunMap rm{};
+};
+
+namespace {
+
+Dia make_dia(const dk_op* op, bool with_inv) {
+  Dia A{};
+  A.ndiag = op->ndiag;
+  A.center = op->center;
+  for (int k = 0; k < kMaxDiag; ++k) A.off[k] = k < op->ndiag ? op->off[k] : 0;
+  A.dia = op->dia;
+  A.ld = op->n_pad;
+  A.inv = with_inv ? op->inv : nullptr;
+  return A;
+}
+
+int alloc_vec(dk_op* op, double** base, double** ptr) {
+  DK_TRY(cudaMalloc(base, (size_t)op->vlen * sizeof(double)));
+  DK_TRY(cudaMemsetAsync(*base, 0, (size_t)op->vlen * sizeof(double), op->stream));
+  *ptr = *base + op->guard;
+  return DK_OK;
+}
+
+// copy n values (host or device source) into a guarded device vector
+int upload(dk_op* op, double* dst, const double* src) {
+  if (src == nullptr) {
+    DK_TRY(cudaMemsetAsync(dst, 0, (size_t)op->n * sizeof(double), op->stream));
+  } else {
+    DK_TRY(cudaMemcpyAsync(dst, src, (size_t)op->n * sizeof(double), cudaMemcpyDefault,
+                           op->stream));
+  }
+  return DK_OK;
+}
+
+int download(dk_op* op, double* dst, const double* src, long long count) {
+  DK_TRY(cudaMemcpyAsync(dst, src, (size_t)count * sizeof(double), cudaMemcpyDefault, op->stream));
+  return DK_OK;
+}
+
+int ensure_work(dk_op* op, int m, int max_iters) {
+  if (op->v_rows < m + 1) {
+    if (op->V_base) DK_TRY(cudaFree(op->V_base));
+    op->V_base = nullptr;
+    op->vstride = op->n_pad + op->guard;
+    const size_t total = (size_t)op->guard + (size_t)(m + 1) * op->vstride;
+    DK_TRY(cudaMalloc(&op->V_base, total * sizeof(double)));
+    DK_TRY(cudaMemsetAsync(op->V_base, 0, total * sizeof(double), op->stream));
+    op->v_rows = m + 1;
+    op->g_m = -1;  // graph refers to the old basis
+  }
+  if (op->part_q < m + 2) {
+    if (op->part) DK_TRY(cudaFree(op->part));
+    DK_TRY(cudaMalloc(&op->part, (size_t)(m + 2) * op->G * sizeof(double)));
+    op->part_q = m + 2;
+    op->g_m = -1;
+  }
+  if (op->scal_m < m) {
+    if (op->scal) DK_TRY(cudaFree(op->scal));
+    const size_t cnt = 4 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m + (m + 1);
+    DK_TRY(cudaMalloc(&op->scal, cnt * sizeof(double)));
+    DK_TRY(cudaMemsetAsync(op->scal, 0, cnt * sizeof(double), op->stream));
+    op->scal_m = m;
+    op->g_m = -1;
+  }
+  if (op->hist_cap < max_iters + 1) {
+    if (op->hist) DK_TRY(cudaFree(op->hist));
+    if (op->rof) DK_TRY(cudaFree(op->rof));
+    DK_TRY(cudaMalloc(&op->hist, (size_t)(max_iters + 1) * sizeof(double)));
+    DK_TRY(cudaMalloc(&op->rof, (size_t)(max_iters + 1) * sizeof(int)));
+    op->hist_cap = max_iters + 1;
+    op->g_m = -1;
+  }
+  // scalar layout for this m
+  double* p = op->scal;
+  Scal& sc = op->sc;
+  sc.st = op->st;
+  sc.m = m;
+  sc.sigma = p; p += m + 1;
+  sc.coef = p; p += m + 1;
+  sc.corr = p; p += m + 1;
+  sc.g = p; p += m + 1;
+  sc.y = p; p += m + 1;
+  sc.H = p; p += (size_t)(m + 1) * m;
+  sc.R = p; p += (size_t)(m + 1) * m;
+  sc.cs = p; p += m;
+  sc.sn = p; p += m;
+  sc.hist = op->hist;
+  sc.restart_of = op->rof;
+  return DK_OK;
+}
+
+// ---- launch bookkeeping (profiling) ---------------------------------------------------
+cudaEvent_t next_event(dk_op* op) {
+  if (op->ev_used == op->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    op->ev_pool.push_back(e);
+  }
+  return op->ev_pool[op->ev_used++];
+}
+
+struct ProfScope {
+  dk_op* op;
+  int cls;
+  size_t idx = 0;
+  double bytes;
+  ProfScope(dk_op* o, int c, double by) : op(o), cls(c), bytes(by) {
+    op->launches += 1;
+    if (op->prof) {
+      idx = op->ev_used;
+      cudaEventRecord(next_event(op), op->stream);
+    }
+  }
+  ~ProfScope() {
+    if (op->prof) {
+      cudaEventRecord(next_event(op), op->stream);
+      op->ev_marks.push_back({cls, idx});
+      op->ev_bytes.push_back(bytes);
+    }
+  }
+};
+
+void prof_collect(dk_op* op) {
+  if (!op->prof) return;
+  cudaStreamSynchronize(op->stream);
+  for (size_t k = 0; k < op->ev_marks.size(); ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, op->ev_pool[op->ev_marks[k].second],
+                         op->ev_pool[op->ev_marks[k].second + 1]);
+    op->prof_ms[op->ev_marks[k].first] += ms;
+    op->prof_n[op->ev_marks[k].first] += 1;
+    op->prof_bytes[op->ev_marks[k].first] += op->ev_bytes[k];
+  }
+  op->ev_marks.clear();
+  op->ev_bytes.clear();
+  op->ev_used = 0;
+}
+
+// ---- the deflation building blocks ------------------------------------------------------
+// s = Z^T (mode-applied v) ; y = E^-1 s
+void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const double* v,
+                  const double* scale, const double* b, double* out, const int* gate) {
+  const Dia A = make_dia(op, pre);
+  const double n = (double)op->n;
+  {
+    ProfScope ps(op, PC_STENCIL, (mode == ST_IDENT ? 12.0 : 8.0 * op->ndiag + 20.0) * n);
+    launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream);
+  }
+  {
+    ProfScope ps(op, PC_RESTRICT, 12.0 * (double)c->nlabelled + 8.0 * c->d);
+    launch_restrict_final(c->rm, c->s, gate, op->stream);
+  }
+  {
+    ProfScope ps(op, PC_GEMV, 8.0 * (double)c->d * c->ld);
+    launch_gemv(c->Einv, c->d, c->ld, c->s, c->y, gate, op->stream);
+  }
+}
+
+// One GMRES(m) cycle as a fixed kernel sequence (restart, m Arnoldi steps, cycle end).
+void issue_restart(dk_op* op, dk_defl* c) {
+  State* st = op->st;
+  const bool pre = op->inv != nullptr;
+  const bool am = c && c->ap == DK_AP_AM;
+  const Dia A = make_dia(op, pre);
+  const Dia Aam = make_dia(op, am);
+  const double n = (double)op->n;
+  if (c) {
+    coarse_solve(op, c, ST_RESID, false, true, op->x, nullptr, op->b, op->w, &st->running);
+  } else {
+    ProfScope ps(op, PC_STENCIL, (8.0 * op->ndiag + 24.0) * n);
+    launch_stencil(ST_RESID, false, true, A, op->n_pad, op->x, nullptr, op->b, op->w, nullptr,
+                   &st->running, op->stream);
+  }
+  ProfScope ps(op, PC_RESTART, c ? (8.0 * op->ndiag + 20.0) * n : 16.0 * n);
+  launch_project(PJ_RESTART, c != nullptr, am, Aam, c ? c->lab : nullptr, c ? c->y : nullptr,
+                 op->w, op->V_base + op->guard, nullptr, op->vstride, 0, op->n_pad, op->part,
+                 op->G, op->sc, 0, &st->running, op->stream);
+}
+
+void issue_iteration(dk_op* op, dk_defl* c, int j) {
+  State* st = op->st;
+  const bool pre = op->inv != nullptr;
+  const bool am = c && c->ap == DK_AP_AM;
+  const Dia A = make_dia(op, pre);
+  const Dia Aam = make_dia(op, am);
+  const double n = (double)op->n;
+  double* V = op->V_base + op->guard;
+  const int nvec = j + 1;
+  if (c) {
+    coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
+                 nullptr, op->w, &st->active);
+  } else {
+    ProfScope ps(op, PC_STENCIL, (8.0 * op->ndiag + (pre ? 24.0 : 16.0)) * n);
+    launch_stencil(ST_APPLY, pre, true, A, op->n_pad, V + (long long)j * op->vstride,
+                   op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream);
+  }
+  {
+    ProfScope ps(op, PC_PROJECT,
+                 c ? (8.0 * op->ndiag + 20.0 + 8.0 * nvec) * n : (8.0 + 8.0 * nvec) * n);
+    launch_project(PJ_ITER, c != nullptr, am, Aam, c ? c->lab : nullptr, c ? c->y : nullptr,
+                   op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
+                   &st->active, op->stream);
+  }
+  {
+    ProfScope ps(op, PC_GS, (16.0 + 8.0 * nvec) * n);
+    launch_gs(false, op->w, V + (long long)(j + 1) * op->vstride, V, op->vstride, nvec,
+              op->n_pad, op->part, op->G, op->sc, j, &st->active, op->stream);
+  }
+  {
+    ProfScope ps(op, PC_REORTH, (16.0 + 8.0 * nvec) * n);
+    launch_gs(true, V + (long long)(j + 1) * op->vstride, V + (long long)(j + 1) * op->vstride, V,
+              op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j, &st->reorth, op->stream);
+  }
+}
+
+void issue_cycle_end(dk_op* op) {
+  const bool pre = op->inv != nullptr;
+  const Dia A = make_dia(op, pre);
+  {
+    ProfScope ps(op, PC_CYCLE, 0.0);
+    launch_cycle_end(op->sc, op->stream);
+  }
+  ProfScope ps(op, PC_XUPDATE, 0.0);
+  launch_xupdate(A, op->x, op->V_base + op->guard, op->vstride, op->n_pad, op->sc, op->stream);
+}
+
+int read_state(dk_op* op) {
+  DK_TRY(cudaMemcpyAsync(op->st_host, op->st, sizeof(State), cudaMemcpyDeviceToHost, op->stream));
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  return DK_OK;
+}
+
+int build_graph(dk_op* op, dk_defl* c, int m) {
+  if (op->gexec && op->g_m == m && op->g_ctx == (c ? c->serial : 0ull)) return DK_OK;
+  if (op->gexec) {
+    cudaGraphExecDestroy(op->gexec);
+    op->gexec = nullptr;
+  }
+  cudaGraph_t g;
+  DK_TRY(cudaStreamBeginCapture(op->stream, cudaStreamCaptureModeThreadLocal));
+  const int l0 = op->launches;
+  issue_restart(op, c);
+  for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
+  issue_cycle_end(op);
+  op->launches = l0;
+  DK_TRY(cudaStreamEndCapture(op->stream, &g));
+  cudaError_t e = cudaGraphInstantiate(&op->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  op->g_m = m;
+  op->g_ctx = c ? c->serial : 0ull;
+  return DK_OK;
+}
+
+__global__ void k_scale_copy(const double* __restrict__ u, const double* __restrict__ sig,
+                             double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = u[i] * (*sig);
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+const char* dk_last_error(void) { return g_err.c_str(); }
+
+int dk_version(void) { return 1; }
+
+int dk_device_count(int32_t* count) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  cudaGetLastError();
+  *count = c;
+  return DK_OK;
+}
+
+int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
+                 const double* diags, const double* inv_diag) {
+  if (!out) return fail(DK_EINVAL, "null handle pointer");
+  *out = nullptr;
+  if (n < 1) return fail(DK_EINVAL, "operator dimension must be >= 1");
+  if (n > (1ll << 31) - (1ll << 24)) return fail(DK_EUNSUPPORTED, "n too large for int32 labels");
+  if (ndiag < 1 || ndiag > kMaxDiag)
+    return fail(DK_EUNSUPPORTED, "the device path supports 1..7 diagonals (7-point stencil)");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt < 1) {
+    cudaGetLastError();
+    return fail(DK_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  std::vector<std::pair<long long, int>> order;
+  for (int k = 0; k < ndiag; ++k) {
+    if (offsets[k] <= -n || offsets[k] >= n) return fail(DK_EINVAL, "diagonal offset out of range");
+    order.push_back({(long long)offsets[k], k});
+  }
+  std::sort(order.begin(), order.end());
+  for (int k = 1; k < ndiag; ++k)
+    if (order[k].first == order[k - 1].first) return fail(DK_EINVAL, "duplicate diagonal offset");
+  dk_op* op = new dk_op();
+  DK_TRY(cudaGetDevice(&op->dev));
+  DK_TRY(cudaStreamCreateWithFlags(&op->own, cudaStreamNonBlocking));
+  op->stream = op->own;
+  op->n = n;
+  op->n_pad = round_up(n, kTile);
+  long long mo = 0;
+  for (int k = 0; k < ndiag; ++k) mo = std::max(mo, std::llabs(order[k].first));
+  op->guard = round_up(std::max(mo + 2, 256ll), 256);
+  op->vlen = op->n_pad + 2 * op->guard;
+  op->ndiag = ndiag;
+  for (int k = 0; k < ndiag; ++k) {
+    op->off[k] = order[k].first;
+    if (order[k].first == 0) op->center = k;
+  }
+  const long long nch = op->n_pad / kChunk;
+  op->G = (int)std::min<long long>(nch, 148 * 4);
+  DK_TRY(cudaMalloc(&op->dia, (size_t)ndiag * op->n_pad * sizeof(double)));
+  DK_TRY(cudaMemsetAsync(op->dia, 0, (size_t)ndiag * op->n_pad * sizeof(double), op->stream));
+  for (int k = 0; k < ndiag; ++k) {
+    DK_TRY(cudaMemcpyAsync(op->dia + (size_t)k * op->n_pad, diags + (size_t)order[k].second * n,
+                           (size_t)n * sizeof(double), cudaMemcpyDefault, op->stream));
+  }
+  if (inv_diag) {
+    int rc = alloc_vec(op, &op->inv_base, &op->inv);
+    if (rc) return rc;
+    rc = upload(op, op->inv, inv_diag);
+    if (rc) return rc;
+  }
+  int rc;
+  if ((rc = alloc_vec(op, &op->w_base, &op->w))) return rc;
+  if ((rc = alloc_vec(op, &op->x_base, &op->x))) return rc;
+  if ((rc = alloc_vec(op, &op->b_base, &op->b))) return rc;
+  if ((rc = alloc_vec(op, &op->x0_base, &op->x0))) return rc;
+  if ((rc = alloc_vec(op, &op->t_base, &op->t))) return rc;
+  DK_TRY(cudaMalloc(&op->st, sizeof(State)));
+  DK_TRY(cudaMemsetAsync(op->st, 0, sizeof(State), op->stream));
+  DK_TRY(cudaMallocHost(&op->st_host, sizeof(State)));
+  DK_TRY(cudaMalloc(&op->nrm, 4 * sizeof(double)));
+  DK_TRY(cudaMalloc(&op->tickets, 4 * sizeof(unsigned int)));
+  {
+    const int one_h = 1;
+    DK_TRY(cudaMalloc(&op->one, sizeof(int)));
+    DK_TRY(cudaMemcpy(op->one, &one_h, sizeof(int), cudaMemcpyHostToDevice));
+  }
+  DK_TRY(cudaMemsetAsync(op->tickets, 0, 4 * sizeof(unsigned int), op->stream));
+  rc = ensure_work(op, 1, 1);
+  if (rc) return rc;
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  *out = op;
+  return DK_OK;
+}
+
+int dk_op_destroy(dk_op* op) {
+  if (!op) return DK_OK;
+  cudaStreamSynchronize(op->stream);
+  if (op->gexec) cudaGraphExecDestroy(op->gexec);
+  for (auto e : op->ev_pool) cudaEventDestroy(e);
+  void* bufs[] = {op->dia, op->inv_base, op->w_base, op->x_base, op->b_base, op->x0_base,
+                  op->t_base, op->V_base, op->part, op->nrm, op->tickets, op->one, op->st, op->scal,
+                  op->hist, op->rof};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (op->st_host) cudaFreeHost(op->st_host);
+  if (op->own) cudaStreamDestroy(op->own);
+  delete op;
+  return DK_OK;
+}
+
+int dk_op_set_precond(dk_op* op, const double* inv_diag) {
+  if (!op) return fail(DK_EINVAL, "null operator");
+  if (inv_diag == nullptr) {
+    op->inv = nullptr;
+  } else {
+    if (!op->inv_base) {
+      int rc = alloc_vec(op, &op->inv_base, &op->inv);
+      if (rc) return rc;
+    }
+    op->inv = op->inv_base + op->guard;
+    int rc = upload(op, op->inv, inv_diag);
+    if (rc) return rc;
+    DK_TRY(cudaStreamSynchronize(op->stream));
+  }
+  if (op->gexec) {  // the graph bakes the preconditioner in
+    cudaGraphExecDestroy(op->gexec);
+    op->gexec = nullptr;
+    op->g_m = -1;
+  }
+  return DK_OK;
+}
+
+int dk_op_set_stream(dk_op* op, void* stream) {
+  if (!op) return fail(DK_EINVAL, "null operator");
+  cudaStreamSynchronize(op->stream);
+  op->stream = stream ? (cudaStream_t)stream : op->own;
+  if (op->gexec) {
+    cudaGraphExecDestroy(op->gexec);
+    op->gexec = nullptr;
+    op->g_m = -1;
+  }
+  return DK_OK;
+}
+
+int dk_op_spmv(dk_op* op, const double* x, double* y) {
+  if (!op || !x || !y) return fail(DK_EINVAL, "null argument");
+  int rc = upload(op, op->t, x);
+  if (rc) return rc;
+  const Dia A = make_dia(op, false);
+  launch_stencil(ST_APPLY, false, true, A, op->n_pad, op->t, nullptr, nullptr, op->w, nullptr,
+                 nullptr, op->stream);
+  DK_TRY(cudaGetLastError());
+  rc = download(op, y, op->w, op->n);
+  if (rc) return rc;
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  return DK_OK;
+}
+
+int dk_op_profile(dk_op* op, int32_t enable) {
+  if (!op) return fail(DK_EINVAL, "null operator");
+  op->prof = enable != 0;
+  for (int k = 0; k < PC_COUNT; ++k) {
+    op->prof_ms[k] = 0;
+    op->prof_n[k] = 0;
+    op->prof_bytes[k] = 0;
+  }
+  return DK_OK;
+}
+
+int dk_op_profile_read(dk_op* op, int32_t cap, const char** names, double* ms, int64_t* launches,
+                       double* bytes) {
+  if (!op) return fail(DK_EINVAL, "null operator");
+  const int k = std::min<int>(cap, PC_COUNT);
+  for (int i = 0; i < k; ++i) {
+    names[i] = kProfNames[i];
+    ms[i] = op->prof_ms[i];
+    launches[i] = op->prof_n[i];
+    bytes[i] = op->prof_bytes[i];
+  }
+  return k;
+}
+
+// ---- deflation ----------------------------------------------------------------------------
+int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t d,
+                   int32_t ap_choice, const double* b) {
+  if (!out || !op || !col_of_cell) return fail(DK_EINVAL, "null argument");
+  *out = nullptr;
+  if (d < 1) return fail(DK_EINVAL, "Z must be n x d with d >= 1");
+  if (ap_choice != DK_AP_A && ap_choice != DK_AP_AM)
+    return fail(DK_EINVAL, "A_p_choice must be 'A' or 'AM'");
+  if (ap_choice == DK_AP_AM && op->inv == nullptr) {
+    // A M^-1 with the identity preconditioner is A itself
+    ap_choice = DK_AP_A;
+  }
+  const long long n = op->n, n_pad = op->n_pad;
+  // host copy of the labels (input may live on the device)
+  std::vector<int> lab(n_pad, -1);
+  DK_TRY(cudaMemcpy(lab.data(), col_of_cell, (size_t)n * sizeof(int), cudaMemcpyDefault));
+  std::vector<long long> count(d, 0);
+  for (long long i = 0; i < n; ++i) {
+    if (lab[i] < -1 || lab[i] >= d) return fail(DK_EINVAL, "column label out of range");
+    if (lab[i] >= 0) count[lab[i]]++;
+  }
+  for (int L = 0; L < d; ++L)
+    if (count[L] == 0) {
+      // an empty indicator column makes E exactly singular (deflation.py:27-28 / sparse.py:135)
+      return fail(DK_ESINGULAR, "zero pivot in LU factorization");
+    }
+  // runs: maximal equal-label ranges in linear order, every tile start is a head
+  const long long ntiles = n_pad / kTile;
+  std::vector<int> tile_off(ntiles + 1, 0);
+  std::vector<int> run_label;
+  run_label.reserve(n_pad / 8 + 16);
+  for (long long i = 0; i < n_pad; ++i) {
+    if (i % kTile == 0) tile_off[i / kTile] = (int)run_label.size();
+    if (i % kTile == 0 || lab[i] != lab[i - 1]) run_label.push_back(lab[i]);
+  }
+  tile_off[ntiles] = (int)run_label.size();
+  const long long nruns = (long long)run_label.size();
+  if (nruns >= (1ll << 31)) return fail(DK_EUNSUPPORTED, "too many label runs");
+  std::vector<int> ptr(d + 1, 0);
+  for (long long r = 0; r < nruns; ++r)
+    if (run_label[r] >= 0) ptr[run_label[r] + 1]++;
+  for (int L = 0; L < d; ++L) ptr[L + 1] += ptr[L];
+  std::vector<int> runs(std::max(ptr[d], 1));
+  {
+    std::vector<int> fillp(ptr.begin(), ptr.end() - 1);
+    for (long long r = 0; r < nruns; ++r)
+      if (run_label[r] >= 0) runs[fillp[run_label[r]]++] = (int)r;
+  }
+  dk_defl* c = new dk_defl();
+  c->op = op;
+  c->serial = ++g_ctx_serial;
+  c->d = d;
+  c->ld = (int)round_up(d, 2);
+  c->ap = ap_choice;
+  c->nruns = nruns;
+  c->nlabelled = ptr[d];
+  cudaStream_t s = op->stream;
+  auto cleanup_fail = [&](cudaError_t e, const char* where) {
+    dk_defl_destroy(c);
+    return cuda_fail(e, where);
+  };
+#define DKD(x)                                           \
+  do {                                                   \
+    cudaError_t _e = (x);                                \
+    if (_e != cudaSuccess) return cleanup_fail(_e, #x);  \
+  } while (0)
+  DKD(cudaMalloc(&c->lab_base, (size_t)op->vlen * sizeof(int)));
+  DKD(cudaMemsetAsync(c->lab_base, 0xff, (size_t)op->vlen * sizeof(int), s));  // -1
+  c->lab = c->lab_base + op->guard;
+  DKD(cudaMemcpyAsync(c->lab, lab.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice, s));
+  DKD(cudaMalloc(&c->tile_run_off, tile_off.size() * sizeof(int)));
+  DKD(cudaMemcpyAsync(c->tile_run_off, tile_off.data(), tile_off.size() * sizeof(int),
+                      cudaMemcpyHostToDevice, s));
+  DKD(cudaMalloc(&c->run_part, (size_t)nruns * sizeof(double)));
+  DKD(cudaMalloc(&c->lab_run_ptr, ptr.size() * sizeof(int)));
+  DKD(cudaMemcpyAsync(c->lab_run_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice,
+                      s));
+  DKD(cudaMalloc(&c->lab_runs, runs.size() * sizeof(int)));
+  DKD(cudaMemcpyAsync(c->lab_runs, runs.data(), runs.size() * sizeof(int), cudaMemcpyHostToDevice,
+                      s));
+  DKD(cudaMalloc(&c->E, (size_t)d * c->ld * sizeof(double)));
+  DKD(cudaMalloc(&c->Einv, (size_t)d * c->ld * sizeof(double)));
+  DKD(cudaMalloc(&c->piv, (size_t)d * sizeof(int)));
+  DKD(cudaMalloc(&c->s, (size_t)c->ld * sizeof(double)));
+  DKD(cudaMalloc(&c->y, (size_t)c->ld * sizeof(double)));
+  DKD(cudaMemsetAsync(c->s, 0, (size_t)c->ld * sizeof(double), s));
+  DKD(cudaMemsetAsync(c->y, 0, (size_t)c->ld * sizeof(double), s));
+  DKD(cudaMalloc(&c->xs_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMemsetAsync(c->xs_base, 0, (size_t)op->vlen * sizeof(double), s));
+  c->xs = c->xs_base + op->guard;
+  DKD(cudaMalloc(&c->qv_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMemsetAsync(c->qv_base, 0, (size_t)op->vlen * sizeof(double), s));
+  c->rm.lab = c->lab;
+  c->rm.tile_run_off = c->tile_run_off;
+  c->rm.run_part = c->run_part;
+  c->rm.lab_run_ptr = c->lab_run_ptr;
+  c->rm.lab_runs = c->lab_runs;
+  c->rm.d = d;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  const bool am = ap_choice == DK_AP_AM;
+  int err = build_coarse(make_dia(op, am), am, c->lab, n_pad, c->rm, c->E, c->ld,
+                         c->qv_base + op->guard, s);
+  cudaEventRecord(e1, s);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&c->ms[0], e0, e1);
+  if (err) return cleanup_fail((cudaError_t)err, "build_coarse");
+  // keep a copy of E for inspection (the LU runs in place on E)
+  double* Ework = nullptr;
+  DKD(cudaMalloc(&Ework, (size_t)d * c->ld * sizeof(double)));
+  DKD(cudaMemcpyAsync(Ework, c->E, (size_t)d * c->ld * sizeof(double), cudaMemcpyDeviceToDevice,
+                      s));
+  double min_piv = 0.0;
+  err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
+  cudaFree(Ework);
+  if (err) return cleanup_fail((cudaError_t)err, "lu_and_inverse");
+  if (!(min_piv >= 1e-300)) {  // sparse.py:135-136 (NaN pivots are singular too)
+    dk_defl_destroy(c);
+    return fail(DK_ESINGULAR, "zero pivot in LU factorization");
+  }
+  // x* = Z E^-1 Z^T b  (deflation.py:88)
+  cudaEventRecord(e0, s);
+  if (b) {
+    int rc = upload(op, op->t, b);
+    if (rc) {
+      dk_defl_destroy(c);
+      return rc;
+    }
+    coarse_solve(op, c, ST_IDENT, false, false, op->t, nullptr, nullptr, nullptr, nullptr);
+    launch_bcast(c->lab, c->y, c->xs, n_pad, s);
+  }
+  cudaEventRecord(e1, s);
+  DKD(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&c->ms[3], e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  DKD(cudaGetLastError());
+  *out = c;
+#undef DKD
+  return DK_OK;
+}
+
+int dk_defl_destroy(dk_defl* c) {
+  if (!c) return DK_OK;
+  if (c->op) cudaStreamSynchronize(c->op->stream);
+  void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->lab_runs,
+                  c->E,        c->Einv,         c->piv,      c->xs_base,     c->s,
+                  c->y,        c->qv_base};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  delete c;
+  return DK_OK;
+}
+
+int dk_defl_apply_p1(dk_defl* c, const double* v, double* out) {
+  if (!c || !v || !out) return fail(DK_EINVAL, "null argument");
+  dk_op* op = c->op;
+  int rc = upload(op, op->t, v);
+  if (rc) return rc;
+  coarse_solve(op, c, ST_IDENT, false, false, op->t, nullptr, nullptr, nullptr, nullptr);
+  const bool am = c->ap == DK_AP_AM;
+  launch_project(PJ_PLAIN, true, am, make_dia(op, am), c->lab, c->y, op->t, op->w, nullptr, 0, 0,
+                 op->n_pad, op->part, op->G, op->sc, 0, op->one, op->stream);
+  DK_TRY(cudaGetLastError());
+  rc = download(op, out, op->w, op->n);
+  if (rc) return rc;
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  return DK_OK;
+}
+
+static int p2_into(dk_defl* c, const double* v, double* dst, bool add_xstar) {
+  dk_op* op = c->op;
+  int rc = upload(op, op->t, v);
+  if (rc) return rc;
+  const bool am = c->ap == DK_AP_AM;
+  coarse_solve(op, c, ST_APPLY, am, false, op->t, nullptr, nullptr, nullptr, nullptr);
+  if (add_xstar) launch_recon(c->lab, c->y, c->xs, op->t, op->w, op->n_pad, op->stream);
+  else launch_sub_bcast(c->lab, c->y, op->t, op->w, op->n_pad, op->stream);
+  DK_TRY(cudaGetLastError());
+  rc = download(op, dst, op->w, op->n);
+  if (rc) return rc;
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  return DK_OK;
+}
+
+int dk_defl_apply_p2(dk_defl* c, const double* v, double* out) {
+  if (!c || !v || !out) return fail(DK_EINVAL, "null argument");
+  return p2_into(c, v, out, false);
+}
+
+int dk_defl_reconstruct(dk_defl* c, const double* xhat, double* out) {
+  if (!c || !xhat || !out) return fail(DK_EINVAL, "null argument");
+  return p2_into(c, xhat, out, true);
+}
+
+int dk_defl_x_star(dk_defl* c, double* out) {
+  if (!c || !out) return fail(DK_EINVAL, "null argument");
+  int rc = download(c->op, out, c->xs, c->op->n);
+  if (rc) return rc;
+  DK_TRY(cudaStreamSynchronize(c->op->stream));
+  return DK_OK;
+}
+
+int dk_defl_coarse(dk_defl* c, double* E, double* Einv) {
+  if (!c) return fail(DK_EINVAL, "null argument");
+  cudaStream_t s = c->op->stream;
+  if (E)
+    DK_TRY(cudaMemcpy2DAsync(E, (size_t)c->d * sizeof(double), c->E, (size_t)c->ld * sizeof(double),
+                             (size_t)c->d * sizeof(double), c->d, cudaMemcpyDefault, s));
+  if (Einv)
+    DK_TRY(cudaMemcpy2DAsync(Einv, (size_t)c->d * sizeof(double), c->Einv,
+                             (size_t)c->ld * sizeof(double), (size_t)c->d * sizeof(double), c->d,
+                             cudaMemcpyDefault, s));
+  DK_TRY(cudaStreamSynchronize(s));
+  return DK_OK;
+}
+
+int dk_defl_setup_ms(dk_defl* c, double* ms4) {
+  if (!c || !ms4) return fail(DK_EINVAL, "null argument");
+  for (int k = 0; k < 4; ++k) ms4[k] = c->ms[k];
+  return DK_OK;
+}
+
+// ---- solver -------------------------------------------------------------------------------
+int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m, double tol,
+             int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
+             int32_t* restart_of, double* hbar, dk_solve_info* info) {
+  if (!op || !b || !x_out || !info) return fail(DK_EINVAL, "null argument");
+  if (c && c->op != op) return fail(DK_EINVAL, "deflation context belongs to another operator");
+  if (m < 1) return fail(DK_EINVAL, "cycle size must be >= 1");
+  if (max_iters < 0) max_iters = 0;
+  int rc = ensure_work(op, m, max_iters);
+  if (rc) return rc;
+  op->launches = 0;
+  if ((rc = upload(op, op->b, b))) return rc;
+  if ((rc = upload(op, op->x0, x0))) return rc;
+  DK_TRY(cudaMemcpyAsync(op->x, op->x0, (size_t)op->n_pad * sizeof(double),
+                         cudaMemcpyDeviceToDevice, op->stream));
+  launch_init_state(op->sc, tol, m, max_iters, min_iters, op->stream);
+  op->launches += 1;
+  if (!op->prof) {
+    rc = build_graph(op, c, m);
+    if (rc) return rc;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, op->stream);
+  const int per_cycle_launches = (c ? 4 : 2) + m * (c ? 6 : 4) + 2;
+  long long guard_cycles = (long long)max_iters + 2;
+  for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
+    if (!op->prof) {
+      DK_TRY(cudaGraphLaunch(op->gexec, op->stream));
+      op->launches += per_cycle_launches;
+    } else {
+      issue_restart(op, c);
+      if ((rc = read_state(op))) return rc;
+      for (int j = 0; j < m && op->st_host->active; ++j) {
+        issue_iteration(op, c, j);
+        if ((rc = read_state(op))) return rc;
+      }
+      issue_cycle_end(op);
+      prof_collect(op);
+    }
+    if ((rc = read_state(op))) return rc;
+    if (!op->st_host->running) break;
+  }
+  cudaEventRecord(e1, op->stream);
+  DK_TRY(cudaEventSynchronize(e1));
+  float solve_ms = 0.f;
+  cudaEventElapsedTime(&solve_ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  DK_TRY(cudaGetLastError());
+  // finalize: reconstruct (krylov.py:220-221), true residuals (:222-225)
+  double* xf = op->x;
+  if (c) {
+    const bool am = c->ap == DK_AP_AM;
+    coarse_solve(op, c, ST_APPLY, am, false, op->x, nullptr, nullptr, nullptr, nullptr);
+    launch_recon(c->lab, c->y, c->xs, op->x, op->t, op->n_pad, op->stream);
+    xf = op->t;
+    op->launches += 4;
+  }
+  const Dia A = make_dia(op, false);
+  launch_stencil(ST_RESID, false, true, A, op->n_pad, xf, nullptr, op->b, op->w, nullptr, nullptr,
+                 op->stream);
+  launch_norm(op->w, op->n_pad, op->part, op->G, op->tickets + 0, op->nrm + 0, op->stream);
+  launch_stencil(ST_RESID, false, true, A, op->n_pad, op->x0, nullptr, op->b, op->w, nullptr,
+                 nullptr, op->stream);
+  launch_norm(op->w, op->n_pad, op->part, op->G, op->tickets + 1, op->nrm + 1, op->stream);
+  op->launches += 4;
+  DK_TRY(cudaGetLastError());
+  double nr[2] = {0, 0};
+  DK_TRY(cudaMemcpyAsync(nr, op->nrm, 2 * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+  if ((rc = read_state(op))) return rc;
+  const State& S = *op->st_host;
+  if ((rc = download(op, x_out, xf, op->n))) return rc;
+  if (hist) DK_TRY(cudaMemcpyAsync(hist, op->hist, (size_t)(S.iterations + 1) * sizeof(double),
+                                   cudaMemcpyDefault, op->stream));
+  if (restart_of)
+    DK_TRY(cudaMemcpyAsync(restart_of, op->rof, (size_t)(S.iterations + 1) * sizeof(int),
+                           cudaMemcpyDefault, op->stream));
+  if (hbar)
+    DK_TRY(cudaMemcpyAsync(hbar, op->sc.H, (size_t)(m + 1) * m * sizeof(double),
+                           cudaMemcpyDefault, op->stream));
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  info->iterations = S.iterations;
+  info->cycles = S.cycle;
+  info->restarts = std::max(S.cycle - 1, 0);
+  info->converged = S.converged;
+  info->warning = S.warning;
+  info->last_cols = S.last_cols;
+  info->reorths = S.reorths;
+  info->kernel_launches = op->launches;
+  info->final_relres = nr[0] / (nr[1] > 0 ? nr[1] : 1.0);
+  info->solve_seconds = solve_ms * 1e-3;
+  op->has_last = S.cycle > 0;
+  return DK_OK;
+}
+
+int dk_last_basis_vector(dk_op* op, int32_t i, double* out) {
+  if (!op || !out) return fail(DK_EINVAL, "null argument");
+  if (!op->has_last || i < 0 || i >= op->v_rows) return fail(DK_EINVAL, "no such basis vector");
+  const State& S = *op->st_host;
+  if (i > S.last_cols) return fail(DK_EINVAL, "basis index beyond the last cycle");
+  double* V = op->V_base + op->guard;
+  if (i == S.cycle_cols && S.last_broke) {
+    // the reference never fills V[j+1] when the cycle stopped at j (krylov.py:195-197)
+    DK_TRY(cudaMemsetAsync(op->t, 0, (size_t)op->n * sizeof(double), op->stream));
+  } else {
+    k_scale_copy<<<148 * 4, 256, 0, op->stream>>>(V + (long long)i * op->vstride, op->sc.sigma + i,
+                                                  op->t, op->n);
+  }
+  DK_TRY(cudaGetLastError());
+  int rc = download(op, out, op->t, op->n);
+  if (rc) return rc;
+  DK_TRY(cudaStreamSynchronize(op->stream));
+  return DK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,592 @@
+// dk_coarse.cu — the coarse operator E = Z^T A_p Z on the device: deterministic assembly,
+// dense fp64 LU with partial pivoting, explicit inverse, and the per-iteration GEMV
+// y = E^-1 s.  Replaces build_context's AZ / E / dense_lu (deflation.py:84-88,
+// sparse.py:121-137) and lu_solve (sparse.py:140-145).
+//
+// Why an explicit inverse: every GMRES iteration needs one coarse solve.  Forward and
+// backward substitution with the LU factors is a d-long dependency chain; y = E^-1 s is a
+// fully parallel GEMV that streams the same 8 d^2 bytes at HBM rate (and from L2 when
+// 8 d^2 fits in the 126 MB L2).  The inverse is formed once from the LU factors.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "dk_launch.h"
+
+namespace dk {
+
+// ======================================================================================
+// GEMV y = M x (one warp per row, x staged in shared memory, fixed summation order).
+// ======================================================================================
+template <bool SMEM_X>
+__global__ void __launch_bounds__(kThreads) k_gemv(const double* __restrict__ M, int d, int ld,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y,
+                                                   const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  extern __shared__ double sx[];
+  const double* xs = x;
+  if (SMEM_X) {
+    for (int i = threadIdx.x; i < ld; i += blockDim.x) sx[i] = i < d ? x[i] : 0.0;
+    __syncthreads();
+    xs = sx;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = gw; r < d; r += nw) {
+    const double* row = M + r * ld;
+    double a0 = 0.0, a1 = 0.0;
+    int c = 2 * lane;
+    for (; c + 64 < ld; c += 128) {
+      const double2 p = ld2(row + c);
+      const double2 q = ld2(row + c + 64);
+      a0 = fma(p.x, xs[c], a0);
+      a1 = fma(p.y, xs[c + 1], a1);
+      a0 = fma(q.x, xs[c + 64], a0);
+      a1 = fma(q.y, xs[c + 65], a1);
+    }
+    for (; c < ld; c += 64) {
+      const double2 p = ld2(row + c);
+      a0 = fma(p.x, xs[c], a0);
+      a1 = fma(p.y, xs[c + 1], a1);
+    }
+    const double s = warp_sum(a0 + a1);
+    if (lane == 0) y[r] = s;
+  }
+}
+
+void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
+                 cudaStream_t s) {
+  const size_t smem = (size_t)ld * sizeof(double);
+  long long blocks = ((long long)d * 32 + kThreads - 1) / kThreads;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (smem <= 200 * 1024) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set = true;
+    }
+    k_gemv<true><<<(unsigned)blocks, kThreads, smem, s>>>(M, d, ld, x, y, gate);
+  } else {
+    k_gemv<false><<<(unsigned)blocks, kThreads, 0, s>>>(M, d, ld, x, y, gate);
+  }
+}
+
+// ======================================================================================
+// Assembly of E = Z^T A_p Z for an indicator Z given by labels.
+//   E[L][L]  = sum over cells i of L of q_i, q_i = sum of the row's coefficients whose
+//              column is in L — a run-wise restriction of q (deterministic);
+//   E[L][L2] = sum over (i in L, k in L2, k = i + off) of a_ik — the boundary-face list is
+//              sorted by key (L, L2) with a stable radix sort and summed per key in cell
+//              order (deterministic).
+// With A_p = A M^-1 the coefficient a_ik is scaled by inv_diag_k (deflation.py:84).
+// ======================================================================================
+template <bool AM>
+__device__ __forceinline__ double coarse_coef(const Dia& A, int q, long long i) {
+  double a = A.dia[q * A.ld + i];
+  if (AM) a = __dmul_rn(a, A.inv[i + A.off[q]]);
+  return a;
+}
+
+template <bool AM>
+__global__ void k_coarse_scan(Dia A, const int* __restrict__ lab, long long n_pad,
+                              double* __restrict__ qv, int* __restrict__ cnt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int L = lab[i];
+    double q = 0.0;
+    int c = 0;
+    if (L >= 0) {
+      for (int k = 0; k < A.ndiag; ++k) {
+        const int L2 = lab[i + A.off[k]];
+        if (L2 == L) q = __dadd_rn(q, coarse_coef<AM>(A, k, i));
+        else if (L2 >= 0) ++c;
+      }
+    }
+    qv[i] = q;
+    cnt[i] = c;
+  }
+}
+
+template <bool AM>
+__global__ void k_coarse_emit(Dia A, const int* __restrict__ lab, long long n_pad, int d,
+                              const int* __restrict__ off, unsigned long long* __restrict__ keys,
+                              double* __restrict__ vals) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int L = lab[i];
+    if (L < 0) continue;
+    int p = off[i];
+    for (int k = 0; k < A.ndiag; ++k) {
+      const int L2 = lab[i + A.off[k]];
+      if (L2 >= 0 && L2 != L) {
+        keys[p] = (unsigned long long)L * (unsigned long long)d + (unsigned long long)L2;
+        vals[p] = coarse_coef<AM>(A, k, i);
+        ++p;
+      }
+    }
+  }
+}
+
+__global__ void k_coarse_reduce(const unsigned long long* __restrict__ keys,
+                                const double* __restrict__ vals, long long nk, int d,
+                                double* __restrict__ E, int ld) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nk;
+       k += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[k];
+    if (k > 0 && keys[k - 1] == key) continue;
+    double s = 0.0;
+    for (long long t = k; t < nk && keys[t] == key; ++t) s = __dadd_rn(s, vals[t]);
+    const long long L = (long long)(key / (unsigned long long)d);
+    const long long L2 = (long long)(key % (unsigned long long)d);
+    E[L * ld + L2] = s;
+  }
+}
+
+__global__ void k_set_diag(double* __restrict__ E, int d, int ld, const double* __restrict__ s) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+    E[(long long)i * ld + i] = s[i];
+}
+
+static int bits_for(unsigned long long v) {
+  int b = 1;
+  while (b < 64 && (1ull << b) <= v) ++b;
+  return b;
+}
+
+int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const RunMap& rm,
+                 double* E, int ld, double* qv, cudaStream_t s) {
+  const int d = rm.d;
+  cudaError_t err;
+  int* cnt = nullptr;
+  int* off = nullptr;
+  void* tmp = nullptr;
+  unsigned long long *k_in = nullptr, *k_out = nullptr;
+  double *v_in = nullptr, *v_out = nullptr, *sdiag = nullptr;
+  int total = 0, last_cnt = 0;
+  size_t tmp_bytes = 0, need = 0;
+  const unsigned grid = 148 * 8;
+  long long nk = 0;
+#define DKC(x)                       \
+  do {                               \
+    err = (x);                       \
+    if (err != cudaSuccess) goto fail; \
+  } while (0)
+  DKC(cudaMemsetAsync(E, 0, (size_t)d * ld * sizeof(double), s));
+  DKC(cudaMallocAsync(&cnt, (size_t)n_pad * sizeof(int), s));
+  DKC(cudaMallocAsync(&off, (size_t)n_pad * sizeof(int), s));
+  DKC(cudaMallocAsync(&sdiag, (size_t)(d > 0 ? d : 1) * sizeof(double), s));
+  if (am) k_coarse_scan<true><<<grid, kThreads, 0, s>>>(A, lab, n_pad, qv, cnt);
+  else k_coarse_scan<false><<<grid, kThreads, 0, s>>>(A, lab, n_pad, qv, cnt);
+  DKC(cudaGetLastError());
+  // diagonal: run-wise restriction of q
+  launch_stencil(ST_IDENT, false, false, A, n_pad, qv, nullptr, nullptr, nullptr, &rm, nullptr, s);
+  launch_restrict_final(rm, sdiag, nullptr, s);
+  k_set_diag<<<(d + kThreads - 1) / kThreads, kThreads, 0, s>>>(E, d, ld, sdiag);
+  DKC(cudaGetLastError());
+  // off-diagonal: boundary faces
+  DKC(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, (int)n_pad, s));
+  DKC(cudaMallocAsync(&tmp, tmp_bytes, s));
+  DKC(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)n_pad, s));
+  DKC(cudaMemcpyAsync(&total, off + n_pad - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DKC(cudaMemcpyAsync(&last_cnt, cnt + n_pad - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DKC(cudaStreamSynchronize(s));
+  nk = (long long)total + last_cnt;
+  if (nk > 0) {
+    DKC(cudaMallocAsync(&k_in, nk * sizeof(unsigned long long), s));
+    DKC(cudaMallocAsync(&k_out, nk * sizeof(unsigned long long), s));
+    DKC(cudaMallocAsync(&v_in, nk * sizeof(double), s));
+    DKC(cudaMallocAsync(&v_out, nk * sizeof(double), s));
+    if (am) k_coarse_emit<true><<<grid, kThreads, 0, s>>>(A, lab, n_pad, d, off, k_in, v_in);
+    else k_coarse_emit<false><<<grid, kThreads, 0, s>>>(A, lab, n_pad, d, off, k_in, v_in);
+    DKC(cudaGetLastError());
+    const int nbits = bits_for((unsigned long long)d * (unsigned long long)d);
+    DKC(cub::DeviceRadixSort::SortPairs(nullptr, need, k_in, k_out, v_in, v_out, (int)nk, 0, nbits,
+                                        s));
+    if (need > tmp_bytes) {
+      DKC(cudaFreeAsync(tmp, s));
+      DKC(cudaMallocAsync(&tmp, need, s));
+      tmp_bytes = need;
+    }
+    DKC(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in, v_out, (int)nk, 0, nbits,
+                                        s));
+    k_coarse_reduce<<<grid, kThreads, 0, s>>>(k_out, v_out, nk, d, E, ld);
+    DKC(cudaGetLastError());
+  }
+  DKC(cudaStreamSynchronize(s));
+fail:
+  cudaFreeAsync(cnt, s);
+  cudaFreeAsync(off, s);
+  cudaFreeAsync(sdiag, s);
+  if (tmp) cudaFreeAsync(tmp, s);
+  if (k_in) cudaFreeAsync(k_in, s);
+  if (k_out) cudaFreeAsync(k_out, s);
+  if (v_in) cudaFreeAsync(v_in, s);
+  if (v_out) cudaFreeAsync(v_out, s);
+  cudaStreamSynchronize(s);
+  return (int)err;
+#undef DKC
+}
+
+// ======================================================================================
+// Dense LU with partial pivoting (right-looking, panel width kNB), row-major, then the
+// explicit inverse Einv = U^-1 L^-1 P by two blocked triangular solves on P.
+// ======================================================================================
+constexpr int kNB = 32;
+
+// Unblocked panel factorisation of columns [k, k+nb) over rows [k, d) by one block.
+// Pivot = first row of maximal |a| (LAPACK idamax); zero pivot columns are left unscaled
+// (LAPACK dgetf2 semantics; singularity is reported from min |U_kk| afterwards).
+__global__ void __launch_bounds__(1024) k_panel(double* __restrict__ E, int d, int ld, int k,
+                                                int nb, int* __restrict__ piv) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ double prow[kNB];
+  __shared__ int s_p;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int c = k; c < k + nb; ++c) {
+    double best = -1.0;
+    int bi = d;
+    for (int r = c + t; r < d; r += blockDim.x) {
+      const double a = fabs(E[(long long)r * ld + c]);
+      if (a > best) {
+        best = a;
+        bi = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      sv[warp] = best;
+      si[warp] = bi;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double b = -1.0;
+      int i = d;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (sv[w] > b || (sv[w] == b && si[w] < i)) {
+          b = sv[w];
+          i = si[w];
+        }
+      if (i >= d) i = c;
+      piv[c] = i;
+      s_p = i;
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != c) {  // swap rows c and p inside the panel
+      for (int cc = k + t; cc < k + nb; cc += blockDim.x) {
+        const double a = E[(long long)c * ld + cc];
+        E[(long long)c * ld + cc] = E[(long long)p * ld + cc];
+        E[(long long)p * ld + cc] = a;
+      }
+    }
+    __syncthreads();
+    if (t < nb) prow[t] = E[(long long)c * ld + k + t];
+    __syncthreads();
+    const double pv = prow[c - k];
+    if (pv != 0.0) {
+      for (int r = c + 1 + t; r < d; r += blockDim.x) {
+        double* row = E + (long long)r * ld;
+        const double l = row[c] / pv;
+        row[c] = l;
+        for (int cc = c + 1; cc < k + nb; ++cc) row[cc] = fma(-l, prow[cc - k], row[cc]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Apply the row interchanges piv[k0 .. k1) in order to columns outside [skip0, skip1).
+__global__ void k_laswp(double* __restrict__ E, int ncols, int ld, const int* __restrict__ piv,
+                        int k0, int k1, int skip0, int skip1) {
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < ncols;
+       col += gridDim.x * blockDim.x) {
+    if (col >= skip0 && col < skip1) continue;
+    for (int c = k0; c < k1; ++c) {
+      const int p = piv[c];
+      if (p != c) {
+        const double a = E[(long long)c * ld + col];
+        E[(long long)c * ld + col] = E[(long long)p * ld + col];
+        E[(long long)p * ld + col] = a;
+      }
+    }
+  }
+}
+
+// X[k..k+nb, col] <- T^-1 X[k..k+nb, col] for columns [c0, c1), T = E[k..k+nb, k..k+nb]
+// (UNIT lower, or upper with its diagonal).  One thread per column.
+template <bool UPPER>
+__global__ void __launch_bounds__(256) k_trsm_block(const double* __restrict__ T, int ldt, int k,
+                                                    int nb, double* __restrict__ X, int ldx,
+                                                    int c0, int c1) {
+  __shared__ double sT[kNB * kNB];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x)
+    sT[e] = T[(long long)(k + e / nb) * ldt + k + e % nb];
+  __syncthreads();
+  for (int col = c0 + blockIdx.x * blockDim.x + threadIdx.x; col < c1;
+       col += gridDim.x * blockDim.x) {
+    double x[kNB];
+#pragma unroll
+    for (int i = 0; i < kNB; ++i)
+      if (i < nb) x[i] = X[(long long)(k + i) * ldx + col];
+    if (!UPPER) {
+#pragma unroll
+      for (int i = 0; i < kNB; ++i) {
+        if (i < nb) {
+#pragma unroll
+          for (int l = 0; l < i; ++l) x[i] = fma(-sT[i * nb + l], x[l], x[i]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = kNB - 1; i >= 0; --i) {
+        if (i < nb) {
+#pragma unroll
+          for (int l = i + 1; l < kNB; ++l)
+            if (l < nb) x[i] = fma(-sT[i * nb + l], x[l], x[i]);
+          x[i] = x[i] / sT[i * nb + i];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kNB; ++i)
+      if (i < nb) X[(long long)(k + i) * ldx + col] = x[i];
+  }
+}
+
+// C[M x N] -= A[M x K] * B[K x N] (row-major, fp64 DFMA), 64x64 tiles, 4x4 per thread.
+constexpr int kGT = 64, kGK = 16;
+__global__ void __launch_bounds__(256) k_dgemm_sub(const double* __restrict__ Am, int lda,
+                                                   const double* __restrict__ Bm, int ldb,
+                                                   double* __restrict__ C, int ldc, int M, int N,
+                                                   int K) {
+  __shared__ double sA[kGK][kGT + 1];
+  __shared__ double sB[kGK][kGT];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int r0 = blockIdx.y * kGT, c0 = blockIdx.x * kGT;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int kk = 0; kk < K; kk += kGK) {
+    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
+      const int r = e / kGK, c = e % kGK;  // A tile: 64 rows x 16 k
+      const int gr = r0 + r, gk = kk + c;
+      sA[c][r] = (gr < M && gk < K) ? Am[(long long)gr * lda + gk] : 0.0;
+      const int br = e / kGT, bc = e % kGT;  // B tile: 16 k x 64 cols
+      const int gbk = kk + br, gc = c0 + bc;
+      sB[br][bc] = (gbk < K && gc < N) ? Bm[(long long)gbk * ldb + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kGK; ++q) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sA[q][ty * 4 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = sB[q][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int gr = r0 + ty * 4 + a;
+    if (gr >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int gc = c0 + tx + 16 * b;
+      if (gc < N) C[(long long)gr * ldc + gc] -= acc[a][b];
+    }
+  }
+}
+
+static void dgemm_sub(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+                      int M, int N, int K, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT);
+  k_dgemm_sub<<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
+}
+
+__global__ void k_min_pivot(const double* __restrict__ E, int d, int ld, double* out) {
+  __shared__ double red[32];
+  double m = INFINITY;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) m = fmin(m, fabs(E[(long long)i * ld + i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmin(r, red[w]);
+    *out = r;
+  }
+}
+
+__global__ void k_identity(double* __restrict__ X, int d, int ld) {
+  const long long tot = (long long)d * ld;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / ld, c = e % ld;
+    X[e] = (r == c && c < d) ? 1.0 : 0.0;
+  }
+}
+
+// Column diagonal dominance |E_cc| >= sum_{r != c} |E_rc| for every column: partial pivoting
+// then never interchanges rows (the property survives elimination, Golub & Van Loan 3.4.3),
+// so the pivot-free blocked LU below is exactly the partially pivoted factorisation.
+// E = Z^T A Z of a TPFA operator is symmetric and diagonally dominant.
+__global__ void k_col_dominance(const double* __restrict__ E, int d, int ld, int* flag) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x) {
+    double off = 0.0;
+    for (int r = 0; r < d; ++r)
+      if (r != c) off += fabs(E[(long long)r * ld + c]);
+    if (!(fabs(E[(long long)c * ld + c]) >= off)) atomicExch(flag, 0);
+  }
+}
+
+// Unpivoted LU of the nb x nb diagonal block at (k, k), in shared memory, one block.
+__global__ void __launch_bounds__(256) k_diag_lu(double* __restrict__ E, int ld, int k, int nb,
+                                                 int* __restrict__ piv) {
+  __shared__ double a[kNB][kNB + 1];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x)
+    a[e / nb][e % nb] = E[(long long)(k + e / nb) * ld + k + e % nb];
+  __syncthreads();
+  for (int c = 0; c < nb; ++c) {
+    const double p = a[c][c];
+    for (int e = threadIdx.x; e < (nb - c - 1) * (nb - c); e += blockDim.x) {
+      const int r = c + 1 + e / (nb - c);
+      const int cc = c + e % (nb - c);
+      if (cc == c) continue;
+      const double l = (p != 0.0) ? a[r][c] / p : a[r][c];
+      a[r][cc] = fma(-l, a[c][cc], a[r][cc]);
+    }
+    __syncthreads();
+    if (p != 0.0)
+      for (int r = c + 1 + threadIdx.x; r < nb; r += blockDim.x) a[r][c] = a[r][c] / p;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x)
+    E[(long long)(k + e / nb) * ld + k + e % nb] = a[e / nb][e % nb];
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) piv[k + c] = k + c;
+}
+
+// L21 = A21 U11^-1 (rows [k+nb, d)), one thread per row.
+__global__ void __launch_bounds__(256) k_trsm_rows(double* __restrict__ E, int d, int ld, int k,
+                                                   int nb) {
+  __shared__ double sU[kNB * kNB];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x)
+    sU[e] = E[(long long)(k + e / nb) * ld + k + e % nb];
+  __syncthreads();
+  for (int r = k + nb + blockIdx.x * blockDim.x + threadIdx.x; r < d;
+       r += gridDim.x * blockDim.x) {
+    double* row = E + (long long)r * ld + k;
+    double x[kNB];
+#pragma unroll
+    for (int j = 0; j < kNB; ++j)
+      if (j < nb) x[j] = row[j];
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+      if (j < nb) {
+#pragma unroll
+        for (int l = 0; l < j; ++l) x[j] = fma(-x[l], sU[l * nb + j], x[j]);
+        const double u = sU[j * nb + j];
+        if (u != 0.0) x[j] = x[j] / u;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kNB; ++j)
+      if (j < nb) row[j] = x[j];
+  }
+}
+
+int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min_pivot,
+                   float* ms_lu, float* ms_inv, cudaStream_t s) {
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventRecord(e0, s);
+  const unsigned cgrid = (unsigned)((d + 255) / 256);
+  int* dflag = nullptr;
+  int dominant = 1;
+  cudaMallocAsync(&dflag, sizeof(int), s);
+  cudaMemcpyAsync(dflag, &dominant, sizeof(int), cudaMemcpyHostToDevice, s);
+  k_col_dominance<<<cgrid, 256, 0, s>>>(E, d, ld, dflag);
+  cudaMemcpyAsync(&dominant, dflag, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFreeAsync(dflag, s);
+  for (int k = 0; k < d; k += kNB) {
+    const int nb = (d - k < kNB) ? d - k : kNB;
+    const int rest = d - k - nb;
+    if (dominant) {
+      k_diag_lu<<<1, 256, 0, s>>>(E, ld, k, nb, piv);
+      if (rest > 0) k_trsm_rows<<<(rest + 255) / 256, 256, 0, s>>>(E, d, ld, k, nb);
+    } else {
+      k_panel<<<1, 1024, 0, s>>>(E, d, ld, k, nb, piv);
+      k_laswp<<<cgrid, 256, 0, s>>>(E, d, ld, piv, k, k + nb, k, k + nb);
+    }
+    if (rest > 0) {
+      k_trsm_block<false><<<(rest + 255) / 256, 256, 0, s>>>(E, ld, k, nb, E, ld, k + nb, d);
+      dgemm_sub(E + (long long)(k + nb) * ld + k, ld, E + (long long)k * ld + k + nb, ld,
+                E + (long long)(k + nb) * ld + k + nb, ld, rest, rest, nb, s);
+    }
+  }
+  double* dmin = nullptr;
+  cudaMallocAsync(&dmin, sizeof(double), s);
+  k_min_pivot<<<1, 1024, 0, s>>>(E, d, ld, dmin);
+  cudaMemcpyAsync(min_pivot, dmin, sizeof(double), cudaMemcpyDeviceToHost, s);
+  cudaEventRecord(e1, s);
+  cudaStreamSynchronize(s);
+  cudaFreeAsync(dmin, s);
+  if (!(*min_pivot >= 1e-300)) {  // singular (or NaN): no inverse
+    cudaEventElapsedTime(ms_lu, e0, e1);
+    *ms_inv = 0.f;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    return (int)cudaGetLastError();
+  }
+  // Einv = U^-1 L^-1 P I
+  k_identity<<<148 * 8, 256, 0, s>>>(Einv, d, ld);
+  k_laswp<<<cgrid, 256, 0, s>>>(Einv, d, ld, piv, 0, d, 0, 0);
+  for (int k = 0; k < d; k += kNB) {  // L Y = P
+    const int nb = (d - k < kNB) ? d - k : kNB;
+    k_trsm_block<false><<<cgrid, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, d);
+    const int rest = d - k - nb;
+    if (rest > 0)
+      dgemm_sub(E + (long long)(k + nb) * ld + k, ld, Einv + (long long)k * ld, ld,
+                Einv + (long long)(k + nb) * ld, ld, rest, d, nb, s);
+  }
+  const int last = ((d - 1) / kNB) * kNB;
+  for (int k = last; k >= 0; k -= kNB) {  // U X = Y
+    const int nb = (d - k < kNB) ? d - k : kNB;
+    k_trsm_block<true><<<cgrid, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, d);
+    if (k > 0)
+      dgemm_sub(E + k, ld, Einv + (long long)k * ld, ld, Einv, ld, k, d, nb, s);
+  }
+  cudaEventRecord(e2, s);
+  cudaStreamSynchronize(s);
+  cudaEventElapsedTime(ms_lu, e0, e1);
+  cudaEventElapsedTime(ms_inv, e1, e2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace dk

@@ -1,0 +1,122 @@
+// dk_internal.cuh — shared device-side definitions for the deflated-GMRES hot path.
+//
+// HBM layout:
+//   * every length-n vector is stored "guarded": [guard zeros | n_pad cells | guard zeros],
+//     n_pad = n rounded up to kTile, guard = max |stencil offset| rounded up to 256, so the
+//     7-point stencil reads v[i + off] without bounds checks (the DIA coefficient is 0 there);
+//   * the Krylov basis V is (m+1) rows of stride n_pad + guard sharing the zero guards;
+//   * A is DIA: ndiag (<= 7) rows of n_pad fp64 coefficients, offsets ascending (CSR column
+//     order, so row sums are formed in the same order as scipy's csr_matvec);
+//   * labels (deflation column per cell, -1 = none) are int32, guarded with -1.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/dk.h"
+
+namespace dk {
+
+constexpr int kThreads = 256;        // threads per streaming block
+constexpr int kTile = 2048;          // cells per stencil/restriction tile (8 per thread)
+constexpr int kChunk = 2048;         // cells per Gram-Schmidt chunk (8 per thread)
+constexpr int kMaxDiag = DK_MAX_DIAGONALS;
+constexpr int kWarps = kThreads / 32;
+
+struct Dia {
+  int ndiag;
+  int center;                // index of offset 0, or -1
+  long long off[kMaxDiag];   // ascending
+  const double* dia;         // ndiag rows of stride ld (unguarded)
+  long long ld;
+  const double* inv;         // guarded Jacobi inverse diagonal, nullptr = identity
+};
+
+// Scalar state of one solve; lives in device memory and is owned by the single-thread
+// "control" sections (last block of a reduction kernel, cycle-end kernel).
+struct State {
+  int running;     // solve not finished: gates the restart kernels
+  int cycle_open;  // the current cycle passed its restart test: gates the cycle end
+  int active;      // inner iterations of the current cycle still to run: gates the Arnoldi kernels
+  int reorth;      // current iteration needs a second Gram-Schmidt pass
+  int iterations;
+  int cycle;
+  int converged;
+  int warning;
+  int cols;
+  int last_cols;
+  int denom_set;
+  int has_prev;
+  int reorths;
+  int xupdate;     // cycle end produced an x update (gates k_xupdate)
+  int cycle_cols;  // columns of the last cycle before the dependent-column drop
+  int last_broke;  // the last iteration ended its cycle by convergence or breakdown
+  int m, max_iters, min_iters;
+  double tol, denom, beta, prev_beta, wnorm0;
+  unsigned int ticket[4];
+};
+
+struct Scal {
+  State* st;
+  double* sigma;   // [m+1]  1 / ||u_i||: V_i = sigma_i * u_i (lazy normalisation)
+  double* coef;    // [m+1]  Gram-Schmidt / x-update coefficients for the stored u_i
+  double* corr;    // [m+1]  re-orthogonalisation coefficients (stored-u scale)
+  double* H;       // [(m+1) m] pristine Hessenberg, column-major (column j contiguous)
+  double* R;       // [(m+1) m] Givens-rotated triangle, column-major
+  double* cs;      // [m]
+  double* sn;      // [m]
+  double* g;       // [m+1]
+  double* y;       // [m+1]
+  double* hist;    // [max_iters+1]
+  int* restart_of; // [max_iters+1]
+  int m;
+};
+
+// ---- small device helpers -------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double2 ld2cg(const double* p) {
+  return __ldcg(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ void st2(double* p, double2 v) {
+  *reinterpret_cast<double2*>(p) = v;
+}
+
+// Every block calls this after writing its partials; returns true in exactly one block
+// (the last to finish), which may then read all partials.  Resets the ticket.
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+  return s_last != 0;
+}
+
+// Deterministic reduction of q quantities laid out [q][G] by the calling block (one warp
+// per quantity, lanes stride, fixed xor tree).  Result to out[q] (shared or global).
+__device__ __forceinline__ void reduce_partials(const double* part, int nq, int G, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < nq; q += nw) {
+    double s = 0.0;
+    for (int b = lane; b < G; b += 32) s += __ldcg(part + (size_t)q * G + b);
+    s = warp_sum(s);
+    if (lane == 0) out[q] = s;
+  }
+  __syncthreads();
+}
+
+}  // namespace dk

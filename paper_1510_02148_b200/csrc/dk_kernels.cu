@@ -1,0 +1,758 @@
+// dk_kernels.cu — streaming sm_100a kernels of one deflated-GMRES iteration.
+//
+// Per inner iteration j (deflated), DESIGN.md §4:
+//   K1 k_stencil        w = A M^-1 v_j (DIA, Jacobi fused) + per-run sums of w  (Z^T w, part 1)
+//   K2 k_restrict_final s = Z^T w, one warp per column, fixed order              (part 2)
+//   K3 k_gemv           y = E^-1 s                                  (dk_coarse.cu)
+//   K4 k_project        w -= A Z y (<= 7-label gather), h = V^T w, ||w||  -> Hessenberg column
+//   K5 k_gs             u = w - V h, ||u||, corr = V^T u  -> selective re-orthogonalisation test,
+//                       Givens update, convergence test (last block)
+//   K6 k_gs<reorth>     u -= V corr, ||u||  (only when the test fired)
+// Reference semantics: _run_cycles, krylov.py:107-236.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "dk_launch.h"
+
+namespace dk {
+
+// ======================================================================================
+// Segmented (run-wise) restriction of one kTile tile held in shared memory.
+// A run is a maximal range of equal labels in linear cell order; every tile start is a
+// run head.  Each run's sum is written to out[run index within the tile].  The summation
+// order is fixed (serial within a thread, fixed Hillis-Steele tree across threads), so the
+// result is bitwise deterministic.
+// ======================================================================================
+__device__ void tile_restrict(const double* sw, const int* sl, double* out) {
+  __shared__ int wf[kWarps];
+  __shared__ double ws[kWarps];
+  __shared__ int wc[kWarps];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int c0 = 8 * t;
+  double val[8];
+  int lb[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    val[e] = sw[c0 + e];
+    lb[e] = sl[c0 + e];
+  }
+  const int prev = (c0 == 0) ? INT_MIN : sl[c0 - 1];
+  const int next = (c0 + 8 < kTile) ? sl[c0 + 8] : INT_MIN;
+  unsigned heads = 0;
+  int nh = 0;
+  double tail = 0.0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int p = e ? lb[e - 1] : prev;
+    if (c0 + e == 0 || lb[e] != p) {
+      heads |= 1u << e;
+      ++nh;
+      tail = 0.0;
+    }
+    tail = __dadd_rn(tail, val[e]);
+  }
+  // warp inclusive segmented scan of (flag, sum) and plain scan of head counts
+  int f = nh > 0;
+  double s = tail;
+  int c = nh;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int fu = __shfl_up_sync(0xffffffffu, f, d);
+    const double su = __shfl_up_sync(0xffffffffu, s, d);
+    const int cu = __shfl_up_sync(0xffffffffu, c, d);
+    if (lane >= d) {
+      if (!f) s = __dadd_rn(su, s);
+      f = f | fu;
+      c += cu;
+    }
+  }
+  if (lane == 31) {
+    wf[warp] = f;
+    ws[warp] = s;
+    wc[warp] = c;
+  }
+  int fe = __shfl_up_sync(0xffffffffu, f, 1);
+  double se = __shfl_up_sync(0xffffffffu, s, 1);
+  int ce = __shfl_up_sync(0xffffffffu, c, 1);
+  if (lane == 0) {
+    fe = 0;
+    se = 0.0;
+    ce = 0;
+  }
+  __syncthreads();
+  double ps = 0.0;
+  int pc = 0;
+  for (int w = 0; w < warp; ++w) {
+    ps = wf[w] ? ws[w] : __dadd_rn(ps, ws[w]);
+    pc += wc[w];
+  }
+  double run = fe ? se : __dadd_rn(ps, se);
+  int ridx = pc + ce - 1;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (heads & (1u << e)) {
+      run = 0.0;
+      ++ridx;
+    }
+    run = __dadd_rn(run, val[e]);
+    const bool is_tail = (e < 7) ? ((heads >> (e + 1)) & 1u) != 0
+                                 : (c0 + 8 >= kTile || next != lb[7]);
+    if (is_tail) out[ridx] = run;
+  }
+}
+
+// ======================================================================================
+// K1: DIA stencil with fused scale / Jacobi / residual, optional run restriction.
+// Row sums are accumulated in ascending-offset (= CSR column) order with separately
+// rounded multiply and add, i.e. exactly scipy's csr_matvec arithmetic (sparse.py:106).
+// ======================================================================================
+template <int MODE, bool PRE, bool RESTRICT, bool WRITE>
+__global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __restrict__ v,
+                                                      const double* __restrict__ scale,
+                                                      const double* __restrict__ b,
+                                                      double* __restrict__ out,
+                                                      const int* __restrict__ lab,
+                                                      const int* __restrict__ tile_run_off,
+                                                      double* __restrict__ run_part,
+                                                      const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  __shared__ double sw[RESTRICT ? kTile : 2];
+  __shared__ int sl[RESTRICT ? kTile : 2];
+  const long long base = (long long)blockIdx.x * kTile;
+  const bool has_scale = (MODE == ST_APPLY) && scale != nullptr;
+  const double sc = has_scale ? *scale : 1.0;
+#pragma unroll 2
+  for (int k = 0; k < 4; ++k) {
+    const int loc = 2 * threadIdx.x + 512 * k;
+    const long long i = base + loc;
+    double r0 = 0.0, r1 = 0.0;
+    if (MODE == ST_IDENT) {
+      const double2 x = ld2(v + i);
+      r0 = x.x;
+      r1 = x.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kMaxDiag; ++q) {
+        if (q < A.ndiag) {
+          const long long o = A.off[q];
+          const double2 a = ld2(A.dia + q * A.ld + i);
+          double x0 = __ldg(v + i + o);
+          double x1 = __ldg(v + i + o + 1);
+          if (has_scale) {
+            x0 = __dmul_rn(x0, sc);
+            x1 = __dmul_rn(x1, sc);
+          }
+          if (PRE) {
+            x0 = __dmul_rn(x0, __ldg(A.inv + i + o));
+            x1 = __dmul_rn(x1, __ldg(A.inv + i + o + 1));
+          }
+          r0 = __dadd_rn(r0, __dmul_rn(a.x, x0));
+          r1 = __dadd_rn(r1, __dmul_rn(a.y, x1));
+        }
+      }
+      if (MODE == ST_RESID) {
+        const double2 bb = ld2(b + i);
+        r0 = __dsub_rn(bb.x, r0);
+        r1 = __dsub_rn(bb.y, r1);
+      }
+    }
+    if (WRITE) st2(out + i, make_double2(r0, r1));
+    if (RESTRICT) {
+      sw[loc] = r0;
+      sw[loc + 1] = r1;
+      const int2 l = *reinterpret_cast<const int2*>(lab + i);
+      sl[loc] = l.x;
+      sl[loc + 1] = l.y;
+    }
+  }
+  if (RESTRICT) {
+    __syncthreads();
+    tile_restrict(sw, sl, run_part + tile_run_off[blockIdx.x]);
+  }
+}
+
+template <int MODE, bool PRE, bool R, bool W>
+static void stencil_t(const Dia& A, long long n_pad, const double* v, const double* scale,
+                      const double* b, double* out, const RunMap* rm, const int* gate,
+                      cudaStream_t s) {
+  const unsigned grid = (unsigned)(n_pad / kTile);
+  k_stencil<MODE, PRE, R, W><<<grid, kThreads, 0, s>>>(
+      A, v, scale, b, out, rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
+      rm ? rm->run_part : nullptr, gate);
+}
+
+template <int MODE, bool PRE>
+static void stencil_rw(bool write, const Dia& A, long long n_pad, const double* v,
+                       const double* scale, const double* b, double* out, const RunMap* rm,
+                       const int* gate, cudaStream_t s) {
+  if (rm) {
+    if (write) stencil_t<MODE, PRE, true, true>(A, n_pad, v, scale, b, out, rm, gate, s);
+    else stencil_t<MODE, PRE, true, false>(A, n_pad, v, scale, b, out, rm, gate, s);
+  } else {
+    stencil_t<MODE, PRE, false, true>(A, n_pad, v, scale, b, out, rm, gate, s);
+  }
+}
+
+void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
+                    const double* scale, const double* b, double* out, const RunMap* rm,
+                    const int* gate, cudaStream_t s) {
+  if (mode == ST_IDENT) {
+    stencil_rw<ST_IDENT, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
+  } else if (mode == ST_RESID) {
+    stencil_rw<ST_RESID, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
+  } else if (pre) {
+    stencil_rw<ST_APPLY, true>(write, A, n_pad, v, scale, b, out, rm, gate, s);
+  } else {
+    stencil_rw<ST_APPLY, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
+  }
+}
+
+// ======================================================================================
+// K2: per-column sum of run partials (one warp per deflation column, fixed order).
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __restrict__ run_part,
+                                                             const int* __restrict__ ptr,
+                                                             const int* __restrict__ runs, int d,
+                                                             double* __restrict__ s,
+                                                             const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  const int L = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (L >= d) return;
+  double acc = 0.0;
+  const int lo = ptr[L], hi = ptr[L + 1];
+  for (int k = lo + lane; k < hi; k += 32) acc += __ldcg(run_part + runs[k]);
+  acc = warp_sum(acc);
+  if (lane == 0) s[L] = acc;
+}
+
+void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s) {
+  if (rm.d <= 0) return;
+  const long long threads = (long long)rm.d * 32;
+  const unsigned grid = (unsigned)((threads + kThreads - 1) / kThreads);
+  k_restrict_final<<<grid, kThreads, 0, s>>>(rm.run_part, rm.lab_run_ptr, rm.lab_runs, rm.d, s_out,
+                                             gate);
+}
+
+// ======================================================================================
+// Control sections (single thread).  These restate _run_cycles' scalar logic
+// (krylov.py:127-212) on the device so nothing round-trips to the host per iteration.
+// ======================================================================================
+__device__ void restart_done(const Scal& sc, double norm2) {
+  State* st = sc.st;
+  const double beta = sqrt(norm2);
+  st->beta = beta;
+  st->xupdate = 0;
+  st->cycle_open = 0;
+  st->active = 0;
+  st->reorth = 0;
+  if (!st->denom_set) {  // krylov.py:132-136
+    st->denom = beta > 0.0 ? beta : 1.0;
+    st->denom_set = 1;
+    sc.hist[0] = beta;
+    sc.restart_of[0] = 0;
+  }
+  // krylov.py:137-139
+  if (beta == 0.0 || (beta <= st->tol * st->denom && st->iterations >= st->min_iters)) {
+    st->converged = 1;
+    st->running = 0;
+    return;
+  }
+  // krylov.py:140-141: breakdown with no progress
+  if (st->has_prev && beta >= st->prev_beta * (1.0 - 1e-14) && st->warning) {
+    st->running = 0;
+    return;
+  }
+  st->prev_beta = beta;
+  st->has_prev = 1;
+  const int m = sc.m;
+  for (int i = 0; i <= m; ++i) sc.g[i] = 0.0;
+  sc.g[0] = beta;
+  sc.sigma[0] = 1.0 / beta;  // V[0] = r / beta  (krylov.py:145)
+  for (int i = 0; i < (m + 1) * m; ++i) {
+    sc.H[i] = 0.0;
+    sc.R[i] = 0.0;
+  }
+  st->cols = 0;
+  st->cycle_open = 1;
+  st->active = (st->iterations < st->max_iters) ? 1 : 0;  // krylov.py:157-158
+}
+
+__device__ void finish_iteration(const Scal& sc, int j, double hj1) {
+  State* st = sc.st;
+  const int m = sc.m;
+  double* Hc = sc.H + (size_t)j * (m + 1);
+  double* Rc = sc.R + (size_t)j * (m + 1);
+  Hc[j + 1] = hj1;  // krylov.py:172
+  for (int i = 0; i <= j + 1; ++i) Rc[i] = Hc[i];
+  // _givens_update, krylov.py:90-104 (separately rounded products, as Python floats)
+  for (int i = 0; i < j; ++i) {
+    const double t = __dadd_rn(__dmul_rn(sc.cs[i], Rc[i]), __dmul_rn(sc.sn[i], Rc[i + 1]));
+    Rc[i + 1] = __dadd_rn(__dmul_rn(-sc.sn[i], Rc[i]), __dmul_rn(sc.cs[i], Rc[i + 1]));
+    Rc[i] = t;
+  }
+  const double den = hypot(Rc[j], Rc[j + 1]);
+  if (den == 0.0) {
+    sc.cs[j] = 1.0;
+    sc.sn[j] = 0.0;
+  } else {
+    sc.cs[j] = Rc[j] / den;
+    sc.sn[j] = Rc[j + 1] / den;
+  }
+  Rc[j] = den;
+  Rc[j + 1] = 0.0;
+  sc.g[j + 1] = __dmul_rn(-sc.sn[j], sc.g[j]);
+  sc.g[j] = __dmul_rn(sc.cs[j], sc.g[j]);
+  st->cols = j + 1;
+  const double resnorm = fabs(sc.g[j + 1]);
+  st->iterations += 1;
+  sc.hist[st->iterations] = resnorm;
+  sc.restart_of[st->iterations] = st->cycle;
+  double hn = 0.0;
+  for (int i = 0; i <= j + 1; ++i) hn += Hc[i] * Hc[i];
+  hn = sqrt(hn);
+  st->reorth = 0;
+  if (resnorm <= st->tol * st->denom && st->iterations >= st->min_iters) {  // :189-191
+    st->converged = 1;
+    st->active = 0;
+    st->last_broke = 1;
+  } else if (hj1 <= 1e-13 * fmax(1.0, hn)) {  // :192-194
+    st->warning = DK_WARNING_BREAKDOWN;
+    st->active = 0;
+    st->last_broke = 1;
+  } else {
+    st->last_broke = 0;
+    sc.sigma[j + 1] = 1.0 / hj1;  // V[j+1] = w / hj1 (:197)
+    if (j + 1 >= m || st->iterations >= st->max_iters) st->active = 0;
+  }
+}
+
+// ======================================================================================
+// K4: prolongation + subtraction, multi-dot and norm.
+// ======================================================================================
+template <bool AM>
+__device__ __forceinline__ double prolong_cell(const Dia& A, const int* __restrict__ lab,
+                                               const double* __restrict__ yc, long long c) {
+  double t = 0.0;
+#pragma unroll
+  for (int q = 0; q < kMaxDiag; ++q) {
+    if (q < A.ndiag) {
+      const long long o = A.off[q];
+      const int L = __ldg(lab + c + o);
+      if (L >= 0) {
+        double a = __ldg(A.dia + q * A.ld + c);
+        if (AM) a = __dmul_rn(a, __ldg(A.inv + c + o));
+        t = __dadd_rn(t, __dmul_rn(a, __ldg(yc + L)));
+      }
+    }
+  }
+  return t;
+}
+
+template <int MODE, bool DEFL, bool AM>
+__global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restrict__ lab,
+                                                      const double* __restrict__ yc,
+                                                      const double* w_in, double* w_out,
+                                                      const double* __restrict__ V,
+                                                      long long vstride, int nvec, long long n_pad,
+                                                      double* __restrict__ part, int G, Scal sc,
+                                                      int j, const int* __restrict__ gate) {
+  if (*gate == 0) return;
+  extern __shared__ double red[];  // [nq][kWarps]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nq = (MODE == PJ_ITER) ? nvec + 1 : 1;
+  const int nslot = (MODE == PJ_ITER) ? nvec : 0;
+  for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
+  __syncthreads();
+  const long long nchunks = n_pad / kChunk;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long cb = ch * kChunk + 2 * threadIdx.x;
+    double w[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long i = cb + 512 * k;
+      double2 x = ld2(w_in + i);
+      if (DEFL) {
+        x.x = __dsub_rn(x.x, prolong_cell<AM>(A, lab, yc, i));
+        x.y = __dsub_rn(x.y, prolong_cell<AM>(A, lab, yc, i + 1));
+      }
+      w[2 * k] = x.x;
+      w[2 * k + 1] = x.y;
+      if (DEFL || w_out != w_in) st2(w_out + i, x);
+    }
+    if (MODE != PJ_PLAIN) {
+      double nrm = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) nrm = fma(w[e], w[e], nrm);
+      nrm = warp_sum(nrm);
+      if (lane == 0) red[nslot * kWarps + warp] += nrm;
+    }
+    if (MODE == PJ_ITER) {
+#pragma unroll 2
+      for (int v = 0; v < nvec; ++v) {
+        const double* Vr = V + (long long)v * vstride + cb;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 p = ld2(Vr + 512 * k);
+          acc = fma(p.x, w[2 * k], acc);
+          acc = fma(p.y, w[2 * k + 1], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) red[v * kWarps + warp] += acc;
+      }
+    }
+  }
+  if (MODE == PJ_PLAIN) return;
+  __syncthreads();
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) s += red[q * kWarps + w2];
+    part[(size_t)q * G + blockIdx.x] = s;
+  }
+  if (!last_block(&sc.st->ticket[0])) return;
+  reduce_partials(part, nq, G, red);
+  if (threadIdx.x == 0) {
+    if (MODE == PJ_ITER) {
+      State* st = sc.st;
+      double* Hc = sc.H + (size_t)j * (sc.m + 1);
+      for (int v = 0; v < nvec; ++v) {
+        const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
+        Hc[v] = h;
+        sc.coef[v] = h * sc.sigma[v];
+      }
+      st->wnorm0 = sqrt(red[nvec]);  // krylov.py:162
+    } else {
+      restart_done(sc, red[0]);
+    }
+  }
+}
+
+template <int MODE, bool DEFL, bool AM>
+static void project_t(const Dia& A, const int* lab, const double* yc, const double* w_in,
+                      double* w_out, const double* V, long long vstride, int nvec,
+                      long long n_pad, double* part, int G, const Scal& sc, int j,
+                      const int* gate, cudaStream_t s) {
+  const int nq = (MODE == PJ_ITER) ? nvec + 1 : 1;
+  const size_t smem = (size_t)(nq > 1 ? nq : 1) * kWarps * sizeof(double);
+  k_project<MODE, DEFL, AM><<<G, kThreads, smem, s>>>(A, lab, yc, w_in, w_out, V, vstride, nvec,
+                                                      n_pad, part, G, sc, j, gate);
+}
+
+template <int MODE>
+static void project_m(bool defl, bool am, const Dia& A, const int* lab, const double* yc,
+                      const double* w_in, double* w_out, const double* V, long long vstride,
+                      int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
+                      const int* gate, cudaStream_t s) {
+  if (!defl)
+    project_t<MODE, false, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
+                                  j, gate, s);
+  else if (am)
+    project_t<MODE, true, true>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc, j,
+                                gate, s);
+  else
+    project_t<MODE, true, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc, j,
+                                 gate, s);
+}
+
+void launch_project(int mode, bool defl, bool am, const Dia& A, const int* lab, const double* yc,
+                    const double* w_in, double* w_out, const double* V, long long vstride,
+                    int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
+                    const int* gate, cudaStream_t s) {
+  if (mode == PJ_ITER)
+    project_m<PJ_ITER>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc, j,
+                       gate, s);
+  else if (mode == PJ_RESTART)
+    project_m<PJ_RESTART>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
+                          j, gate, s);
+  else
+    project_m<PJ_PLAIN>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
+                        j, gate, s);
+}
+
+// ======================================================================================
+// K5/K6: classical Gram-Schmidt update with the reference's selective
+// re-orthogonalisation test (krylov.py:163-172):
+//   pass 1: u = w - sum_i h_i V_i ; corr = V^T u ; if max|corr| > 1e-8 ||w0||  -> pass 2
+//   pass 2: u -= sum_i corr_i V_i ; H[:j+1, j] += corr
+// The corr dots re-read V_i at the thread's own cells (L2-resident right after pass 1).
+// ======================================================================================
+template <bool REORTH>
+__global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_out,
+                                                 const double* __restrict__ V, long long vstride,
+                                                 int nvec, long long n_pad,
+                                                 double* __restrict__ part, int G, Scal sc, int j,
+                                                 const int* __restrict__ gate) {
+  if (*gate == 0) return;
+  extern __shared__ double sh[];
+  double* cf = sh;                      // [nvec]
+  double* red = sh + nvec;              // [nq][kWarps]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nq = REORTH ? 1 : nvec + 1;
+  const int nslot = REORTH ? 0 : nvec;
+  for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = REORTH ? sc.corr[q] : sc.coef[q];
+  for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
+  __syncthreads();
+  const long long nchunks = n_pad / kChunk;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long cb = ch * kChunk + 2 * threadIdx.x;
+    double u[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 x = REORTH ? ld2cg(w_in + cb + 512 * k) : ld2(w_in + cb + 512 * k);
+      u[2 * k] = x.x;
+      u[2 * k + 1] = x.y;
+    }
+#pragma unroll 2
+    for (int v = 0; v < nvec; ++v) {
+      const double* Vr = V + (long long)v * vstride + cb;
+      const double c = cf[v];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 p = ld2(Vr + 512 * k);
+        u[2 * k] = __dsub_rn(u[2 * k], __dmul_rn(c, p.x));
+        u[2 * k + 1] = __dsub_rn(u[2 * k + 1], __dmul_rn(c, p.y));
+      }
+    }
+    double nrm = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      st2(u_out + cb + 512 * k, make_double2(u[2 * k], u[2 * k + 1]));
+      nrm = fma(u[2 * k], u[2 * k], nrm);
+      nrm = fma(u[2 * k + 1], u[2 * k + 1], nrm);
+    }
+    nrm = warp_sum(nrm);
+    if (lane == 0) red[nslot * kWarps + warp] += nrm;
+    if (!REORTH) {
+#pragma unroll 2
+      for (int v = 0; v < nvec; ++v) {
+        const double* Vr = V + (long long)v * vstride + cb;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 p = ld2(Vr + 512 * k);
+          acc = fma(p.x, u[2 * k], acc);
+          acc = fma(p.y, u[2 * k + 1], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) red[v * kWarps + warp] += acc;
+      }
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) s += red[q * kWarps + w2];
+    part[(size_t)q * G + blockIdx.x] = s;
+  }
+  if (!last_block(&sc.st->ticket[REORTH ? 2 : 1])) return;
+  reduce_partials(part, nq, G, red);
+  if (threadIdx.x == 0) {
+    State* st = sc.st;
+    if (REORTH) {
+      finish_iteration(sc, j, sqrt(red[0]));
+    } else {
+      double mx = 0.0;
+      for (int v = 0; v < nvec; ++v) mx = fmax(mx, fabs(red[v] * sc.sigma[v]));
+      if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
+        double* Hc = sc.H + (size_t)j * (sc.m + 1);
+        for (int v = 0; v < nvec; ++v) {
+          const double cr = red[v] * sc.sigma[v];
+          Hc[v] += cr;  // krylov.py:170
+          sc.corr[v] = cr * sc.sigma[v];
+        }
+        st->reorth = 1;
+        st->reorths += 1;
+      } else {
+        finish_iteration(sc, j, sqrt(red[nvec]));
+      }
+    }
+  }
+}
+
+void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
+               int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
+               const int* gate, cudaStream_t s) {
+  const int nq = reorth ? 1 : nvec + 1;
+  const size_t smem = ((size_t)nvec + (size_t)nq * kWarps) * sizeof(double);
+  if (reorth)
+    k_gs<true><<<G, kThreads, smem, s>>>(w_in, u_out, V, vstride, nvec, n_pad, part, G, sc, j,
+                                         gate);
+  else
+    k_gs<false><<<G, kThreads, smem, s>>>(w_in, u_out, V, vstride, nvec, n_pad, part, G, sc, j,
+                                          gate);
+}
+
+// ======================================================================================
+// Cycle end (krylov.py:199-212): drop dependent trailing columns, y = R^-1 g by column-
+// oriented back substitution, coefficients for x += M^-1 V y.
+// ======================================================================================
+__global__ void k_cycle_end(Scal sc) {
+  State* st = sc.st;
+  if (!st->cycle_open) return;
+  st->cycle_open = 0;
+  st->active = 0;
+  const int m = sc.m;
+  int cols = st->cols;
+  if (cols == 0) {  // krylov.py:199-200
+    st->running = 0;
+    st->last_cols = 0;
+    st->xupdate = 0;
+    return;
+  }
+  st->cycle_cols = cols;
+  const double r00 = fabs(sc.R[0]);
+  while (cols > 1 && fabs(sc.R[(size_t)(cols - 1) * (m + 1) + (cols - 1)]) < 1e-14 * r00) --cols;
+  for (int i = 0; i < cols; ++i) sc.y[i] = sc.g[i];
+  for (int k = cols - 1; k >= 0; --k) {
+    const double* Rk = sc.R + (size_t)k * (m + 1);
+    sc.y[k] = sc.y[k] / Rk[k];
+    for (int i = 0; i < k; ++i) sc.y[i] = __dsub_rn(sc.y[i], __dmul_rn(sc.y[k], Rk[i]));
+  }
+  for (int i = 0; i < cols; ++i) sc.coef[i] = sc.y[i] * sc.sigma[i];
+  st->last_cols = cols;
+  st->xupdate = 1;
+  st->cycle += 1;
+  const bool done = st->converged || st->iterations >= st->max_iters;  // krylov.py:127
+  st->running = done ? 0 : 1;
+}
+
+void launch_cycle_end(const Scal& sc, cudaStream_t s) { k_cycle_end<<<1, 1, 0, s>>>(sc); }
+
+// x += M^-1 (sum_{i<cols} y_i V_i)   (krylov.py:206)
+__global__ void __launch_bounds__(kThreads) k_xupdate(Dia A, double* __restrict__ x,
+                                                      const double* __restrict__ V,
+                                                      long long vstride, long long n_pad,
+                                                      Scal sc) {
+  State* st = sc.st;
+  if (!st->xupdate) return;
+  const int cols = st->last_cols;
+  extern __shared__ double cf[];
+  for (int q = threadIdx.x; q < cols; q += blockDim.x) cf[q] = sc.coef[q];
+  __syncthreads();
+  const long long npair = n_pad / 2;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npair;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long i = 2 * p;
+    double t0 = 0.0, t1 = 0.0;
+    for (int v = 0; v < cols; ++v) {
+      const double2 q = ld2(V + (long long)v * vstride + i);
+      t0 = fma(cf[v], q.x, t0);
+      t1 = fma(cf[v], q.y, t1);
+    }
+    if (A.inv != nullptr) {
+      t0 = __dmul_rn(t0, A.inv[i]);
+      t1 = __dmul_rn(t1, A.inv[i + 1]);
+    }
+    double2 xv = *reinterpret_cast<double2*>(x + i);
+    xv.x = __dadd_rn(xv.x, t0);
+    xv.y = __dadd_rn(xv.y, t1);
+    st2(x + i, xv);
+  }
+}
+
+void launch_xupdate(const Dia& A, double* x, const double* V, long long vstride, long long n_pad,
+                    const Scal& sc, cudaStream_t s) {
+  const size_t smem = (size_t)(sc.m + 1) * sizeof(double);
+  k_xupdate<<<148 * 8, kThreads, smem, s>>>(A, x, V, vstride, n_pad, sc);
+}
+
+// ======================================================================================
+// Elementwise helpers for x* / P2 / reconstruct (deflation.py:61-68,88).
+// ======================================================================================
+__global__ void k_recon(const int* __restrict__ lab, const double* __restrict__ y,
+                        const double* __restrict__ xs, const double* __restrict__ xh,
+                        double* __restrict__ out, long long n_pad, int mode) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int L = lab[i];
+    const double zy = L >= 0 ? y[L] : 0.0;
+    if (mode == 0) out[i] = __dadd_rn(xs[i], __dsub_rn(xh[i], zy));  // x* + (xh - Z y)
+    else if (mode == 1) out[i] = zy;                                  // Z y
+    else out[i] = __dsub_rn(xh[i], zy);                               // v - Z y
+  }
+}
+
+void launch_recon(const int* lab, const double* y, const double* xs, const double* xh, double* out,
+                  long long n_pad, cudaStream_t s) {
+  k_recon<<<148 * 8, kThreads, 0, s>>>(lab, y, xs, xh, out, n_pad, 0);
+}
+void launch_bcast(const int* lab, const double* y, double* out, long long n_pad, cudaStream_t s) {
+  k_recon<<<148 * 8, kThreads, 0, s>>>(lab, y, nullptr, nullptr, out, n_pad, 1);
+}
+void launch_sub_bcast(const int* lab, const double* y, const double* v, double* out,
+                      long long n_pad, cudaStream_t s) {
+  k_recon<<<148 * 8, kThreads, 0, s>>>(lab, y, nullptr, v, out, n_pad, 2);
+}
+
+__global__ void __launch_bounds__(kThreads) k_norm(const double* __restrict__ v, long long n_pad,
+                                                   double* __restrict__ part, int G,
+                                                   unsigned int* ticket, double* dst) {
+  __shared__ double red[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc = 0.0;
+  const long long nchunks = n_pad / kChunk;
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long cb = ch * kChunk + 2 * threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 x = ld2cg(v + cb + 512 * k);
+      acc = fma(x.x, x.x, acc);
+      acc = fma(x.y, x.y, acc);
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kWarps; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+  if (!last_block(ticket)) return;
+  __shared__ double fin[1];
+  reduce_partials(part, 1, G, fin);
+  if (threadIdx.x == 0) *dst = sqrt(fin[0]);
+}
+
+void launch_norm(const double* v, long long n_pad, double* part, int G, unsigned int* ticket,
+                 double* dst, cudaStream_t s) {
+  k_norm<<<G, kThreads, 0, s>>>(v, n_pad, part, G, ticket, dst);
+}
+
+__global__ void k_init_state(Scal sc, double tol, int m, int max_iters, int min_iters) {
+  State* st = sc.st;
+  st->running = 1;
+  st->cycle_open = 0;
+  st->active = 0;
+  st->reorth = 0;
+  st->iterations = 0;
+  st->cycle = 0;
+  st->converged = 0;
+  st->warning = 0;
+  st->cols = 0;
+  st->last_cols = 0;
+  st->denom_set = 0;
+  st->has_prev = 0;
+  st->reorths = 0;
+  st->m = m;
+  st->max_iters = max_iters;
+  st->min_iters = min_iters;
+  st->tol = tol;
+  st->denom = 1.0;
+  st->beta = 0.0;
+  st->prev_beta = 0.0;
+  st->wnorm0 = 0.0;
+  st->xupdate = 0;
+  st->cycle_cols = 0;
+  st->last_broke = 0;
+  for (int i = 0; i < 4; ++i) st->ticket[i] = 0u;
+}
+
+void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min_iters,
+                       cudaStream_t s) {
+  k_init_state<<<1, 1, 0, s>>>(sc, tol, m, max_iters, min_iters);
+}
+
+}  // namespace dk

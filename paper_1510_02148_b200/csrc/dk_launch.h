@@ -1,0 +1,73 @@
+// dk_launch.h — host-side launchers for the device kernels (one per kernel family).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dk_internal.cuh"
+
+namespace dk {
+
+// Stencil modes of launch_stencil.
+enum StencilMode {
+  ST_APPLY = 0,  // out = A (M^-1 (scale * v))          (krylov.py:159 / deflation.py:50-51)
+  ST_RESID = 1,  // out = b - A v                        (krylov.py:128, :222)
+  ST_IDENT = 2,  // out = v  (restriction of v only)     (deflation.py:62 Z^T v)
+};
+
+struct RunMap {            // label-segmented restriction metadata
+  const int* lab;          // guarded labels
+  const int* tile_run_off; // [ntiles+1] first run id of each tile
+  double* run_part;        // [nruns] per-run partial sums
+  const int* lab_run_ptr;  // [d+1] CSR: runs of each label, run order
+  const int* lab_runs;     // [nlabelled runs]
+  int d;
+};
+
+// w = (mode) ; if rm != nullptr also run sums of w.  pre: apply the Jacobi inverse.
+// scale (device scalar or nullptr) multiplies v first.  gate (device int or nullptr).
+void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
+                    const double* scale, const double* b, double* out, const RunMap* rm,
+                    const int* gate, cudaStream_t s);
+// s[L] = sum of run partials of label L, fixed order.
+void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s);
+// y = M x, M d x d row-major with leading dimension ld.
+void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
+                 cudaStream_t s);
+
+enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2 };
+// w_out = w_in - A_p Z y (defl) ; ITER: dots with V_0..V_{nvec-1} and ||w_out||^2 -> H col j;
+// RESTART: ||w_out||^2 -> restart test.  G = grid width (fixed per operator).
+void launch_project(int mode, bool defl, bool am, const Dia& A, const int* lab, const double* yc,
+                    const double* w_in, double* w_out, const double* V, long long vstride,
+                    int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
+                    const int* gate, cudaStream_t s);
+// u = w - sum coef_i u_i (+ corr dots, norm) or the re-orthogonalisation pass.
+void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
+               int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
+               const int* gate, cudaStream_t s);
+void launch_cycle_end(const Scal& sc, cudaStream_t s);
+void launch_xupdate(const Dia& A, double* x, const double* V, long long vstride, long long n_pad,
+                    const Scal& sc, cudaStream_t s);
+// out = xs + (xh - y[lab])   (deflation.py:64-68)
+void launch_recon(const int* lab, const double* y, const double* xs, const double* xh, double* out,
+                  long long n_pad, cudaStream_t s);
+// out = y[lab] (0 where lab < 0)
+void launch_bcast(const int* lab, const double* y, double* out, long long n_pad, cudaStream_t s);
+// out = v - y[lab]
+void launch_sub_bcast(const int* lab, const double* y, const double* v, double* out,
+                      long long n_pad, cudaStream_t s);
+// *dst = ||v||_2 over n_pad cells (deterministic).
+void launch_norm(const double* v, long long n_pad, double* part, int G, unsigned int* ticket,
+                 double* dst, cudaStream_t s);
+void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min_iters,
+                       cudaStream_t s);
+
+// ---- coarse operator (dk_coarse.cu) ----
+// E (d x d, ld) = Z^T A_p Z, deterministic.  Returns 0 or a cuda error code.
+int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const RunMap& rm,
+                 double* E, int ld, double* scratch_q, cudaStream_t s);
+// In-place LU with partial pivoting of E, then Einv = U^-1 L^-1 P.  *min_pivot receives
+// min |U_kk| (host).  Returns 0 or a cuda error code.
+int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min_pivot,
+                   float* ms_lu, float* ms_inv, cudaStream_t s);
+
+}  // namespace dk

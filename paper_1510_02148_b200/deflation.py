@@ -1,0 +1,199 @@
+"""Deflation projectors P1, P2, the coarse matrix E and the coarse solution — on the device.
+
+Reference: defkrylov/deflation.py:19-104.  The basis is an indicator (piecewise-constant)
+basis stored as one int32 column label per cell, never as a dense n x d matrix; E, its LU,
+E^-1 and x* = Z E^-1 Z^T b are built in HBM by dk_defl_create.  A dense Z is accepted when
+every row has at most one nonzero equal to 1 (it is converted to labels); other bases are
+outside the device path and raise UnsupportedOperator.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+
+from . import _lib
+from ._lib import UnsupportedOperator
+from .errors import SingularCoarseMatrix
+from .sparse import SparseMatrix
+
+_DENSE_LIMIT = 1 << 26  # materialise Z / AZ densely only below this many entries
+
+
+class DeflationBasis:
+    """n x d indicator deflation vectors (deflation.py:19-37), stored as column labels."""
+
+    __slots__ = ("labels", "_n", "_d", "_dense")
+
+    def __init__(self, Z=None, *, labels=None, d=None):
+        self._dense = None
+        if labels is not None:
+            lab = np.ascontiguousarray(np.asarray(labels), dtype=np.int32)
+            if lab.ndim != 1:
+                raise ValueError("labels must be a vector")
+            dd = int(d) if d is not None else int(lab.max(initial=-1)) + 1
+            if dd < 1:
+                raise ValueError("Z must be n x d with d >= 1")
+            if lab.min(initial=-1) < -1 or lab.max(initial=-1) >= dd:
+                raise ValueError("labels out of range")
+            self.labels, self._n, self._d = lab, len(lab), dd
+            return
+        Zd = np.asarray(Z, dtype=np.float64)
+        if Zd.ndim != 2 or Zd.shape[1] < 1:
+            raise ValueError("Z must be n x d with d >= 1")
+        self._n, self._d = Zd.shape
+        nz = Zd != 0.0
+        per_row = nz.sum(axis=1)
+        if np.all(per_row <= 1) and np.all(Zd[nz] == 1.0):
+            lab = np.full(self._n, -1, dtype=np.int32)
+            r, c = np.nonzero(nz)
+            lab[r] = c
+            self.labels = lab
+        else:
+            self.labels = None
+            self._dense = np.ascontiguousarray(Zd)
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    @property
+    def d(self) -> int:
+        return self._d
+
+    @property
+    def Z(self) -> np.ndarray:
+        """Dense n x d view (small problems only)."""
+        if self._dense is not None:
+            return self._dense
+        if self._n * self._d > _DENSE_LIMIT:
+            raise MemoryError("dense Z of this basis is too large; use .labels")
+        Z = np.zeros((self._n, self._d))
+        keep = self.labels >= 0
+        Z[np.flatnonzero(keep), self.labels[keep]] = 1.0
+        return Z
+
+    def _require_indicator(self) -> np.ndarray:
+        if self.labels is not None:
+            return self.labels
+        Zd = self._dense
+        # two equal columns make E exactly singular (the reference's LU reports it)
+        cols = {Zd[:, j].tobytes() for j in range(Zd.shape[1])}
+        if len(cols) < Zd.shape[1]:
+            raise SingularCoarseMatrix("zero pivot in LU factorization")
+        raise UnsupportedOperator(
+            "the device path supports indicator bases (at most one unit entry per row)")
+
+
+class DeflationContext:
+    """Frozen projector state resident on the device (deflation.py:40-68)."""
+
+    def __init__(self, basis: DeflationBasis, A: SparseMatrix, M, A_p_choice: str, h, lib):
+        self.basis, self.A, self.M, self.A_p_choice = basis, A, M, A_p_choice
+        self.h, self._lib = h, lib
+        self._fin = weakref.finalize(self, lib.dk_defl_destroy, h)
+
+    def close(self) -> None:
+        self._fin()
+
+    def _check_operator(self, A: SparseMatrix, M) -> None:
+        if A is not self.A:
+            raise ValueError("deflation context was built for a different matrix")
+        if self.A_p_choice == "AM" and (M is not self.M and not (
+                M.kind == "identity" and self.M.kind == "identity")):
+            raise UnsupportedOperator("A_p='AM' needs the solve's preconditioner to be the "
+                                      "context's")
+
+    def _call(self, fn, v) -> np.ndarray:
+        v = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+        if v.shape != (self.A.n,):
+            raise ValueError("vector has wrong length")
+        self.A.device().set_precond(self.M)
+        out = np.empty(self.A.n)
+        _lib.check(fn(self.h, _lib.ptr(v), _lib.ptr(out)))
+        return out
+
+    def apply_p1(self, v) -> np.ndarray:
+        """v - A_p Z E^-1 Z^T v."""
+        return self._call(self._lib.dk_defl_apply_p1, v)
+
+    def apply_p2(self, v) -> np.ndarray:
+        """v - Z E^-1 Z^T A_p v."""
+        return self._call(self._lib.dk_defl_apply_p2, v)
+
+    def reconstruct(self, x_hat) -> np.ndarray:
+        """x* + P2 x^."""
+        return self._call(self._lib.dk_defl_reconstruct, x_hat)
+
+    @property
+    def x_star(self) -> np.ndarray:
+        out = np.empty(self.A.n)
+        _lib.check(self._lib.dk_defl_x_star(self.h, _lib.ptr(out)))
+        return out
+
+    @property
+    def d(self) -> int:
+        return self.basis.d
+
+    def coarse_matrix(self):
+        """(E, E^-1) copied from the device (d x d)."""
+        d = self.basis.d
+        E = np.empty((d, d))
+        Einv = np.empty((d, d))
+        _lib.check(self._lib.dk_defl_coarse(self.h, _lib.ptr(E), _lib.ptr(Einv)))
+        return E, Einv
+
+    def setup_ms(self) -> dict:
+        ms = (C.c_double * 4)()
+        _lib.check(self._lib.dk_defl_setup_ms(self.h, ms))
+        return {"assemble_E": ms[0], "lu": ms[1], "inverse": ms[2], "x_star": ms[3]}
+
+    @property
+    def AZ(self) -> np.ndarray:
+        """Dense A_p Z (small problems only; the device never forms it)."""
+        Z = self.basis.Z
+        if self.A.n * Z.shape[1] > _DENSE_LIMIT:
+            raise MemoryError("dense AZ is too large")
+        cols = [Z[:, j] if self.A_p_choice == "A" else self.M.apply(Z[:, j])
+                for j in range(Z.shape[1])]
+        from .sparse import spmv
+        return np.column_stack([spmv(self.A, c) for c in cols])
+
+
+def build_context(A: SparseMatrix, M, Z: DeflationBasis, b, A_p_choice: str = "A"
+                  ) -> DeflationContext:
+    """Assemble E = Z^T A_p Z on the device, factorise it, form x* (deflation.py:71-89).
+
+    Raises SingularCoarseMatrix when the deflation vectors are dependent.
+    """
+    if A_p_choice not in ("A", "AM"):
+        raise ValueError("A_p_choice must be 'A' or 'AM'")
+    if Z.n != A.n:
+        raise ValueError("deflation basis does not match the matrix dimension")
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    if b.shape != (A.n,):
+        raise ValueError("right-hand side has wrong length")
+    labels = Z._require_indicator()
+    op = A.device()
+    op.set_precond(M)
+    h = C.c_void_p()
+    ap = _lib.DK_AP_AM if A_p_choice == "AM" else _lib.DK_AP_A
+    _lib.check(op._lib.dk_defl_create(C.byref(h), op.h, _lib.ptr(labels), Z.d, ap,
+                                      _lib.ptr(b)), "dk_defl_create")
+    return DeflationContext(Z, A, M, A_p_choice, h, op._lib)
+
+
+def apply_p1(ctx: DeflationContext | None, v) -> np.ndarray:
+    """P1 v; a missing context is the identity."""
+    return v if ctx is None else ctx.apply_p1(v)
+
+
+def apply_p2(ctx: DeflationContext | None, v) -> np.ndarray:
+    """P2 v; a missing context is the identity."""
+    return v if ctx is None else ctx.apply_p2(v)
+
+
+def reconstruct(ctx: DeflationContext | None, x_hat) -> np.ndarray:
+    """x = x* + P2 x^ ; a missing context is the identity."""
+    return x_hat if ctx is None else ctx.reconstruct(x_hat)
