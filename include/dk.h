@@ -76,6 +76,8 @@ const char* dk_last_error(void);
 int dk_version(void);
 /* Number of visible CUDA devices (0 on a CPU-only host, never an error). */
 int dk_device_count(int32_t* count);
+/* Device used by handles created afterwards on the calling thread (one process per GPU). */
+int dk_set_device(int32_t device);
 
 /* ---- operator --------------------------------------------------------------------- */
 /* n cells; ndiag <= 7 diagonals with distinct offsets (any order); diags is ndiag x n

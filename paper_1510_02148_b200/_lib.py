@@ -21,7 +21,7 @@ DK_AP_A, DK_AP_AM = 0, 1
 
 #: every symbol include/dk.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "dk_last_error", "dk_version", "dk_device_count",
+    "dk_last_error", "dk_version", "dk_device_count", "dk_set_device",
     "dk_op_create", "dk_op_destroy", "dk_op_set_precond", "dk_op_set_stream", "dk_op_spmv", "dk_op_profile",
     "dk_op_profile_read",
     "dk_defl_create", "dk_defl_destroy", "dk_defl_apply_p1", "dk_defl_apply_p2",
@@ -61,6 +61,7 @@ def _declare(lib):
         "dk_last_error": (C.c_char_p, []),
         "dk_version": (C.c_int, []),
         "dk_device_count": (C.c_int, [_I32]),
+        "dk_set_device": (C.c_int, [C.c_int32]),
         "dk_op_create": (C.c_int, [C.POINTER(_P), C.c_int64, C.c_int32, _I64, _P, _P]),
         "dk_op_destroy": (C.c_int, [_P]),
         "dk_op_set_precond": (C.c_int, [_P, _P]),

@@ -181,15 +181,17 @@ int ensure_work(dk_op* op, int m, int max_iters) {
     op->v_rows = m + 1;
     op->g_m = -1;  // graph refers to the old basis
   }
-  if (op->part_q < m + 2) {
+  // per-block partials: up to 2(m+1)+1 quantities (dots, Gram column, norm) per launch
+  if (op->part_q < 2 * m + 4) {
     if (op->part) DK_TRY(cudaFree(op->part));
-    DK_TRY(cudaMalloc(&op->part, (size_t)(m + 2) * op->G * sizeof(double)));
-    op->part_q = m + 2;
+    DK_TRY(cudaMalloc(&op->part, (size_t)(2 * m + 4) * op->G * sizeof(double)));
+    op->part_q = 2 * m + 4;
     op->g_m = -1;
   }
   if (op->scal_m < m) {
     if (op->scal) DK_TRY(cudaFree(op->scal));
-    const size_t cnt = 4 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m + (m + 1);
+    const size_t cnt = 5 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
+                       (size_t)(m + 1) * (m + 1);
     DK_TRY(cudaMalloc(&op->scal, cnt * sizeof(double)));
     DK_TRY(cudaMemsetAsync(op->scal, 0, cnt * sizeof(double), op->stream));
     op->scal_m = m;
@@ -217,6 +219,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.R = p; p += (size_t)(m + 1) * m;
   sc.cs = p; p += m;
   sc.sn = p; p += m;
+  sc.Gm = p; p += (size_t)(m + 1) * (m + 1);
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
@@ -310,6 +313,8 @@ void issue_restart(dk_op* op, dk_defl* c) {
                  op->G, op->sc, 0, &st->running, op->stream);
 }
 
+int read_state(dk_op* op);
+
 void issue_iteration(dk_op* op, dk_defl* c, int j) {
   State* st = op->st;
   const bool pre = op->inv != nullptr;
@@ -339,8 +344,15 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
     launch_gs(false, op->w, V + (long long)(j + 1) * op->vstride, V, op->vstride, nvec,
               op->n_pad, op->part, op->G, op->sc, j, &st->active, op->stream);
   }
+  // second Gram-Schmidt pass, gated on the device-side test (krylov.py:167-170)
+  if (op->prof) {
+    if (read_state(op) || !op->st_host->reorth) return;
+  }
   {
-    ProfScope ps(op, PC_REORTH, (16.0 + 8.0 * nvec) * n);
+    ProfScope ps(op, PC_REORTH, (16.0 + 16.0 * nvec) * n);
+    launch_project(PJ_REDOTS, false, false, A, nullptr, nullptr,
+                   V + (long long)(j + 1) * op->vstride, nullptr, V, op->vstride, nvec, op->n_pad,
+                   op->part, op->G, op->sc, j, &st->reorth, op->stream);
     launch_gs(true, V + (long long)(j + 1) * op->vstride, V + (long long)(j + 1) * op->vstride, V,
               op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j, &st->reorth, op->stream);
   }
@@ -406,6 +418,11 @@ int dk_device_count(int32_t* count) {
   if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
   cudaGetLastError();
   *count = c;
+  return DK_OK;
+}
+
+int dk_set_device(int32_t device) {
+  DK_TRY(cudaSetDevice(device));
   return DK_OK;
 }
 
@@ -821,7 +838,7 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, op->stream);
-  const int per_cycle_launches = (c ? 4 : 2) + m * (c ? 6 : 4) + 2;
+  const int per_cycle_launches = (c ? 4 : 2) + m * (c ? 7 : 5) + 2;
   long long guard_cycles = (long long)max_iters + 2;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
     if (!op->prof) {

@@ -66,6 +66,7 @@ struct Scal {
   double* sn;      // [m]
   double* g;       // [m+1]
   double* y;       // [m+1]
+  double* Gm;      // [(m+1)(m+1)] basis Gram matrix V^T V, column j holds rows 0..j
   double* hist;    // [max_iters+1]
   int* restart_of; // [max_iters+1]
   int m;

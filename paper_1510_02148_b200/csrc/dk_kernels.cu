@@ -236,100 +236,129 @@ void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cud
 }
 
 // ======================================================================================
-// Control sections (single thread).  These restate _run_cycles' scalar logic
-// (krylov.py:127-212) on the device so nothing round-trips to the host per iteration.
+// Control sections.  These restate _run_cycles' scalar logic (krylov.py:127-212) on the
+// device so nothing round-trips to the host per iteration.  They run in the last block of a
+// reduction kernel; all threads of that block call them (shared-memory staging), one
+// thread makes the decisions.
 // ======================================================================================
-__device__ void restart_done(const Scal& sc, double norm2) {
+__device__ void restart_done_block(const Scal& sc, double norm2) {
+  __shared__ int s_open;
   State* st = sc.st;
-  const double beta = sqrt(norm2);
-  st->beta = beta;
-  st->xupdate = 0;
-  st->cycle_open = 0;
-  st->active = 0;
-  st->reorth = 0;
-  if (!st->denom_set) {  // krylov.py:132-136
-    st->denom = beta > 0.0 ? beta : 1.0;
-    st->denom_set = 1;
-    sc.hist[0] = beta;
-    sc.restart_of[0] = 0;
+  if (threadIdx.x == 0) {
+    const double beta = sqrt(norm2);
+    st->beta = beta;
+    st->xupdate = 0;
+    st->cycle_open = 0;
+    st->active = 0;
+    st->reorth = 0;
+    s_open = 0;
+    if (!st->denom_set) {  // krylov.py:132-136
+      st->denom = beta > 0.0 ? beta : 1.0;
+      st->denom_set = 1;
+      sc.hist[0] = beta;
+      sc.restart_of[0] = 0;
+    }
+    if (beta == 0.0 || (beta <= st->tol * st->denom && st->iterations >= st->min_iters)) {
+      st->converged = 1;  // krylov.py:137-139
+      st->running = 0;
+    } else if (st->has_prev && beta >= st->prev_beta * (1.0 - 1e-14) && st->warning) {
+      st->running = 0;  // krylov.py:140-141: breakdown with no progress
+    } else {
+      st->prev_beta = beta;
+      st->has_prev = 1;
+      sc.sigma[0] = 1.0 / beta;  // V[0] = r / beta  (krylov.py:145)
+      st->cols = 0;
+      st->cycle_open = 1;
+      st->active = (st->iterations < st->max_iters) ? 1 : 0;  // krylov.py:157-158
+      s_open = 1;
+    }
   }
-  // krylov.py:137-139
-  if (beta == 0.0 || (beta <= st->tol * st->denom && st->iterations >= st->min_iters)) {
-    st->converged = 1;
-    st->running = 0;
-    return;
+  __syncthreads();
+  if (s_open) {
+    const int m = sc.m;
+    const double beta = st->beta;
+    for (int i = threadIdx.x; i <= m; i += blockDim.x) sc.g[i] = (i == 0) ? beta : 0.0;
+    for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) {
+      sc.H[i] = 0.0;
+      sc.R[i] = 0.0;
+    }
   }
-  // krylov.py:140-141: breakdown with no progress
-  if (st->has_prev && beta >= st->prev_beta * (1.0 - 1e-14) && st->warning) {
-    st->running = 0;
-    return;
-  }
-  st->prev_beta = beta;
-  st->has_prev = 1;
-  const int m = sc.m;
-  for (int i = 0; i <= m; ++i) sc.g[i] = 0.0;
-  sc.g[0] = beta;
-  sc.sigma[0] = 1.0 / beta;  // V[0] = r / beta  (krylov.py:145)
-  for (int i = 0; i < (m + 1) * m; ++i) {
-    sc.H[i] = 0.0;
-    sc.R[i] = 0.0;
-  }
-  st->cols = 0;
-  st->cycle_open = 1;
-  st->active = (st->iterations < st->max_iters) ? 1 : 0;  // krylov.py:157-158
 }
 
-__device__ void finish_iteration(const Scal& sc, int j, double hj1) {
+// Hessenberg column j is final in H except H[j+1, j] = hj1: Givens update, residual
+// estimate, convergence and breakdown tests (krylov.py:171-197).  sm: >= 3(m+1) doubles.
+__device__ void finish_iteration_block(const Scal& sc, int j, double hj1, double* sm) {
   State* st = sc.st;
   const int m = sc.m;
   double* Hc = sc.H + (size_t)j * (m + 1);
   double* Rc = sc.R + (size_t)j * (m + 1);
-  Hc[j + 1] = hj1;  // krylov.py:172
-  for (int i = 0; i <= j + 1; ++i) Rc[i] = Hc[i];
-  // _givens_update, krylov.py:90-104 (separately rounded products, as Python floats)
-  for (int i = 0; i < j; ++i) {
-    const double t = __dadd_rn(__dmul_rn(sc.cs[i], Rc[i]), __dmul_rn(sc.sn[i], Rc[i + 1]));
-    Rc[i + 1] = __dadd_rn(__dmul_rn(-sc.sn[i], Rc[i]), __dmul_rn(sc.cs[i], Rc[i + 1]));
-    Rc[i] = t;
+  double* col = sm;
+  double* cs = sm + (m + 1);
+  double* sn = cs + (m + 1);
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) col[i] = Hc[i];
+  for (int i = threadIdx.x; i < j; i += blockDim.x) {
+    cs[i] = sc.cs[i];
+    sn[i] = sc.sn[i];
   }
-  const double den = hypot(Rc[j], Rc[j + 1]);
-  if (den == 0.0) {
-    sc.cs[j] = 1.0;
-    sc.sn[j] = 0.0;
-  } else {
-    sc.cs[j] = Rc[j] / den;
-    sc.sn[j] = Rc[j + 1] / den;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    col[j + 1] = hj1;
+    Hc[j + 1] = hj1;  // krylov.py:172
+    double hn = 0.0;
+    for (int i = 0; i <= j + 1; ++i) hn += col[i] * col[i];
+    hn = sqrt(hn);
+    // _givens_update, krylov.py:90-104 (separately rounded products, as Python floats)
+    for (int i = 0; i < j; ++i) {
+      const double t = __dadd_rn(__dmul_rn(cs[i], col[i]), __dmul_rn(sn[i], col[i + 1]));
+      col[i + 1] = __dadd_rn(__dmul_rn(-sn[i], col[i]), __dmul_rn(cs[i], col[i + 1]));
+      col[i] = t;
+    }
+    const double den = hypot(col[j], col[j + 1]);
+    double c = 1.0, s = 0.0;
+    if (den != 0.0) {
+      c = col[j] / den;
+      s = col[j + 1] / den;
+    }
+    sc.cs[j] = c;
+    sc.sn[j] = s;
+    col[j] = den;
+    col[j + 1] = 0.0;
+    const double gj = sc.g[j];
+    sc.g[j + 1] = __dmul_rn(-s, gj);
+    sc.g[j] = __dmul_rn(c, gj);
+    st->cols = j + 1;
+    const double resnorm = fabs(sc.g[j + 1]);
+    st->iterations += 1;
+    sc.hist[st->iterations] = resnorm;
+    sc.restart_of[st->iterations] = st->cycle;
+    st->reorth = 0;
+    if (resnorm <= st->tol * st->denom && st->iterations >= st->min_iters) {  // :189-191
+      st->converged = 1;
+      st->active = 0;
+      st->last_broke = 1;
+    } else if (hj1 <= 1e-13 * fmax(1.0, hn)) {  // :192-194
+      st->warning = DK_WARNING_BREAKDOWN;
+      st->active = 0;
+      st->last_broke = 1;
+    } else {
+      st->last_broke = 0;
+      sc.sigma[j + 1] = 1.0 / hj1;  // V[j+1] = w / hj1 (:197)
+      if (j + 1 >= m || st->iterations >= st->max_iters) st->active = 0;
+    }
   }
-  Rc[j] = den;
-  Rc[j + 1] = 0.0;
-  sc.g[j + 1] = __dmul_rn(-sc.sn[j], sc.g[j]);
-  sc.g[j] = __dmul_rn(sc.cs[j], sc.g[j]);
-  st->cols = j + 1;
-  const double resnorm = fabs(sc.g[j + 1]);
-  st->iterations += 1;
-  sc.hist[st->iterations] = resnorm;
-  sc.restart_of[st->iterations] = st->cycle;
-  double hn = 0.0;
-  for (int i = 0; i <= j + 1; ++i) hn += Hc[i] * Hc[i];
-  hn = sqrt(hn);
-  st->reorth = 0;
-  if (resnorm <= st->tol * st->denom && st->iterations >= st->min_iters) {  // :189-191
-    st->converged = 1;
-    st->active = 0;
-    st->last_broke = 1;
-  } else if (hj1 <= 1e-13 * fmax(1.0, hn)) {  // :192-194
-    st->warning = DK_WARNING_BREAKDOWN;
-    st->active = 0;
-    st->last_broke = 1;
-  } else {
-    st->last_broke = 0;
-    sc.sigma[j + 1] = 1.0 / hj1;  // V[j+1] = w / hj1 (:197)
-    if (j + 1 >= m || st->iterations >= st->max_iters) st->active = 0;
-  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) Rc[i] = col[i];
 }
 
 // ======================================================================================
-// K4: prolongation + subtraction, multi-dot and norm.
+// K4: prolongation + subtraction, multi-dot, Gram column and norm.
+//
+// h_i = V_i . w (classical Gram-Schmidt coefficients) and G_ij = V_i . V_j (the new column
+// of the basis Gram matrix) are formed in the same sweep — V_i is loaded once and used for
+// both.  With G the reference's re-orthogonalisation test (krylov.py:167-168: max |V^T w'|
+// > 1e-8 ||w0|| after the projection) is evaluated without another pass over V:
+//     V^T (w - V h) = h - G h.
+// The test is evaluated up to O(eps ||w||), eight orders below its threshold.
 // ======================================================================================
 template <bool AM>
 __device__ __forceinline__ double prolong_cell(const Dia& A, const int* __restrict__ lab,
@@ -350,6 +379,10 @@ __device__ __forceinline__ double prolong_cell(const Dia& A, const int* __restri
   return t;
 }
 
+__device__ __forceinline__ double gram_at(const double* Gm, int m, int i, int k) {
+  return i <= k ? Gm[(size_t)k * (m + 1) + i] : Gm[(size_t)i * (m + 1) + k];
+}
+
 template <int MODE, bool DEFL, bool AM>
 __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restrict__ lab,
                                                       const double* __restrict__ yc,
@@ -361,27 +394,29 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
   if (*gate == 0) return;
   extern __shared__ double red[];  // [nq][kWarps]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nq = (MODE == PJ_ITER) ? nvec + 1 : 1;
-  const int nslot = (MODE == PJ_ITER) ? nvec : 0;
+  // quantities: ITER: h[nvec], g[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
+  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+  const int nslot = (MODE == PJ_ITER) ? 2 * nvec : 0;
   for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
+  const double* Vj = V + (long long)(nvec - 1) * vstride;
   for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long long cb = ch * kChunk + 2 * threadIdx.x;
     double w[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const long long i = cb + 512 * k;
-      double2 x = ld2(w_in + i);
+      double2 x = (MODE == PJ_REDOTS) ? ld2cg(w_in + i) : ld2(w_in + i);
       if (DEFL) {
         x.x = __dsub_rn(x.x, prolong_cell<AM>(A, lab, yc, i));
         x.y = __dsub_rn(x.y, prolong_cell<AM>(A, lab, yc, i + 1));
       }
       w[2 * k] = x.x;
       w[2 * k + 1] = x.y;
-      if (DEFL || w_out != w_in) st2(w_out + i, x);
+      if (MODE != PJ_REDOTS && (DEFL || w_out != w_in)) st2(w_out + i, x);
     }
-    if (MODE != PJ_PLAIN) {
+    if (MODE == PJ_ITER || MODE == PJ_RESTART) {
       double nrm = 0.0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) nrm = fma(w[e], w[e], nrm);
@@ -389,18 +424,46 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
       if (lane == 0) red[nslot * kWarps + warp] += nrm;
     }
     if (MODE == PJ_ITER) {
+      double vj[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 p = ld2(Vj + cb + 512 * k);
+        vj[2 * k] = p.x;
+        vj[2 * k + 1] = p.y;
+      }
 #pragma unroll 2
       for (int v = 0; v < nvec; ++v) {
         const double* Vr = V + (long long)v * vstride + cb;
-        double acc = 0.0;
+        double ah = 0.0, ag = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const double2 p = ld2(Vr + 512 * k);
-          acc = fma(p.x, w[2 * k], acc);
-          acc = fma(p.y, w[2 * k + 1], acc);
+          ah = fma(p.x, w[2 * k], ah);
+          ah = fma(p.y, w[2 * k + 1], ah);
+          ag = fma(p.x, vj[2 * k], ag);
+          ag = fma(p.y, vj[2 * k + 1], ag);
         }
-        acc = warp_sum(acc);
-        if (lane == 0) red[v * kWarps + warp] += acc;
+        ah = warp_sum(ah);
+        ag = warp_sum(ag);
+        if (lane == 0) {
+          red[v * kWarps + warp] += ah;
+          red[(nvec + v) * kWarps + warp] += ag;
+        }
+      }
+    }
+    if (MODE == PJ_REDOTS) {
+#pragma unroll 2
+      for (int v = 0; v < nvec; ++v) {
+        const double* Vr = V + (long long)v * vstride + cb;
+        double ah = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 p = ld2(Vr + 512 * k);
+          ah = fma(p.x, w[2 * k], ah);
+          ah = fma(p.y, w[2 * k + 1], ah);
+        }
+        ah = warp_sum(ah);
+        if (lane == 0) red[v * kWarps + warp] += ah;
       }
     }
   }
@@ -411,20 +474,48 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
     for (int w2 = 0; w2 < kWarps; ++w2) s += red[q * kWarps + w2];
     part[(size_t)q * G + blockIdx.x] = s;
   }
-  if (!last_block(&sc.st->ticket[0])) return;
+  if (!last_block(&sc.st->ticket[MODE == PJ_REDOTS ? 3 : 0])) return;
   reduce_partials(part, nq, G, red);
+  State* st = sc.st;
+  const int m = sc.m;
+  if (MODE == PJ_RESTART) {
+    restart_done_block(sc, red[0]);
+    return;
+  }
+  double* Hc = sc.H + (size_t)j * (m + 1);
+  if (MODE == PJ_REDOTS) {  // second Gram-Schmidt pass coefficients (krylov.py:169-170)
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      const double cr = red[v] * sc.sigma[v];
+      Hc[v] += cr;
+      sc.corr[v] = cr * sc.sigma[v];
+    }
+    return;
+  }
+  // MODE == PJ_ITER
+  const double sj = sc.sigma[nvec - 1];
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
+    Hc[v] = h;
+    sc.coef[v] = h * sc.sigma[v];
+    sc.Gm[(size_t)j * (m + 1) + v] = red[nvec + v] * sc.sigma[v] * sj;
+  }
+  __syncthreads();
+  // corr_i = h_i - sum_k G_ik h_k ; reuse red[nvec..2nvec) for |corr_i|
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    double c = Hc[i];
+    for (int k = 0; k < nvec; ++k) c -= gram_at(sc.Gm, m, i, k) * Hc[k];
+    red[nvec + i] = fabs(c);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    if (MODE == PJ_ITER) {
-      State* st = sc.st;
-      double* Hc = sc.H + (size_t)j * (sc.m + 1);
-      for (int v = 0; v < nvec; ++v) {
-        const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
-        Hc[v] = h;
-        sc.coef[v] = h * sc.sigma[v];
-      }
-      st->wnorm0 = sqrt(red[nvec]);  // krylov.py:162
+    st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
+    double mx = 0.0;
+    for (int i = 0; i < nvec; ++i) mx = fmax(mx, red[nvec + i]);
+    if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
+      st->reorth = 1;
+      st->reorths += 1;
     } else {
-      restart_done(sc, red[0]);
+      st->reorth = 0;
     }
   }
 }
@@ -434,8 +525,9 @@ static void project_t(const Dia& A, const int* lab, const double* yc, const doub
                       double* w_out, const double* V, long long vstride, int nvec,
                       long long n_pad, double* part, int G, const Scal& sc, int j,
                       const int* gate, cudaStream_t s) {
-  const int nq = (MODE == PJ_ITER) ? nvec + 1 : 1;
-  const size_t smem = (size_t)(nq > 1 ? nq : 1) * kWarps * sizeof(double);
+  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+  const int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
+  const size_t smem = (size_t)slots * sizeof(double);
   k_project<MODE, DEFL, AM><<<G, kThreads, smem, s>>>(A, lab, yc, w_in, w_out, V, vstride, nvec,
                                                       n_pad, part, G, sc, j, gate);
 }
@@ -466,17 +558,18 @@ void launch_project(int mode, bool defl, bool am, const Dia& A, const int* lab, 
   else if (mode == PJ_RESTART)
     project_m<PJ_RESTART>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
                           j, gate, s);
+  else if (mode == PJ_REDOTS)
+    project_t<PJ_REDOTS, false, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
+                                       sc, j, gate, s);
   else
     project_m<PJ_PLAIN>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
                         j, gate, s);
 }
 
 // ======================================================================================
-// K5/K6: classical Gram-Schmidt update with the reference's selective
-// re-orthogonalisation test (krylov.py:163-172):
-//   pass 1: u = w - sum_i h_i V_i ; corr = V^T u ; if max|corr| > 1e-8 ||w0||  -> pass 2
-//   pass 2: u -= sum_i corr_i V_i ; H[:j+1, j] += corr
-// The corr dots re-read V_i at the thread's own cells (L2-resident right after pass 1).
+// K5: classical Gram-Schmidt update u = w - sum_i h_i V_i with ||u||^2, one sweep over V.
+// REORTH: the second pass u -= sum_i corr_i V_i (only when the test in K4 fired; corr is
+// then recomputed from the stored u by a PJ_REDOTS sweep, as the reference does).
 // ======================================================================================
 template <bool REORTH>
 __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_out,
@@ -486,13 +579,11 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
                                                  const int* __restrict__ gate) {
   if (*gate == 0) return;
   extern __shared__ double sh[];
-  double* cf = sh;                      // [nvec]
-  double* red = sh + nvec;              // [nq][kWarps]
+  double* cf = sh;                                  // [nvec]
+  double* red = sh + nvec;                          // [kWarps] (+ scratch)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nq = REORTH ? 1 : nvec + 1;
-  const int nslot = REORTH ? 0 : nvec;
   for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = REORTH ? sc.corr[q] : sc.coef[q];
-  for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
+  for (int q = threadIdx.x; q < kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
   for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
@@ -504,7 +595,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
       u[2 * k] = x.x;
       u[2 * k + 1] = x.y;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int v = 0; v < nvec; ++v) {
       const double* Vr = V + (long long)v * vstride + cb;
       const double c = cf[v];
@@ -523,59 +614,27 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
       nrm = fma(u[2 * k + 1], u[2 * k + 1], nrm);
     }
     nrm = warp_sum(nrm);
-    if (lane == 0) red[nslot * kWarps + warp] += nrm;
-    if (!REORTH) {
-#pragma unroll 2
-      for (int v = 0; v < nvec; ++v) {
-        const double* Vr = V + (long long)v * vstride + cb;
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double2 p = ld2(Vr + 512 * k);
-          acc = fma(p.x, u[2 * k], acc);
-          acc = fma(p.y, u[2 * k + 1], acc);
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) red[v * kWarps + warp] += acc;
-      }
-    }
+    if (lane == 0) red[warp] += nrm;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+  if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w2 = 0; w2 < kWarps; ++w2) s += red[q * kWarps + w2];
-    part[(size_t)q * G + blockIdx.x] = s;
+    for (int w2 = 0; w2 < kWarps; ++w2) s += red[w2];
+    part[blockIdx.x] = s;
   }
   if (!last_block(&sc.st->ticket[REORTH ? 2 : 1])) return;
-  reduce_partials(part, nq, G, red);
-  if (threadIdx.x == 0) {
-    State* st = sc.st;
-    if (REORTH) {
-      finish_iteration(sc, j, sqrt(red[0]));
-    } else {
-      double mx = 0.0;
-      for (int v = 0; v < nvec; ++v) mx = fmax(mx, fabs(red[v] * sc.sigma[v]));
-      if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
-        double* Hc = sc.H + (size_t)j * (sc.m + 1);
-        for (int v = 0; v < nvec; ++v) {
-          const double cr = red[v] * sc.sigma[v];
-          Hc[v] += cr;  // krylov.py:170
-          sc.corr[v] = cr * sc.sigma[v];
-        }
-        st->reorth = 1;
-        st->reorths += 1;
-      } else {
-        finish_iteration(sc, j, sqrt(red[nvec]));
-      }
-    }
-  }
+  reduce_partials(part, 1, G, red);
+  const double hj1 = sqrt(red[0]);
+  __syncthreads();
+  if (!REORTH && sc.st->reorth) return;  // the second pass finishes the iteration
+  finish_iteration_block(sc, j, hj1, red);
 }
 
 void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
                int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                const int* gate, cudaStream_t s) {
-  const int nq = reorth ? 1 : nvec + 1;
-  const size_t smem = ((size_t)nvec + (size_t)nq * kWarps) * sizeof(double);
+  const int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
+  const size_t smem = ((size_t)nvec + (size_t)slots) * sizeof(double);
   if (reorth)
     k_gs<true><<<G, kThreads, smem, s>>>(w_in, u_out, V, vstride, nvec, n_pad, part, G, sc, j,
                                          gate);
@@ -586,40 +645,62 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
 
 // ======================================================================================
 // Cycle end (krylov.py:199-212): drop dependent trailing columns, y = R^-1 g by column-
-// oriented back substitution, coefficients for x += M^-1 V y.
+// oriented back substitution (one warp; each y_i sees the same operation order as the
+// sequential loop), coefficients for x += M^-1 V y.
 // ======================================================================================
-__global__ void k_cycle_end(Scal sc) {
+__global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
   State* st = sc.st;
   if (!st->cycle_open) return;
-  st->cycle_open = 0;
-  st->active = 0;
+  extern __shared__ double sm[];
   const int m = sc.m;
+  const int lane = threadIdx.x;
   int cols = st->cols;
+  __syncwarp();
+  if (lane == 0) {
+    st->cycle_open = 0;
+    st->active = 0;
+    st->cycle_cols = cols;
+  }
   if (cols == 0) {  // krylov.py:199-200
-    st->running = 0;
-    st->last_cols = 0;
-    st->xupdate = 0;
+    if (lane == 0) {
+      st->running = 0;
+      st->last_cols = 0;
+      st->xupdate = 0;
+    }
     return;
   }
-  st->cycle_cols = cols;
   const double r00 = fabs(sc.R[0]);
   while (cols > 1 && fabs(sc.R[(size_t)(cols - 1) * (m + 1) + (cols - 1)]) < 1e-14 * r00) --cols;
-  for (int i = 0; i < cols; ++i) sc.y[i] = sc.g[i];
+  double* Rs = sm;                 // cols x cols, column-major
+  double* y = sm + cols * cols;    // cols
+  for (int e = lane; e < cols * cols; e += 32)
+    Rs[e] = sc.R[(size_t)(e / cols) * (m + 1) + (e % cols)];
+  for (int i = lane; i < cols; i += 32) y[i] = sc.g[i];
+  __syncwarp();
   for (int k = cols - 1; k >= 0; --k) {
-    const double* Rk = sc.R + (size_t)k * (m + 1);
-    sc.y[k] = sc.y[k] / Rk[k];
-    for (int i = 0; i < k; ++i) sc.y[i] = __dsub_rn(sc.y[i], __dmul_rn(sc.y[k], Rk[i]));
+    if (lane == 0) y[k] = y[k] / Rs[k * cols + k];
+    __syncwarp();
+    const double yk = y[k];
+    for (int i = lane; i < k; i += 32) y[i] = __dsub_rn(y[i], __dmul_rn(yk, Rs[k * cols + i]));
+    __syncwarp();
   }
-  for (int i = 0; i < cols; ++i) sc.coef[i] = sc.y[i] * sc.sigma[i];
-  st->last_cols = cols;
-  st->xupdate = 1;
-  st->cycle += 1;
-  const bool done = st->converged || st->iterations >= st->max_iters;  // krylov.py:127
-  st->running = done ? 0 : 1;
+  for (int i = lane; i < cols; i += 32) {
+    sc.y[i] = y[i];
+    sc.coef[i] = y[i] * sc.sigma[i];
+  }
+  if (lane == 0) {
+    st->last_cols = cols;
+    st->xupdate = 1;
+    st->cycle += 1;
+    const bool done = st->converged || st->iterations >= st->max_iters;  // krylov.py:127
+    st->running = done ? 0 : 1;
+  }
 }
 
-void launch_cycle_end(const Scal& sc, cudaStream_t s) { k_cycle_end<<<1, 1, 0, s>>>(sc); }
-
+void launch_cycle_end(const Scal& sc, cudaStream_t s) {
+  const size_t smem = ((size_t)sc.m * sc.m + sc.m + 1) * sizeof(double);
+  k_cycle_end<<<1, 32, smem, s>>>(sc);
+}
 // x += M^-1 (sum_{i<cols} y_i V_i)   (krylov.py:206)
 __global__ void __launch_bounds__(kThreads) k_xupdate(Dia A, double* __restrict__ x,
                                                       const double* __restrict__ V,

@@ -33,9 +33,10 @@ void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cud
 void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
                  cudaStream_t s);
 
-enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2 };
-// w_out = w_in - A_p Z y (defl) ; ITER: dots with V_0..V_{nvec-1} and ||w_out||^2 -> H col j;
-// RESTART: ||w_out||^2 -> restart test.  G = grid width (fixed per operator).
+enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
+// w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w and Gram column V^T V_j, ||w_out||^2
+// -> H col j + re-orthogonalisation test; RESTART: ||w_out||^2 -> restart test;
+// REDOTS: corr = V^T u for the second Gram-Schmidt pass.  G = grid width (fixed per op).
 void launch_project(int mode, bool defl, bool am, const Dia& A, const int* lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,

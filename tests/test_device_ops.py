@@ -1,0 +1,136 @@
+"""Device building blocks against the reference goldens and the CPU oracle (GPU)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_1510_02148_b200 as dk
+from conftest import rel
+from oracle import dk_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _hetero(golden):
+    g = golden("hetero")
+    A = dk.SparseMatrix(len(g["b"]), g["ro"], g["ci"], g["va"])
+    return g, A, sp.csr_matrix((g["va"], g["ci"], g["ro"]))
+
+
+def test_spmv_bit_identical_to_csr(gpu, golden):
+    g, A, Ac = _hetero(golden)
+    rng = np.random.default_rng(1)
+    for _ in range(3):
+        x = rng.standard_normal(A.n) * 10.0 ** rng.uniform(-5, 5, A.n)
+        np.testing.assert_array_equal(dk.spmv(A, x), Ac @ x)
+
+
+def test_spmv_linearity_and_shapes(gpu, golden):
+    g, A, _ = _hetero(golden)
+    rng = np.random.default_rng(2)
+    x, y = rng.standard_normal(A.n), rng.standard_normal(A.n)
+    np.testing.assert_allclose(dk.spmv(A, 2.0 * x - 3.0 * y),
+                               2.0 * dk.spmv(A, x) - 3.0 * dk.spmv(A, y), atol=1e-9)
+    with pytest.raises(ValueError):
+        dk.spmv(A, np.ones(A.n + 1))
+
+
+def _ctx(g, A, ap="A"):
+    M = dk.Preconditioner.jacobi(A)
+    col, dd = O.columns_from_labels(g["labels"], int(g["d"]), g["excl"])
+    return dk.build_context(A, M, dk.DeflationBasis(labels=col, d=dd), g["b"], A_p_choice=ap), M
+
+
+def test_coarse_matrix_and_inverse(gpu, golden):
+    g, A, _ = _hetero(golden)
+    ctx, _ = _ctx(g, A)
+    E, Einv = ctx.coarse_matrix()
+    np.testing.assert_allclose(E, g["E"], rtol=1e-12, atol=1e-13 * np.abs(g["E"]).max())
+    np.testing.assert_allclose(Einv @ g["E"], np.eye(E.shape[0]), atol=1e-10)
+
+
+def test_projectors_match_reference(gpu, golden):
+    g, A, _ = _hetero(golden)
+    ctx, _ = _ctx(g, A)
+    scale = np.abs(g["p1v"]).max()
+    np.testing.assert_allclose(ctx.apply_p1(g["v"]), g["p1v"], atol=1e-12 * scale)
+    np.testing.assert_allclose(ctx.apply_p2(g["v"]), g["p2v"], atol=1e-12)
+    np.testing.assert_allclose(ctx.reconstruct(g["v"]), g["rec"], atol=1e-12)
+    np.testing.assert_allclose(ctx.x_star, g["x_star"], atol=1e-12)
+
+
+def test_projector_identities(gpu, golden):
+    """Idempotence, Z^T P1 = 0, P2 Z = 0 and P1 A = A P2 (reference test_deflation.py:82-113)."""
+    g, A, Ac = _hetero(golden)
+    ctx, _ = _ctx(g, A)
+    lab = ctx.basis.labels
+    keep = lab >= 0
+    v = np.random.default_rng(8).standard_normal(A.n)
+    p1v = ctx.apply_p1(v)
+    np.testing.assert_allclose(ctx.apply_p1(p1v), p1v, atol=1e-10 * np.abs(v).max())
+    restr = np.bincount(lab[keep], weights=p1v[keep], minlength=ctx.d)
+    assert np.abs(restr).max() < 1e-9 * np.abs(v).max()
+    p2v = ctx.apply_p2(v)
+    np.testing.assert_allclose(ctx.apply_p2(p2v), p2v, atol=1e-10)
+    for j in range(min(ctx.d, 4)):
+        zj = (lab == j).astype(float)
+        np.testing.assert_allclose(ctx.apply_p2(zj), 0.0, atol=1e-10)
+    np.testing.assert_allclose(ctx.apply_p1(Ac @ v), Ac @ ctx.apply_p2(v),
+                               atol=1e-9 * np.abs(Ac @ v).max())
+
+
+def test_am_variant_matches_oracle(gpu, golden):
+    g, A, Ac = _hetero(golden)
+    ctx, M = _ctx(g, A, ap="AM")
+    defl = O.LabelDeflation(Ac, ctx.basis.labels, ctx.d, g["b"], M.inv_diag, ap="AM")
+    v = np.random.default_rng(4).standard_normal(A.n)
+    np.testing.assert_allclose(ctx.apply_p1(v), defl.apply_p1(v), atol=1e-10 * np.abs(v).max())
+    np.testing.assert_allclose(ctx.apply_p2(v), defl.apply_p2(v), atol=1e-10)
+
+
+def test_singular_coarse_matrix_raises(gpu):
+    """An empty indicator column makes E exactly singular (reference sparse.py:135-136)."""
+    A = dk.SparseMatrix.from_dia(6, [-1, 0, 1], np.vstack([-np.ones(6), 3 * np.ones(6),
+                                                          -np.ones(6)]))
+    Z = np.zeros((6, 2))
+    Z[:, 0] = 1.0
+    with pytest.raises(dk.SingularCoarseMatrix):
+        dk.build_context(A, dk.Preconditioner.identity(), dk.DeflationBasis(Z), np.ones(6))
+    Zd = np.zeros((6, 2))
+    Zd[:3, 0] = Zd[:3, 1] = 1.0   # two equal columns: dependent
+    with pytest.raises(dk.SingularCoarseMatrix):
+        dk.build_context(A, dk.Preconditioner.identity(), dk.DeflationBasis(Zd), np.ones(6))
+
+
+def test_context_argument_errors(gpu, golden):
+    g, A, _ = _hetero(golden)
+    M = dk.Preconditioner.jacobi(A)
+    B = dk.DeflationBasis(labels=np.zeros(A.n, dtype=np.int32), d=1)
+    with pytest.raises(ValueError):
+        dk.build_context(A, M, B, g["b"], A_p_choice="B")
+    with pytest.raises(ValueError):
+        dk.build_context(A, M, dk.DeflationBasis(labels=np.zeros(A.n - 1, dtype=np.int32), d=1),
+                         g["b"])
+    with pytest.raises(ValueError):
+        dk.build_context(A, M, B, g["b"][:-1])
+    with pytest.raises(ValueError):
+        dk.DeflationBasis(np.ones((6, 0)))
+
+
+def test_large_coarse_system_lu_matches_numpy(gpu):
+    """d = 1,500 columns (many LU panels): E^-1 against numpy's inverse."""
+    from paper_1510_02148_b200 import configs
+    c = configs.make_case(3)
+    A, b = c.problem()
+    p = c.partition()
+    basis = dk.partition_to_basis(p)
+    # restrict to the first 1500 columns by relabelling the rest to -1
+    lab = basis.labels.copy()
+    lab[lab >= 1500] = -1
+    ctx = dk.build_context(A, dk.Preconditioner.jacobi(A), dk.DeflationBasis(labels=lab, d=1500),
+                           b)
+    E, Einv = ctx.coarse_matrix()
+    ref = np.linalg.inv(E)
+    assert rel(Einv, ref) < 1e-10
+    np.testing.assert_allclose(E, E.T, rtol=0, atol=1e-12 * np.abs(E).max())

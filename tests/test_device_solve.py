@@ -1,0 +1,226 @@
+"""PDGMRES / GMRES on the device against the reference goldens and the CPU oracle (GPU).
+
+Parity bar (BASELINE north_star): identical labels / column map / d; |x - x_ref| / |x_ref|
+<= 1e-8; iteration count within +-2 of the reference.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1510_02148_b200 as dk
+from conftest import GOLDEN, rel
+from oracle import dk_oracle as O
+from paper_1510_02148_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-8
+IT_TOL = 2
+
+
+def test_sandwich_golden_history(gpu, golden):
+    """The reference frontend's golden convergence.pdgmres.csv (22 iterations, GMRES(40))."""
+    g = golden("sandwich")
+    A = dk.SparseMatrix(len(g["b"]), g["ro"], g["ci"], g["va"])
+    M = dk.Preconditioner.jacobi(A)
+    basis = dk.DeflationBasis(labels=g["labels"].astype(np.int32), d=int(g["d"]))
+    rep = dk.pdgmres(A, g["b"], M=M, m=40, basis=basis, tol=1e-6, max_iters=300)
+    assert rep.converged and rep.iterations == int(g["pd_iters"]) == 22
+    assert len(rep.residual_history) == rep.iterations + 1
+    np.testing.assert_allclose(rep.residual_history, g["fixture_history"], rtol=1e-6)
+    assert np.all(rep.deflated_flags) and rep.deflated_from_cycle == 0
+    assert rel(rep.x, g["pd_x"]) <= X_TOL
+
+
+def test_sandwich_gmres_max_iters(gpu, golden):
+    g = golden("sandwich")
+    A = dk.SparseMatrix(len(g["b"]), g["ro"], g["ci"], g["va"])
+    M = dk.Preconditioner.jacobi(A)
+    rep = dk.gmres(A, g["b"], M=M, m=40, tol=1e-6, max_iters=300)
+    assert rep.iterations == int(g["gm_iters"]) == 300 and not rep.converged
+    assert rep.restarts == 7 and rep.deflated_from_cycle is None
+    h, ref = rep.residual_history, g["gm_history"]
+    # GMRES(40) stagnates here (reference test_acceptance.py:68-78); the first cycle follows
+    # the reference closely, later cycles within the stagnation plateau
+    np.testing.assert_allclose(h[:41], ref[:41], rtol=1e-6)
+    np.testing.assert_allclose(h, ref, rtol=5e-2)
+    assert rel(rep.x, g["gm_x"]) <= 1e-4
+
+
+@pytest.mark.parametrize("ap,key", [("A", "pd"), ("AM", "am")])
+def test_hetero_pdgmres(gpu, golden, ap, key):
+    g = golden("hetero")
+    A = dk.SparseMatrix(len(g["b"]), g["ro"], g["ci"], g["va"])
+    M = dk.Preconditioner.jacobi(A)
+    col, dd = O.columns_from_labels(g["labels"], int(g["d"]), g["excl"])
+    rep = dk.pdgmres(A, g["b"], M=M, m=20, basis=dk.DeflationBasis(labels=col, d=dd), tol=1e-10,
+                     max_iters=2000, A_p_choice=ap)
+    assert rep.converged
+    assert abs(rep.iterations - int(g[f"{key}_iters"])) <= IT_TOL
+    assert rel(rep.x, g[f"{key}_x"]) <= X_TOL
+
+
+def test_hetero_gmres_plain(gpu, golden):
+    g = golden("hetero")
+    A = dk.SparseMatrix(len(g["b"]), g["ro"], g["ci"], g["va"])
+    rep = dk.gmres(A, g["b"], M=dk.Preconditioner.jacobi(A), m=20, tol=1e-10, max_iters=2000)
+    assert abs(rep.iterations - int(g["gm_iters"])) <= IT_TOL
+    assert rel(rep.x, g["gm_x"]) <= X_TOL
+
+
+def _case_solve(idx, deflate=True):
+    case = configs.make_case(idx)
+    A, b = case.problem()
+    M = dk.Preconditioner.jacobi(A)
+    part = case.partition()
+    basis = dk.partition_to_basis(part)
+    if deflate:
+        rep = dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=case.max_iters)
+    else:
+        rep = dk.gmres(A, b, M=M, m=case.m, tol=case.tol, max_iters=case.max_iters)
+    return case, A, b, part, basis, rep
+
+
+def test_config1_parity(gpu, golden):
+    g = golden("config1")
+    case, A, b, part, basis, rep = _case_solve(1)
+    np.testing.assert_array_equal(part.labels, g["labels"])
+    assert rep.converged and abs(rep.iterations - int(g["pd_iters"])) <= IT_TOL
+    assert rel(rep.x, g["pd_x"]) <= X_TOL
+    assert rep.final_relres < 1e-7
+
+
+def test_config1_plain_parity(gpu, golden):
+    g = golden("config1")
+    case, A, b, part, basis, rep = _case_solve(1, deflate=False)
+    assert abs(rep.iterations - int(g["gm_iters"])) <= IT_TOL
+    assert rel(rep.x, g["gm_x"]) <= X_TOL
+
+
+def test_config2_parity(gpu, golden):
+    """128x128x64, d = 112: against the reference's dense-Z pdgmres run."""
+    g = golden("config2")
+    case, A, b, part, basis, rep = _case_solve(2)
+    assert part.d == int(g["d"])
+    assert rep.converged and abs(rep.iterations - int(g["pd_iters"])) <= IT_TOL
+    xs = rep.x[::97]
+    assert np.linalg.norm(xs - g["pd_x_sample"]) / np.linalg.norm(g["pd_x_sample"]) <= X_TOL
+    assert abs(np.linalg.norm(rep.x) - float(g["pd_x_norm"])) <= X_TOL * float(g["pd_x_norm"])
+
+
+def test_config3_parity(gpu):
+    """60x220x85, d = 10,917: against the label-based oracle's full run (golden), plus
+    size-independent properties (true residual, coarse-space orthogonality of P1 r)."""
+    path = GOLDEN / "config3_oracle.npz"
+    if not path.exists():
+        pytest.fail("tests/golden/config3_oracle.npz missing (oracle/run_case.py 3)")
+    g = np.load(path)
+    case, A, b, part, basis, rep = _case_solve(3)
+    assert basis.d == int(g["d"]) == 10917
+    assert rep.converged and abs(rep.iterations - int(g["iters"])) <= IT_TOL
+    xs = rep.x[::97]
+    assert np.linalg.norm(xs - g["x_sample"]) / np.linalg.norm(g["x_sample"]) <= X_TOL
+    assert rep.final_relres < 1e-6
+    # the deflated residual is Z-orthogonal: Z^T (b - A x) ~ 0 (P1 annihilates range(Z^T))
+    r = b - dk.spmv(A, rep.x)
+    keep = basis.labels >= 0
+    zr = np.bincount(basis.labels[keep], weights=r[keep], minlength=basis.d)
+    assert np.abs(zr).max() <= 1e-6 * np.linalg.norm(b)
+
+
+def test_deterministic_rerun(gpu):
+    case, A, b, part, basis, rep = _case_solve(1)
+    rep2 = dk.pdgmres(A, b, M=dk.Preconditioner.jacobi(A), m=case.m, basis=basis, tol=case.tol,
+                      max_iters=case.max_iters)
+    np.testing.assert_array_equal(rep.x, rep2.x)
+    np.testing.assert_array_equal(rep.residual_history, rep2.residual_history)
+
+
+# ---- reference semantics on small operators (test_krylov.py:36-131 restated) -------------
+def _lap(n, shift=3.0):
+    off = np.array([-1, 0, 1])
+    dg = np.vstack([-np.ones(n), shift * np.ones(n), -np.ones(n)])
+    dg[0, 0] = dg[2, -1] = 0.0
+    return dk.SparseMatrix.from_dia(n, off, dg)
+
+
+def test_zero_rhs(gpu):
+    A = dk.SparseMatrix.identity(5)
+    rep = dk.gmres(A, np.zeros(5))
+    assert rep.converged and rep.iterations == 0
+    np.testing.assert_array_equal(rep.x, np.zeros(5))
+
+
+def test_x0_respected(gpu):
+    A = _lap(40)
+    x = np.random.default_rng(5).standard_normal(40)
+    b = dk.spmv(A, x)  # bit-identical operator: b - A x0 is exactly zero
+    rep = dk.gmres(A, b, x0=x, m=20, tol=1e-10)
+    assert rep.converged and rep.iterations == 0
+
+
+def test_max_iters_not_an_error(gpu):
+    A = _lap(60, 2.0)
+    b = np.random.default_rng(4).standard_normal(60)
+    rep = dk.gmres(A, b, m=5, tol=1e-16, max_iters=10)
+    assert not rep.converged and rep.iterations == 10 and len(rep.residual_history) == 11
+
+
+def test_min_iters(gpu):
+    A = dk.SparseMatrix.identity(10)
+    rep = dk.gmres(A, np.ones(10), m=10, tol=1e-6, min_iters=3)
+    assert rep.iterations >= 1
+
+
+def test_history_monotone_within_cycle_and_restarts(gpu):
+    A = _lap(80, 2.05)
+    b = np.random.default_rng(2).standard_normal(80)
+    rep = dk.gmres(A, b, m=10, tol=1e-12, max_iters=300)
+    h, cyc = rep.residual_history, rep.restart_of
+    for i in range(1, len(h)):
+        if cyc[i] == cyc[i - 1]:
+            assert h[i] <= h[i - 1] * (1 + 1e-12)
+    assert rep.restarts >= 1 and rep.iterations + 1 == len(h)
+    o = O.run_cycles(O.csr_from_dia(80, *A.dia()), b, None, None, 10, 1e-12, 300, 0, None)
+    assert abs(rep.iterations - o["iterations"]) <= IT_TOL and rel(rep.x, o["x"]) <= 1e-8
+
+
+def test_final_relres_is_true_residual(gpu):
+    A = _lap(50)
+    b = np.random.default_rng(1).standard_normal(50)
+    rep = dk.gmres(A, b, m=25, tol=1e-8)
+    true = np.linalg.norm(b - A.to_dense() @ rep.x) / np.linalg.norm(b)
+    assert rep.final_relres == pytest.approx(true, rel=1e-6, abs=1e-14)
+
+
+def test_arnoldi_relation(gpu):
+    A = _lap(30)
+    b = np.random.default_rng(7).standard_normal(30)
+    rep = dk.gmres(A, b, m=8, tol=1e-16, max_iters=8)
+    d = rep.arnoldi
+    assert d.m == 8 and d.V.shape == (9, 30) and d.Hbar.shape == (9, 8)
+    Ad = A.to_dense()
+    np.testing.assert_allclose(Ad @ d.V[:8].T, d.V.T @ d.Hbar, atol=1e-8)
+    np.testing.assert_allclose(d.V @ d.V.T, np.eye(9), atol=1e-8)
+    assert dk.ritz_values(d).shape == (8,)
+
+
+def test_input_validation(gpu):
+    A = dk.SparseMatrix.identity(4)
+    with pytest.raises(ValueError):
+        dk.gmres(A, np.ones(3))
+    with pytest.raises(ValueError):
+        dk.gmres(A, np.ones(4), x0=np.ones(5))
+    with pytest.raises(ValueError):
+        dk.gmres(A, np.ones(4), m=0)
+    with pytest.raises(ValueError):
+        dk.gmres(A, np.ones(4), tol=0.0)
+    with pytest.raises(ValueError):
+        dk.pdgmres(A, np.ones(4))
+
+
+def test_jacobi_rejects_zero_diagonal(gpu):
+    A = dk.SparseMatrix.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    with pytest.raises(ValueError):
+        dk.Preconditioner.jacobi(A)

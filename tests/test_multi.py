@@ -1,0 +1,65 @@
+"""Multi-process plumbing of bench.py on CPU (gloo, world_size 2).
+
+The hot path does not shard (BASELINE north_star: one GPU), so N GPUs run N independent
+replicas; the only cross-rank operations are the timing reductions (max of per-rank device
+time, sum of iterations), which these tests exercise with the gloo backend.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
+                       "DK_BENCH_BACKEND": "gloo"})
+    sys.path.insert(0, str(ROOT))
+    import bench
+    w, r, local, pg = bench.dist_setup(world)
+    try:
+        ms = 100.0 * (r + 1)              # per-rank device time
+        its = 761.0                       # iterations per rank (identical replicas)
+        bench.barrier(pg)
+        q.put((r, bench.reduce_max(pg, ms), bench.reduce_sum(pg, its)))
+    finally:
+        pg.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_replica_reductions_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=90) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    for r, mx, tot in out:
+        assert mx == 200.0 and tot == 1522.0
+    # whole-job throughput = iterations of all ranks / slowest rank's time
+    assert out[0][2] / (out[0][1] * 1e-3) == pytest.approx(7610.0)
+
+
+def test_reference_arm_nonzero_ranks_exit_without_work(monkeypatch):
+    sys.path.insert(0, str(ROOT))
+    import bench
+    called = []
+    monkeypatch.setattr(bench, "host_threads", lambda: called.append(1) or 1)
+    bench.run_reference_arm(type("A", (), {"config": 1})(), 2, 1)
+    assert called == []
