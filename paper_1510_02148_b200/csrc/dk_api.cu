@@ -59,6 +59,9 @@ const char* kProfNames[PC_COUNT] = {"stencil_restrict", "restrict_final", "coars
 
 unsigned long long g_ctx_serial = 0;
 
+// below this many deflation columns E^-1 is L2-resident and the plain GEMV is used
+constexpr int kSymvMinD = 256;
+
 }  // namespace
 
 struct dk_defl;
@@ -68,7 +71,11 @@ struct dk_op {
   long long n = 0, n_pad = 0, guard = 0, vlen = 0;
   int ndiag = 0, center = -1;
   long long off[kMaxDiag] = {0};
-  double* dia = nullptr;
+  double* dia = nullptr;           // nstore guarded coefficient rows
+  const double* co[kMaxDiag] = {nullptr};
+  long long csh[kMaxDiag] = {0};
+  int sym = 0;                     // bitwise symmetric: centre + positive diagonals stored
+  int nstore = 0;
   double* inv_base = nullptr;
   double* inv = nullptr;
   cudaStream_t own = nullptr, stream = nullptr;
@@ -130,6 +137,12 @@ struct dk_defl {
   double* s = nullptr;
   double* y = nullptr;
   double* qv_base = nullptr;
+  // symmetric coarse solve (E symmetric): packed upper tile triangle of E^-1 + partials
+  int sym = 0;
+  long long ntiles = 0;
+  double* P = nullptr;
+  double* rowpart = nullptr;
+  double* colpart = nullptr;
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
 };
@@ -140,11 +153,21 @@ Dia make_dia(const dk_op* op, bool with_inv) {
   Dia A{};
   A.ndiag = op->ndiag;
   A.center = op->center;
-  for (int k = 0; k < kMaxDiag; ++k) A.off[k] = k < op->ndiag ? op->off[k] : 0;
-  A.dia = op->dia;
-  A.ld = op->n_pad;
+  for (int k = 0; k < kMaxDiag; ++k) {
+    A.off[k] = k < op->ndiag ? op->off[k] : 0;
+    A.co[k] = k < op->ndiag ? op->co[k] : nullptr;
+    A.csh[k] = k < op->ndiag ? op->csh[k] : 0;
+  }
   A.inv = with_inv ? op->inv : nullptr;
   return A;
+}
+
+// flag <- 0 unless lo[i + o] == up[i] for i in [0, count)  (bitwise symmetry of a pair)
+__global__ void k_check_pair(const double* __restrict__ up, const double* __restrict__ lo,
+                             long long o, long long count, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    if (lo[i + o] != up[i]) atomicExch(flag, 0);
 }
 
 int alloc_vec(dk_op* op, double** base, double** ptr) {
@@ -279,7 +302,7 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
   const Dia A = make_dia(op, pre);
   const double n = (double)op->n;
   {
-    ProfScope ps(op, PC_STENCIL, (mode == ST_IDENT ? 12.0 : 8.0 * op->ndiag + 20.0) * n);
+    ProfScope ps(op, PC_STENCIL, (mode == ST_IDENT ? 12.0 : 8.0 * op->nstore + 20.0) * n);
     launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream);
   }
   {
@@ -287,8 +310,15 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
     launch_restrict_final(c->rm, c->s, gate, op->stream);
   }
   {
-    ProfScope ps(op, PC_GEMV, 8.0 * (double)c->d * c->ld);
-    launch_gemv(c->Einv, c->d, c->ld, c->s, c->y, gate, op->stream);
+    if (c->sym) {
+      // packed tiles + column partials written and read back
+      ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)c->ntiles + 512.0 * (double)c->ntiles);
+      launch_symv(c->P, c->d, c->s, c->rowpart, c->colpart, c->y, gate, op->stream);
+      op->launches += 1;
+    } else {
+      ProfScope ps(op, PC_GEMV, 8.0 * (double)c->d * c->ld);
+      launch_gemv(c->Einv, c->d, c->ld, c->s, c->y, gate, op->stream);
+    }
   }
 }
 
@@ -303,11 +333,11 @@ void issue_restart(dk_op* op, dk_defl* c) {
   if (c) {
     coarse_solve(op, c, ST_RESID, false, true, op->x, nullptr, op->b, op->w, &st->running);
   } else {
-    ProfScope ps(op, PC_STENCIL, (8.0 * op->ndiag + 24.0) * n);
+    ProfScope ps(op, PC_STENCIL, (8.0 * op->nstore + 24.0) * n);
     launch_stencil(ST_RESID, false, true, A, op->n_pad, op->x, nullptr, op->b, op->w, nullptr,
                    &st->running, op->stream);
   }
-  ProfScope ps(op, PC_RESTART, c ? (8.0 * op->ndiag + 20.0) * n : 16.0 * n);
+  ProfScope ps(op, PC_RESTART, c ? (8.0 * op->nstore + 20.0) * n : 16.0 * n);
   launch_project(PJ_RESTART, c != nullptr, am, Aam, c ? c->lab : nullptr, c ? c->y : nullptr,
                  op->w, op->V_base + op->guard, nullptr, op->vstride, 0, op->n_pad, op->part,
                  op->G, op->sc, 0, &st->running, op->stream);
@@ -328,13 +358,13 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
     coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
                  nullptr, op->w, &st->active);
   } else {
-    ProfScope ps(op, PC_STENCIL, (8.0 * op->ndiag + (pre ? 24.0 : 16.0)) * n);
+    ProfScope ps(op, PC_STENCIL, (8.0 * op->nstore + (pre ? 24.0 : 16.0)) * n);
     launch_stencil(ST_APPLY, pre, true, A, op->n_pad, V + (long long)j * op->vstride,
                    op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream);
   }
   {
     ProfScope ps(op, PC_PROJECT,
-                 c ? (8.0 * op->ndiag + 20.0 + 8.0 * nvec) * n : (8.0 + 8.0 * nvec) * n);
+                 c ? (8.0 * op->nstore + 20.0 + 8.0 * nvec) * n : (8.0 + 8.0 * nvec) * n);
     launch_project(PJ_ITER, c != nullptr, am, Aam, c ? c->lab : nullptr, c ? c->y : nullptr,
                    op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
                    &st->active, op->stream);
@@ -464,11 +494,89 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   }
   const long long nch = op->n_pad / kChunk;
   op->G = (int)std::min<long long>(nch, 148 * 4);
-  DK_TRY(cudaMalloc(&op->dia, (size_t)ndiag * op->n_pad * sizeof(double)));
-  DK_TRY(cudaMemsetAsync(op->dia, 0, (size_t)ndiag * op->n_pad * sizeof(double), op->stream));
+  // all diagonals, guarded, ascending offsets
+  DK_TRY(cudaMalloc(&op->dia, (size_t)ndiag * op->vlen * sizeof(double)));
+  DK_TRY(cudaMemsetAsync(op->dia, 0, (size_t)ndiag * op->vlen * sizeof(double), op->stream));
   for (int k = 0; k < ndiag; ++k) {
-    DK_TRY(cudaMemcpyAsync(op->dia + (size_t)k * op->n_pad, diags + (size_t)order[k].second * n,
-                           (size_t)n * sizeof(double), cudaMemcpyDefault, op->stream));
+    DK_TRY(cudaMemcpyAsync(op->dia + (size_t)k * op->vlen + op->guard,
+                           diags + (size_t)order[k].second * n, (size_t)n * sizeof(double),
+                           cudaMemcpyDefault, op->stream));
+  }
+  // bitwise symmetric pattern and values -> keep centre + positive diagonals only
+  {
+    int sym = 1;
+    for (int k = 0; k < ndiag && sym; ++k) {
+      const long long o = op->off[k];
+      if (o <= 0) continue;
+      int partner = -1;
+      for (int q = 0; q < ndiag; ++q)
+        if (op->off[q] == -o) partner = q;
+      if (partner < 0) {
+        sym = 0;
+        break;
+      }
+      int* f = nullptr;
+      int one_h = 1;
+      DK_TRY(cudaMalloc(&f, sizeof(int)));
+      DK_TRY(cudaMemcpy(f, &one_h, sizeof(int), cudaMemcpyHostToDevice));
+      k_check_pair<<<148 * 4, 256, 0, op->stream>>>(op->dia + (size_t)k * op->vlen + op->guard,
+                                                    op->dia + (size_t)partner * op->vlen +
+                                                        op->guard,
+                                                    o, n - o, f);
+      DK_TRY(cudaMemcpyAsync(&one_h, f, sizeof(int), cudaMemcpyDeviceToHost, op->stream));
+      DK_TRY(cudaStreamSynchronize(op->stream));
+      cudaFree(f);
+      sym = one_h;
+    }
+    int npos = 0, nneg = 0;
+    for (int k = 0; k < ndiag; ++k) {
+      if (op->off[k] > 0) ++npos;
+      if (op->off[k] < 0) ++nneg;
+    }
+    if (npos != nneg) sym = 0;
+    op->sym = sym;
+    for (int k = 0; k < ndiag; ++k) {
+      const long long o = op->off[k];
+      int src = k;
+      long long sh = 0;
+      if (sym && o < 0) {
+        for (int q = 0; q < ndiag; ++q)
+          if (op->off[q] == -o) src = q;
+        sh = o;  // a(i, i+o) = up_{-o}[i + o]
+      }
+      op->co[k] = op->dia + (size_t)src * op->vlen + op->guard;
+      op->csh[k] = sh;
+    }
+    if (sym) {  // release the negative diagonals' storage by compaction
+      double* compact = nullptr;
+      int nst = 0;
+      for (int k = 0; k < ndiag; ++k)
+        if (op->off[k] >= 0) ++nst;
+      DK_TRY(cudaMalloc(&compact, (size_t)nst * op->vlen * sizeof(double)));
+      int slot = 0;
+      long long pos_slot[kMaxDiag];
+      for (int k = 0; k < ndiag; ++k) {
+        if (op->off[k] < 0) continue;
+        DK_TRY(cudaMemcpyAsync(compact + (size_t)slot * op->vlen, op->dia + (size_t)k * op->vlen,
+                               (size_t)op->vlen * sizeof(double), cudaMemcpyDeviceToDevice,
+                               op->stream));
+        pos_slot[k] = slot++;
+      }
+      for (int k = 0; k < ndiag; ++k) {
+        const long long o = op->off[k];
+        int src = k;
+        if (o < 0)
+          for (int q = 0; q < ndiag; ++q)
+            if (op->off[q] == -o) src = q;
+        op->co[k] = compact + (size_t)pos_slot[src] * op->vlen + op->guard;
+      }
+      DK_TRY(cudaStreamSynchronize(op->stream));
+      cudaFree(op->dia);
+      op->dia = compact;
+      op->nstore = nst;
+    } else {
+      op->nstore = ndiag;
+    }
   }
   if (inv_diag) {
     int rc = alloc_vec(op, &op->inv_base, &op->inv);
@@ -710,6 +818,16 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     dk_defl_destroy(c);
     return fail(DK_ESINGULAR, "zero pivot in LU factorization");
   }
+  // symmetric E (symmetric A, A_p = A): stream only the upper tile triangle of E^-1
+  if (d >= kSymvMinD && !am && coarse_is_symmetric(c->E, d, c->ld, s)) {
+    c->sym = 1;
+    c->ntiles = symv_tiles(d);
+    DKD(cudaMalloc(&c->P, (size_t)c->ntiles * 1024 * sizeof(double)));
+    DKD(cudaMalloc(&c->rowpart, (size_t)c->ntiles * 32 * sizeof(double)));
+    DKD(cudaMalloc(&c->colpart, (size_t)c->ntiles * 32 * sizeof(double)));
+    launch_symv_pack(c->Einv, d, c->ld, c->P, s);
+    DKD(cudaGetLastError());
+  }
   // x* = Z E^-1 Z^T b  (deflation.py:88)
   cudaEventRecord(e0, s);
   if (b) {
@@ -737,7 +855,7 @@ int dk_defl_destroy(dk_defl* c) {
   if (c->op) cudaStreamSynchronize(c->op->stream);
   void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->lab_runs,
                   c->E,        c->Einv,         c->piv,      c->xs_base,     c->s,
-                  c->y,        c->qv_base};
+                  c->y,        c->qv_base,      c->P,        c->rowpart,     c->colpart};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete c;
@@ -838,7 +956,8 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, op->stream);
-  const int per_cycle_launches = (c ? 4 : 2) + m * (c ? 7 : 5) + 2;
+  const int coarse_launches = c ? (c->sym ? 4 : 3) : 1;  // stencil (+ restrict + E^-1 s)
+  const int per_cycle_launches = coarse_launches + 1 + m * (coarse_launches + 4) + 2;
   long long guard_cycles = (long long)max_iters + 2;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
     if (!op->prof) {

@@ -103,6 +103,205 @@ void launch_gemv(const double* M, int d, int ld, const double* x, double* y, con
 }
 
 // ======================================================================================
+// Symmetric coarse solve y = E^-1 s streaming only the upper tile triangle of E^-1.
+//
+// With A symmetric and A_p = A, E = Z^T A Z and E^-1 are symmetric: the tiles (I, J), I <= J,
+// of 32 x 32 hold every entry once, halving the 8 d^2 bytes per iteration.  Tile (I, J)
+// contributes y_I += T s_J (row part) and, off the diagonal, y_J += T^T s_I (column part).
+// One warp streams a contiguous range of tiles (row-major over the triangle; balanced to
+// +-1 tile): lane r owns tile row r, so the row part accumulates in a register across the
+// warp's tiles of one tile row and the column part is a 32-way butterfly reduce-scatter
+// (lane c ends with column c).  Partials go to fixed slots and k_symv_reduce sums them in
+// a fixed order: deterministic.
+// Tile storage: [16 column pairs][32 rows][2] (one coalesced 512 B double2 load per pair).
+// ======================================================================================
+constexpr int kST = 32;                 // tile edge
+constexpr int kSymvThreads = 512;
+
+__host__ __device__ inline long long tri_start(long long I, long long nb) {
+  return I * nb - I * (I - 1) / 2;      // index of tile (I, I)
+}
+
+__global__ void k_symv_pack(const double* __restrict__ Einv, int d, int ld, int nb,
+                            double* __restrict__ P) {
+  const long long ntiles = (long long)nb * (nb + 1) / 2;
+  const long long tot = ntiles * kST * kST;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long t = e / (kST * kST);
+    const int w = (int)(e % (kST * kST));
+    const int pair = w / (2 * kST), r = (w / 2) % kST, c = 2 * pair + (w & 1);
+    // tile row I: largest I with tri_start(I) <= t
+    long long lo = 0, hi = nb - 1;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) / 2;
+      if (tri_start(mid, nb) <= t) lo = mid; else hi = mid - 1;
+    }
+    const long long I = lo, J = I + (t - tri_start(I, nb));
+    const long long gr = I * kST + r, gc = J * kST + c;
+    double v = 0.0;
+    if (gr < d && gc < d) v = 0.5 * (Einv[gr * ld + gc] + Einv[gc * ld + gr]);
+    P[e] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kSymvThreads) k_symv(const double* __restrict__ P, int d, int nb,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ rowpart,
+                                                       double* __restrict__ colpart,
+                                                       const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  extern __shared__ double sx[];  // nb * 32
+  for (int i = threadIdx.x; i < nb * kST; i += blockDim.x) sx[i] = i < d ? x[i] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long W = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long ntiles = (long long)nb * (nb + 1) / 2;
+  const long long t0 = w * ntiles / W, t1 = (w + 1) * ntiles / W;
+  if (t0 >= t1) return;
+  long long lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) / 2;
+    if (tri_start(mid, nb) <= t0) lo = mid; else hi = mid - 1;
+  }
+  long long I = lo, J = I + (t0 - tri_start(I, nb));
+  long long seg = t0;  // slot of the current row-part segment
+  double racc = 0.0;
+  for (long long t = t0; t < t1; ++t) {
+    const double2* T = reinterpret_cast<const double2*>(P + t * (kST * kST));
+    const double* xJ = sx + J * kST;
+    const double xr = sx[I * kST + lane];
+    // the whole tile row (16 x 16 B) in flight, then reused in place for the column part
+    double cacc[32];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const double2 v = __ldg(T + p * kST + lane);
+      cacc[2 * p] = v.x;
+      cacc[2 * p + 1] = v.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) racc = fma(cacc[c], xJ[c], racc);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) cacc[c] *= xr;
+    if (J != I) {
+      // butterfly reduce-scatter: lane c ends with sum over lanes of cacc[c]
+#pragma unroll
+      for (int k = 16; k >= 1; k >>= 1) {
+        const bool up = (lane & k) != 0;
+#pragma unroll
+        for (int i = 0; i < k; ++i) {
+          const double send = up ? cacc[i] : cacc[i + k];
+          const double keep = up ? cacc[i + k] : cacc[i];
+          cacc[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+        }
+      }
+      colpart[t * kST + lane] = cacc[0];
+    }
+    // advance (I, J); flush the row part when the tile row changes or the range ends
+    ++J;
+    if (J == nb || t + 1 == t1) {
+      rowpart[seg * kST + lane] = racc;
+      racc = 0.0;
+      seg = t + 1;
+      if (J == nb) {
+        ++I;
+        J = I;
+      }
+    }
+  }
+}
+
+// y_J = sum of row-part segments of tile row J (warps in order) + sum_{I<J} column parts
+// of tiles (I, J) (I in order); 8 warps split the I range, combined in a fixed order.
+__global__ void __launch_bounds__(256) k_symv_reduce(const double* __restrict__ rowpart,
+                                                     const double* __restrict__ colpart, int d,
+                                                     int nb, long long W,
+                                                     double* __restrict__ y,
+                                                     const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  __shared__ double red[8][kST];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long Jt = blockIdx.x;
+  const long long ntiles = (long long)nb * (nb + 1) / 2;
+  double acc = 0.0;
+#pragma unroll 4
+  for (long long I = warp; I < Jt; I += 8) {
+    const long long t = tri_start(I, nb) + (Jt - I);
+    acc += colpart[t * kST + lane];
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double s = 0.0;
+    // row-part segments of tile row Jt: one per warp range intersecting [a, b)
+    const long long a = tri_start(Jt, nb), b = a + (nb - Jt);
+    long long wl = a * W / ntiles;
+    while (wl > 0 && (wl * ntiles) / W > a) --wl;
+    while (((wl + 1) * ntiles) / W <= a) ++wl;
+    for (long long ww = wl; ww < W; ++ww) {
+      const long long r0 = ww * ntiles / W, r1 = (ww + 1) * ntiles / W;
+      if (r0 >= b) break;
+      if (r1 <= a || r0 >= r1) continue;
+      const long long slot = r0 > a ? r0 : a;
+      s += rowpart[slot * kST + lane];
+    }
+    for (int w2 = 0; w2 < 8; ++w2) s += red[w2][lane];
+    const long long row = Jt * kST + lane;
+    if (row < d) y[row] = s;
+  }
+}
+
+// flag <- 0 unless |E_ij - E_ji| <= 1e-12 (|E_ij| + |E_ji|) for all i, j (assembly rounding)
+__global__ void k_check_sym(const double* __restrict__ E, int d, int ld, int* flag) {
+  const long long tot = (long long)d * d;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / d, j = e % d;
+    if (j <= i) continue;
+    const double a = E[i * ld + j], b = E[j * ld + i];
+    if (!(fabs(a - b) <= 1e-12 * (fabs(a) + fabs(b)))) atomicExch(flag, 0);
+  }
+}
+
+int coarse_is_symmetric(const double* E, int d, int ld, cudaStream_t s) {
+  int h = 1;
+  int* f = nullptr;
+  cudaMallocAsync(&f, sizeof(int), s);
+  cudaMemcpyAsync(f, &h, sizeof(int), cudaMemcpyHostToDevice, s);
+  k_check_sym<<<148 * 8, 256, 0, s>>>(E, d, ld, f);
+  cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFreeAsync(f, s);
+  return h;
+}
+
+long long symv_tiles(int d) {
+  const long long nb = (d + kST - 1) / kST;
+  return nb * (nb + 1) / 2;
+}
+
+void launch_symv_pack(const double* Einv, int d, int ld, double* P, cudaStream_t s) {
+  const int nb = (d + kST - 1) / kST;
+  k_symv_pack<<<148 * 8, 256, 0, s>>>(Einv, d, ld, nb, P);
+}
+
+void launch_symv(const double* P, int d, const double* x, double* rowpart, double* colpart,
+                 double* y, const int* gate, cudaStream_t s) {
+  const int nb = (d + kST - 1) / kST;
+  const size_t smem = (size_t)nb * kST * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  const unsigned grid = 148;
+  const long long W = (long long)grid * (kSymvThreads / 32);
+  k_symv<<<grid, kSymvThreads, smem, s>>>(P, d, nb, x, rowpart, colpart, gate);
+  k_symv_reduce<<<nb, 256, 0, s>>>(rowpart, colpart, d, nb, W, y, gate);
+}
+
+// ======================================================================================
 // Assembly of E = Z^T A_p Z for an indicator Z given by labels.
 //   E[L][L]  = sum over cells i of L of q_i, q_i = sum of the row's coefficients whose
 //              column is in L — a run-wise restriction of q (deterministic);
@@ -113,7 +312,7 @@ void launch_gemv(const double* M, int d, int ld, const double* x, double* y, con
 // ======================================================================================
 template <bool AM>
 __device__ __forceinline__ double coarse_coef(const Dia& A, int q, long long i) {
-  double a = A.dia[q * A.ld + i];
+  double a = dia_coef(A, q, i);
   if (AM) a = __dmul_rn(a, A.inv[i + A.off[q]]);
   return a;
 }

@@ -22,14 +22,22 @@ constexpr int kChunk = 2048;         // cells per Gram-Schmidt chunk (8 per thre
 constexpr int kMaxDiag = DK_MAX_DIAGONALS;
 constexpr int kWarps = kThreads / 32;
 
+// A(i, i + off[q]) = co[q][i + csh[q]].  Non-symmetric operators store every diagonal
+// (csh = 0).  A symmetric operator stores the centre and the positive diagonals only; the
+// negative diagonal -o reads the +o array at the neighbour, a(i, i-o) = a(i-o, i) = up_o[i-o]
+// (csh = -o) — 4 arrays instead of 7, the same values in the same summation order.
 struct Dia {
   int ndiag;
-  int center;                // index of offset 0, or -1
-  long long off[kMaxDiag];   // ascending
-  const double* dia;         // ndiag rows of stride ld (unguarded)
-  long long ld;
-  const double* inv;         // guarded Jacobi inverse diagonal, nullptr = identity
+  int center;                  // index of offset 0, or -1
+  long long off[kMaxDiag];     // ascending
+  const double* co[kMaxDiag];  // guarded coefficient arrays
+  long long csh[kMaxDiag];     // index shift into co[q]
+  const double* inv;           // guarded Jacobi inverse diagonal, nullptr = identity
 };
+
+__device__ __forceinline__ double dia_coef(const Dia& A, int q, long long i) {
+  return __ldg(A.co[q] + i + A.csh[q]);
+}
 
 // Scalar state of one solve; lives in device memory and is owned by the single-thread
 // "control" sections (last block of a reduction kernel, cycle-end kernel).

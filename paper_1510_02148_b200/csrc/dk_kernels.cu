@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
       for (int q = 0; q < kMaxDiag; ++q) {
         if (q < A.ndiag) {
           const long long o = A.off[q];
-          const double2 a = ld2(A.dia + q * A.ld + i);
+          const double2 a = (A.csh[q] & 1)
+                                ? make_double2(dia_coef(A, q, i), dia_coef(A, q, i + 1))
+                                : ld2(A.co[q] + i + A.csh[q]);
           double x0 = __ldg(v + i + o);
           double x1 = __ldg(v + i + o + 1);
           if (has_scale) {
@@ -370,7 +372,7 @@ __device__ __forceinline__ double prolong_cell(const Dia& A, const int* __restri
       const long long o = A.off[q];
       const int L = __ldg(lab + c + o);
       if (L >= 0) {
-        double a = __ldg(A.dia + q * A.ld + c);
+        double a = dia_coef(A, q, c);
         if (AM) a = __dmul_rn(a, __ldg(A.inv + c + o));
         t = __dadd_rn(t, __dmul_rn(a, __ldg(yc + L)));
       }

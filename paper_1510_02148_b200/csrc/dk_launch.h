@@ -63,6 +63,12 @@ void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min
                        cudaStream_t s);
 
 // ---- coarse operator (dk_coarse.cu) ----
+// symmetric coarse solve from the packed upper tile triangle of E^-1 (32 x 32 tiles)
+long long symv_tiles(int d);
+void launch_symv_pack(const double* Einv, int d, int ld, double* P, cudaStream_t s);
+void launch_symv(const double* P, int d, const double* x, double* rowpart, double* colpart,
+                 double* y, const int* gate, cudaStream_t s);
+int coarse_is_symmetric(const double* E, int d, int ld, cudaStream_t s);
 // E (d x d, ld) = Z^T A_p Z, deterministic.  Returns 0 or a cuda error code.
 int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const RunMap& rm,
                  double* E, int ld, double* scratch_q, cudaStream_t s);

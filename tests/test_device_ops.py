@@ -134,3 +134,11 @@ def test_large_coarse_system_lu_matches_numpy(gpu):
     ref = np.linalg.inv(E)
     assert rel(Einv, ref) < 1e-10
     np.testing.assert_allclose(E, E.T, rtol=0, atol=1e-12 * np.abs(E).max())
+    # the projector through the symmetric packed coarse solve (d >= 256) vs the oracle
+    off, dg = A.dia()
+    Ac = O.csr_from_dia(A.n, off, dg)
+    defl = O.LabelDeflation(Ac, lab, 1500, b, 1.0 / A.diagonal())
+    v = np.random.default_rng(3).standard_normal(A.n)
+    assert rel(ctx.apply_p1(v), defl.apply_p1(v)) < 1e-10
+    assert rel(ctx.apply_p2(v), defl.apply_p2(v)) < 1e-10
+    np.testing.assert_allclose(ctx.x_star, defl.x_star, rtol=1e-9, atol=1e-12)
