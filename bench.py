@@ -300,6 +300,9 @@ def run_ours(args, world, rank, local, pg):
                           "bytes_per_iter": tot_bytes / max(iters_per_solve, 1),
                           "note": "all kernel classes of one event-profiled solve"}
     share = {kname: v["ms"] / (tot_s * 1e3) for kname, v in prof.items()}
+    kernel_avg = {kname: {"us": 1e3 * v["ms"] / v["launches"], "launches": v["launches"],
+                          "GB/s": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None}
+                  for kname, v in prof.items()}
     # ---------------- e2e through the public API with host buffers ----------------------
     off, dg = A.dia()
     e2e_its = 0
@@ -347,7 +350,7 @@ def run_ours(args, world, rank, local, pg):
                     "path": "paper_1510_02148_b200.pdgmres on host numpy arrays (operator "
                             "upload + E setup + solve + x download)"},
             "roofline": roofline, "iteration_roofline": iteration_roofline,
-            "kernel_share": share,
+            "kernel_share": share, "kernel_avg": kernel_avg,
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -51,16 +51,20 @@ enum ProfClass {
   PC_CYCLE,
   PC_XUPDATE,
   PC_RESTART,
+  PC_COARSE_REDUCE,
   PC_COUNT
 };
 const char* kProfNames[PC_COUNT] = {"stencil_restrict", "restrict_final", "coarse_gemv",
                                     "prolong_dots",     "gs_update",      "gs_reorth",
-                                    "cycle_end",        "x_update",       "restart"};
+                                    "cycle_end",        "x_update",       "restart",
+                                    "coarse_reduce"};
 
 unsigned long long g_ctx_serial = 0;
 
 // below this many deflation columns E^-1 is L2-resident and the plain GEMV is used
 constexpr int kSymvMinD = 256;
+// the packed solve stages s in shared memory next to its tile buffers (227 KB per CTA)
+constexpr int kSymvMaxD = 12288;
 
 }  // namespace
 
@@ -128,6 +132,7 @@ struct dk_defl {
   double* run_part = nullptr;
   int* lab_run_ptr = nullptr;
   int* lab_runs = nullptr;
+  int* long_ids = nullptr;
   long long nruns = 0, nlabelled = 0;
   double* E = nullptr;
   double* Einv = nullptr;
@@ -137,12 +142,17 @@ struct dk_defl {
   double* s = nullptr;
   double* y = nullptr;
   double* qv_base = nullptr;
+  double* own_base = nullptr;           // compact prolongation (k_prolong_setup)
+  unsigned char* mask_base = nullptr;
+  Prolong pro{};
   // symmetric coarse solve (E symmetric): packed upper tile triangle of E^-1 + partials
   int sym = 0;
   long long ntiles = 0;
   double* P = nullptr;
   double* rowpart = nullptr;
   double* colpart = nullptr;
+  int* seg_ptr = nullptr;   // row-part segment slots per tile row
+  int* seg_slot = nullptr;
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
 };
@@ -312,9 +322,13 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
   {
     if (c->sym) {
       // packed tiles + column partials written and read back
-      ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)c->ntiles + 512.0 * (double)c->ntiles);
-      launch_symv(c->P, c->d, c->s, c->rowpart, c->colpart, c->y, gate, op->stream);
-      op->launches += 1;
+      {
+        ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)c->ntiles + 256.0 * (double)c->ntiles);
+        launch_symv(c->P, c->d, c->s, c->rowpart, c->colpart, c->y, gate, op->stream);
+      }
+      ProfScope ps(op, PC_COARSE_REDUCE, 256.0 * (double)c->ntiles);
+      launch_symv_reduce(c->d, c->rowpart, c->colpart, c->seg_ptr, c->seg_slot, c->y, gate,
+                         op->stream);
     } else {
       ProfScope ps(op, PC_GEMV, 8.0 * (double)c->d * c->ld);
       launch_gemv(c->Einv, c->d, c->ld, c->s, c->y, gate, op->stream);
@@ -338,7 +352,7 @@ void issue_restart(dk_op* op, dk_defl* c) {
                    &st->running, op->stream);
   }
   ProfScope ps(op, PC_RESTART, c ? (8.0 * op->nstore + 20.0) * n : 16.0 * n);
-  launch_project(PJ_RESTART, c != nullptr, am, Aam, c ? c->lab : nullptr, c ? c->y : nullptr,
+  launch_project(PJ_RESTART, c != nullptr, am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                  op->w, op->V_base + op->guard, nullptr, op->vstride, 0, op->n_pad, op->part,
                  op->G, op->sc, 0, &st->running, op->stream);
 }
@@ -365,7 +379,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   {
     ProfScope ps(op, PC_PROJECT,
                  c ? (8.0 * op->nstore + 20.0 + 8.0 * nvec) * n : (8.0 + 8.0 * nvec) * n);
-    launch_project(PJ_ITER, c != nullptr, am, Aam, c ? c->lab : nullptr, c ? c->y : nullptr,
+    launch_project(PJ_ITER, c != nullptr, am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                    op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
                    &st->active, op->stream);
   }
@@ -380,7 +394,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   }
   {
     ProfScope ps(op, PC_REORTH, (16.0 + 16.0 * nvec) * n);
-    launch_project(PJ_REDOTS, false, false, A, nullptr, nullptr,
+    launch_project(PJ_REDOTS, false, false, A, Prolong{}, nullptr,
                    V + (long long)(j + 1) * op->vstride, nullptr, V, op->vstride, nvec, op->n_pad,
                    op->part, op->G, op->sc, j, &st->reorth, op->stream);
     launch_gs(true, V + (long long)(j + 1) * op->vstride, V + (long long)(j + 1) * op->vstride, V,
@@ -412,13 +426,21 @@ int build_graph(dk_op* op, dk_defl* c, int m) {
     op->gexec = nullptr;
   }
   cudaGraph_t g;
+  launch_error() = cudaSuccess;
   DK_TRY(cudaStreamBeginCapture(op->stream, cudaStreamCaptureModeThreadLocal));
+  pdl_skip_next() = true;
   const int l0 = op->launches;
   issue_restart(op, c);
   for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
   issue_cycle_end(op);
   op->launches = l0;
-  DK_TRY(cudaStreamEndCapture(op->stream, &g));
+  {
+    const cudaError_t le = launch_error();
+    launch_error() = cudaSuccess;
+    const cudaError_t ce = cudaStreamEndCapture(op->stream, &g);
+    if (le != cudaSuccess) return cuda_fail(le, "kernel launch during graph capture");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+  }
   cudaError_t e = cudaGraphInstantiate(&op->gexec, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
@@ -788,12 +810,35 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   c->xs = c->xs_base + op->guard;
   DKD(cudaMalloc(&c->qv_base, (size_t)op->vlen * sizeof(double)));
   DKD(cudaMemsetAsync(c->qv_base, 0, (size_t)op->vlen * sizeof(double), s));
+  DKD(cudaMalloc(&c->own_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMemsetAsync(c->own_base, 0, (size_t)op->vlen * sizeof(double), s));
+  DKD(cudaMalloc(&c->mask_base, (size_t)op->vlen));
+  DKD(cudaMemsetAsync(c->mask_base, 0, (size_t)op->vlen, s));
+  c->pro.lab = c->lab;
+  c->pro.own = c->own_base + op->guard;
+  c->pro.mask = c->mask_base + op->guard;
+  launch_prolong_setup(ap_choice == DK_AP_AM, make_dia(op, ap_choice == DK_AP_AM), c->lab, n_pad,
+                       c->own_base + op->guard, c->mask_base + op->guard, s);
+  DKD(cudaGetLastError());
   c->rm.lab = c->lab;
   c->rm.tile_run_off = c->tile_run_off;
   c->rm.run_part = c->run_part;
   c->rm.lab_run_ptr = c->lab_run_ptr;
   c->rm.lab_runs = c->lab_runs;
   c->rm.d = d;
+  {
+    std::vector<int> long_ids;
+    for (int L = 0; L < d; ++L)
+      if (ptr[L + 1] - ptr[L] > kShortRuns) long_ids.push_back(L);
+    c->rm.nlong = (int)long_ids.size();
+    if (!long_ids.empty()) {
+      DKD(cudaMalloc(&c->long_ids, long_ids.size() * sizeof(int)));
+      DKD(cudaMemcpyAsync(c->long_ids, long_ids.data(), long_ids.size() * sizeof(int),
+                          cudaMemcpyHostToDevice, s));
+      DKD(cudaStreamSynchronize(s));
+    }
+    c->rm.long_ids = c->long_ids;
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -819,7 +864,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     return fail(DK_ESINGULAR, "zero pivot in LU factorization");
   }
   // symmetric E (symmetric A, A_p = A): stream only the upper tile triangle of E^-1
-  if (d >= kSymvMinD && !am && coarse_is_symmetric(c->E, d, c->ld, s)) {
+  if (d >= kSymvMinD && d <= kSymvMaxD && !am && coarse_is_symmetric(c->E, d, c->ld, s)) {
     c->sym = 1;
     c->ntiles = symv_tiles(d);
     DKD(cudaMalloc(&c->P, (size_t)c->ntiles * 1024 * sizeof(double)));
@@ -827,6 +872,14 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     DKD(cudaMalloc(&c->colpart, (size_t)c->ntiles * 32 * sizeof(double)));
     launch_symv_pack(c->Einv, d, c->ld, c->P, s);
     DKD(cudaGetLastError());
+    std::vector<int> sp, ss;
+    symv_segments(d, sp, ss);
+    DKD(cudaMalloc(&c->seg_ptr, sp.size() * sizeof(int)));
+    DKD(cudaMalloc(&c->seg_slot, ss.size() * sizeof(int)));
+    DKD(cudaMemcpyAsync(c->seg_ptr, sp.data(), sp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    DKD(cudaMemcpyAsync(c->seg_slot, ss.data(), ss.size() * sizeof(int), cudaMemcpyHostToDevice,
+                        s));
+    DKD(cudaStreamSynchronize(s));
   }
   // x* = Z E^-1 Z^T b  (deflation.py:88)
   cudaEventRecord(e0, s);
@@ -855,7 +908,8 @@ int dk_defl_destroy(dk_defl* c) {
   if (c->op) cudaStreamSynchronize(c->op->stream);
   void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->lab_runs,
                   c->E,        c->Einv,         c->piv,      c->xs_base,     c->s,
-                  c->y,        c->qv_base,      c->P,        c->rowpart,     c->colpart};
+                  c->y,        c->qv_base,      c->P,        c->rowpart,     c->colpart,
+                  c->own_base, c->mask_base,    c->seg_ptr,  c->seg_slot,    c->long_ids};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete c;
@@ -869,7 +923,7 @@ int dk_defl_apply_p1(dk_defl* c, const double* v, double* out) {
   if (rc) return rc;
   coarse_solve(op, c, ST_IDENT, false, false, op->t, nullptr, nullptr, nullptr, nullptr);
   const bool am = c->ap == DK_AP_AM;
-  launch_project(PJ_PLAIN, true, am, make_dia(op, am), c->lab, c->y, op->t, op->w, nullptr, 0, 0,
+  launch_project(PJ_PLAIN, true, am, make_dia(op, am), c->pro, c->y, op->t, op->w, nullptr, 0, 0,
                  op->n_pad, op->part, op->G, op->sc, 0, op->one, op->stream);
   DK_TRY(cudaGetLastError());
   rc = download(op, out, op->w, op->n);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <vector>
 
 #include "dk_launch.h"
 
@@ -29,6 +30,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(const double* __restrict_
                                                        const double* __restrict__ x,
                                                        double* __restrict__ y, int rows_per_cta,
                                                        const int* __restrict__ gate) {
+  pdl_wait();
   if (gate != nullptr && *gate == 0) return;
   extern __shared__ double sx[];
   __shared__ double red[kGemvRowsAtOnce][kGemvSplit];
@@ -96,9 +98,11 @@ void launch_gemv(const double* M, int d, int ld, const double* x, double* y, con
       cudaFuncSetAttribute(k_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr_set = true;
     }
-    k_gemv<true><<<grid, kGemvThreads, smem, s>>>(M, d, ld, x, y, rows_per_cta, gate);
+    launch_pdl(k_gemv<true>, dim3(grid), dim3(kGemvThreads), smem, s, M, d, ld, x, y,
+               rows_per_cta, gate);
   } else {
-    k_gemv<false><<<grid, kGemvThreads, 0, s>>>(M, d, ld, x, y, rows_per_cta, gate);
+    launch_pdl(k_gemv<false>, dim3(grid), dim3(kGemvThreads), 0, s, M, d, ld, x, y,
+               rows_per_cta, gate);
   }
 }
 
@@ -116,7 +120,6 @@ void launch_gemv(const double* M, int d, int ld, const double* x, double* y, con
 // Tile storage: [16 column pairs][32 rows][2] (one coalesced 512 B double2 load per pair).
 // ======================================================================================
 constexpr int kST = 32;                 // tile edge
-constexpr int kSymvThreads = 512;
 
 __host__ __device__ inline long long tri_start(long long I, long long nb) {
   return I * nb - I * (I - 1) / 2;      // index of tile (I, I)
@@ -145,21 +148,67 @@ __global__ void k_symv_pack(const double* __restrict__ Einv, int d, int ld, int 
   }
 }
 
-__global__ void __launch_bounds__(kSymvThreads) k_symv(const double* __restrict__ P, int d, int nb,
-                                                       const double* __restrict__ x,
-                                                       double* __restrict__ rowpart,
-                                                       double* __restrict__ colpart,
-                                                       const int* __restrict__ gate) {
+// Per-warp TMA pipeline: each warp owns kSymvStages shared-memory tile buffers filled by
+// one-lane cp.async.bulk copies (8 KB each, completion on an mbarrier), so kSymvStages - 1
+// tiles stream in while the warp reduces the current one.
+constexpr int kSymvWarps = 16, kSymvStages = 1;
+constexpr int kTileBytes = kST * kST * 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void tma_tile(void* dst, const void* src, unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"((unsigned)kTileBytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"((unsigned)kTileBytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(kSymvWarps * 32) k_symv(const double* __restrict__ P, int d,
+                                                          int nb, const double* __restrict__ x,
+                                                          double* __restrict__ rowpart,
+                                                          double* __restrict__ colpart,
+                                                          const int* __restrict__ gate) {
+  pdl_wait();
   if (gate != nullptr && *gate == 0) return;
-  extern __shared__ double sx[];  // nb * 32
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bars[kSymvWarps][kSymvStages];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  double* buf = reinterpret_cast<double*>(smem_raw) + (size_t)wl * kSymvStages * (kST * kST);
+  double* sx = reinterpret_cast<double*>(smem_raw) + (size_t)kSymvWarps * kSymvStages * kST * kST;
   for (int i = threadIdx.x; i < nb * kST; i += blockDim.x) sx[i] = i < d ? x[i] : 0.0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const long long W = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long W = (long long)gridDim.x * kSymvWarps;
+  const long long w = (long long)blockIdx.x * kSymvWarps + wl;
   const long long ntiles = (long long)nb * (nb + 1) / 2;
   const long long t0 = w * ntiles / W, t1 = (w + 1) * ntiles / W;
+  if (lane == 0)
+    for (int s = 0; s < kSymvStages; ++s) mbar_init(&bars[wl][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
   if (t0 >= t1) return;
+  if (lane == 0)
+    for (int s = 0; s < kSymvStages && t0 + s < t1; ++s)
+      tma_tile(buf + s * (kST * kST), P + (t0 + s) * (kST * kST), &bars[wl][s]);
   long long lo = 0, hi = nb - 1;
   while (lo < hi) {
     const long long mid = (lo + hi + 1) / 2;
@@ -169,17 +218,22 @@ __global__ void __launch_bounds__(kSymvThreads) k_symv(const double* __restrict_
   long long seg = t0;  // slot of the current row-part segment
   double racc = 0.0;
   for (long long t = t0; t < t1; ++t) {
-    const double2* T = reinterpret_cast<const double2*>(P + t * (kST * kST));
-    const double* xJ = sx + J * kST;
-    const double xr = sx[I * kST + lane];
-    // the whole tile row (16 x 16 B) in flight, then reused in place for the column part
+    const int s = (int)((t - t0) % kSymvStages);
+    const unsigned parity = (unsigned)(((t - t0) / kSymvStages) & 1);
+    mbar_wait(&bars[wl][s], parity);
+    const double2* T = reinterpret_cast<const double2*>(buf + s * (kST * kST));
     double cacc[32];
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
-      const double2 v = __ldg(T + p * kST + lane);
+      const double2 v = T[p * kST + lane];
       cacc[2 * p] = v.x;
       cacc[2 * p + 1] = v.y;
     }
+    __syncwarp();
+    if (lane == 0 && t + kSymvStages < t1)  // refill this stage
+      tma_tile(buf + s * (kST * kST), P + (t + kSymvStages) * (kST * kST), &bars[wl][s]);
+    const double* xJ = sx + J * kST;
+    const double xr = sx[I * kST + lane];
 #pragma unroll
     for (int c = 0; c < 32; ++c) racc = fma(cacc[c], xJ[c], racc);
 #pragma unroll
@@ -213,43 +267,60 @@ __global__ void __launch_bounds__(kSymvThreads) k_symv(const double* __restrict_
 }
 
 // y_J = sum of row-part segments of tile row J (warps in order) + sum_{I<J} column parts
-// of tiles (I, J) (I in order); 8 warps split the I range, combined in a fixed order.
-__global__ void __launch_bounds__(256) k_symv_reduce(const double* __restrict__ rowpart,
+// of tiles (I, J) (I in order); 32 warps split the I range, combined in a fixed order.
+constexpr int kRedWarps = 16;
+__global__ void __launch_bounds__(kRedWarps * 32) k_symv_reduce(const double* __restrict__ rowpart,
                                                      const double* __restrict__ colpart, int d,
-                                                     int nb, long long W,
+                                                     int nb, const int* __restrict__ seg_ptr,
+                                                     const int* __restrict__ seg_slot,
                                                      double* __restrict__ y,
                                                      const int* __restrict__ gate) {
+  pdl_wait();
   if (gate != nullptr && *gate == 0) return;
-  __shared__ double red[8][kST];
+  __shared__ double red[kRedWarps][kST];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long Jt = blockIdx.x;
-  const long long ntiles = (long long)nb * (nb + 1) / 2;
+  const int Jt = blockIdx.x;
   double acc = 0.0;
-#pragma unroll 4
-  for (long long I = warp; I < Jt; I += 8) {
-    const long long t = tri_start(I, nb) + (Jt - I);
-    acc += colpart[t * kST + lane];
+#pragma unroll 8
+  for (int I = warp; I < Jt; I += kRedWarps) {
+    const int t = (int)tri_start(I, nb) + (Jt - I);
+    acc += colpart[(size_t)t * kST + lane];
   }
   red[warp][lane] = acc;
   __syncthreads();
   if (warp == 0) {
     double s = 0.0;
-    // row-part segments of tile row Jt: one per warp range intersecting [a, b)
-    const long long a = tri_start(Jt, nb), b = a + (nb - Jt);
-    long long wl = a * W / ntiles;
-    while (wl > 0 && (wl * ntiles) / W > a) --wl;
-    while (((wl + 1) * ntiles) / W <= a) ++wl;
-    for (long long ww = wl; ww < W; ++ww) {
-      const long long r0 = ww * ntiles / W, r1 = (ww + 1) * ntiles / W;
-      if (r0 >= b) break;
-      if (r1 <= a || r0 >= r1) continue;
-      const long long slot = r0 > a ? r0 : a;
-      s += rowpart[slot * kST + lane];
-    }
-    for (int w2 = 0; w2 < 8; ++w2) s += red[w2][lane];
-    const long long row = Jt * kST + lane;
+    // row-part segments of tile row Jt (host-precomputed slots, in warp order)
+    for (int k = seg_ptr[Jt]; k < seg_ptr[Jt + 1]; ++k)
+      s += rowpart[(size_t)seg_slot[k] * kST + lane];
+    for (int w2 = 0; w2 < kRedWarps; ++w2) s += red[w2][lane];
+    const int row = Jt * kST + lane;
     if (row < d) y[row] = s;
   }
+}
+
+// Row-part segment slots per tile row for the static warp partition of k_symv: the row's
+// first tile plus every warp range start strictly inside the row.
+void symv_segments(int d, std::vector<int>& ptr, std::vector<int>& slots) {
+  const long long nb = (d + kST - 1) / kST;
+  const long long ntiles = nb * (nb + 1) / 2;
+  const long long W = 148LL * kSymvWarps;
+  std::vector<long long> starts;
+  for (long long ww = 0; ww < W; ++ww) {
+    const long long r0 = ww * ntiles / W, r1 = (ww + 1) * ntiles / W;
+    if (r0 < r1) starts.push_back(r0);
+  }
+  ptr.assign(nb + 1, 0);
+  slots.clear();
+  size_t k = 0;
+  for (long long J = 0; J < nb; ++J) {
+    const long long a = tri_start(J, nb), b = a + (nb - J);
+    ptr[J] = (int)slots.size();
+    slots.push_back((int)a);
+    while (k < starts.size() && starts[k] <= a) ++k;
+    for (size_t q = k; q < starts.size() && starts[q] < b; ++q) slots.push_back((int)starts[q]);
+  }
+  ptr[nb] = (int)slots.size();
 }
 
 // flag <- 0 unless |E_ij - E_ji| <= 1e-12 (|E_ij| + |E_ji|) for all i, j (assembly rounding)
@@ -289,16 +360,24 @@ void launch_symv_pack(const double* Einv, int d, int ld, double* P, cudaStream_t
 void launch_symv(const double* P, int d, const double* x, double* rowpart, double* colpart,
                  double* y, const int* gate, cudaStream_t s) {
   const int nb = (d + kST - 1) / kST;
-  const size_t smem = (size_t)nb * kST * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+  const size_t smem =
+      (size_t)kSymvWarps * kSymvStages * kTileBytes + (size_t)nb * kST * sizeof(double);
+  static size_t attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = smem;
   }
   const unsigned grid = 148;
-  const long long W = (long long)grid * (kSymvThreads / 32);
-  k_symv<<<grid, kSymvThreads, smem, s>>>(P, d, nb, x, rowpart, colpart, gate);
-  k_symv_reduce<<<nb, 256, 0, s>>>(rowpart, colpart, d, nb, W, y, gate);
+  launch_pdl(k_symv, dim3(grid), dim3(kSymvWarps * 32), smem, s, P, d, nb, x, rowpart, colpart,
+             gate);
+}
+
+void launch_symv_reduce(int d, const double* rowpart, const double* colpart,
+                        const int* seg_ptr, const int* seg_slot, double* y, const int* gate,
+                        cudaStream_t s) {
+  const int nb = (d + kST - 1) / kST;
+  launch_pdl(k_symv_reduce, dim3(nb), dim3(kRedWarps * 32), 0, s, rowpart, colpart, d, nb,
+             seg_ptr, seg_slot, y, gate);
 }
 
 // ======================================================================================

@@ -80,6 +80,48 @@ struct Scal {
   int m;
 };
 
+// ---- programmatic dependent launch ----------------------------------------------------
+// Every kernel of the solve sequence is launched with programmatic stream serialisation:
+// it may be scheduled while its predecessor drains, waits (griddepcontrol.wait) for the
+// predecessor's completion and memory before touching any data, and lets its own
+// successor launch once its blocks have finished their main sweep.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// first launch error since the last reset (launches inside stream capture report late)
+inline cudaError_t& launch_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+
+// set before the first launch of a stream capture: a graph's root kernel has no kernel
+// predecessor to overlap with and is launched without the programmatic attribute
+inline bool& pdl_skip_next() {
+  static thread_local bool f = false;
+  return f;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_skip_next() ? 0 : 1;
+  pdl_skip_next() = false;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) launch_error() = e;
+  return e;
+}
+
 // ---- small device helpers -------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

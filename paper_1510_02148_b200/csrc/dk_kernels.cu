@@ -24,6 +24,11 @@ namespace dk {
 // order is fixed (serial within a thread, fixed Hillis-Steele tree across threads), so the
 // result is bitwise deterministic.
 // ======================================================================================
+// shared-memory index of tile cell c: one pad slot per 8 cells, so the 8-contiguous-cell
+// reads of the scan below are 2-way instead of 16-way bank conflicted
+__device__ __forceinline__ int pidx(int c) { return c + (c >> 3); }
+constexpr int kTilePad = kTile + kTile / 8;
+
 __device__ void tile_restrict(const double* sw, const int* sl, double* out) {
   __shared__ int wf[kWarps];
   __shared__ double ws[kWarps];
@@ -34,11 +39,11 @@ __device__ void tile_restrict(const double* sw, const int* sl, double* out) {
   int lb[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    val[e] = sw[c0 + e];
-    lb[e] = sl[c0 + e];
+    val[e] = sw[9 * t + e];
+    lb[e] = sl[9 * t + e];
   }
-  const int prev = (c0 == 0) ? INT_MIN : sl[c0 - 1];
-  const int next = (c0 + 8 < kTile) ? sl[c0 + 8] : INT_MIN;
+  const int prev = (c0 == 0) ? INT_MIN : sl[pidx(c0 - 1)];
+  const int next = (c0 + 8 < kTile) ? sl[pidx(c0 + 8)] : INT_MIN;
   unsigned heads = 0;
   int nh = 0;
   double tail = 0.0;
@@ -116,12 +121,18 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
                                                       const int* __restrict__ tile_run_off,
                                                       double* __restrict__ run_part,
                                                       const int* __restrict__ gate) {
+  pdl_wait();
   if (gate != nullptr && *gate == 0) return;
-  __shared__ double sw[RESTRICT ? kTile : 2];
-  __shared__ int sl[RESTRICT ? kTile : 2];
+  __shared__ double sw[RESTRICT ? kTilePad : 2];
+  __shared__ int sl[RESTRICT ? kTilePad : 2];
+  __shared__ double wsum[kWarps];
   const long long base = (long long)blockIdx.x * kTile;
   const bool has_scale = (MODE == ST_APPLY) && scale != nullptr;
   const double sc = has_scale ? *scale : 1.0;
+  // a tile inside one region is a single run: plain block sum instead of the segmented scan
+  const bool one_run =
+      RESTRICT && (tile_run_off[blockIdx.x + 1] - tile_run_off[blockIdx.x] == 1);
+  double tsum = 0.0;
 #pragma unroll 2
   for (int k = 0; k < 4; ++k) {
     const int loc = 2 * threadIdx.x + 512 * k;
@@ -139,15 +150,31 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
           const double2 a = (A.csh[q] & 1)
                                 ? make_double2(dia_coef(A, q, i), dia_coef(A, q, i + 1))
                                 : ld2(A.co[q] + i + A.csh[q]);
-          double x0 = __ldg(v + i + o);
-          double x1 = __ldg(v + i + o + 1);
+          double x0, x1, m0 = 1.0, m1 = 1.0;
+          if ((o & 1) == 0) {  // even offset: aligned 16 B loads of the neighbour pair
+            const double2 xv = ld2(v + i + o);
+            x0 = xv.x;
+            x1 = xv.y;
+            if (PRE) {
+              const double2 mv = ld2(A.inv + i + o);
+              m0 = mv.x;
+              m1 = mv.y;
+            }
+          } else {
+            x0 = __ldg(v + i + o);
+            x1 = __ldg(v + i + o + 1);
+            if (PRE) {
+              m0 = __ldg(A.inv + i + o);
+              m1 = __ldg(A.inv + i + o + 1);
+            }
+          }
           if (has_scale) {
             x0 = __dmul_rn(x0, sc);
             x1 = __dmul_rn(x1, sc);
           }
           if (PRE) {
-            x0 = __dmul_rn(x0, __ldg(A.inv + i + o));
-            x1 = __dmul_rn(x1, __ldg(A.inv + i + o + 1));
+            x0 = __dmul_rn(x0, m0);
+            x1 = __dmul_rn(x1, m1);
           }
           r0 = __dadd_rn(r0, __dmul_rn(a.x, x0));
           r1 = __dadd_rn(r1, __dmul_rn(a.y, x1));
@@ -161,16 +188,32 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
     }
     if (WRITE) st2(out + i, make_double2(r0, r1));
     if (RESTRICT) {
-      sw[loc] = r0;
-      sw[loc + 1] = r1;
-      const int2 l = *reinterpret_cast<const int2*>(lab + i);
-      sl[loc] = l.x;
-      sl[loc + 1] = l.y;
+      if (one_run) {
+        tsum = __dadd_rn(tsum, __dadd_rn(r0, r1));
+      } else {
+        const int p = pidx(loc);
+        sw[p] = r0;
+        sw[p + 1] = r1;
+        const int2 l = *reinterpret_cast<const int2*>(lab + i);
+        sl[p] = l.x;
+        sl[p + 1] = l.y;
+      }
     }
   }
   if (RESTRICT) {
-    __syncthreads();
-    tile_restrict(sw, sl, run_part + tile_run_off[blockIdx.x]);
+    if (one_run) {
+      tsum = warp_sum(tsum);
+      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tsum;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
+        run_part[tile_run_off[blockIdx.x]] = s;
+      }
+    } else {
+      __syncthreads();
+      tile_restrict(sw, sl, run_part + tile_run_off[blockIdx.x]);
+    }
   }
 }
 
@@ -179,9 +222,9 @@ static void stencil_t(const Dia& A, long long n_pad, const double* v, const doub
                       const double* b, double* out, const RunMap* rm, const int* gate,
                       cudaStream_t s) {
   const unsigned grid = (unsigned)(n_pad / kTile);
-  k_stencil<MODE, PRE, R, W><<<grid, kThreads, 0, s>>>(
-      A, v, scale, b, out, rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
-      rm ? rm->run_part : nullptr, gate);
+  launch_pdl(k_stencil<MODE, PRE, R, W>, dim3(grid), dim3(kThreads), 0, s, A, v, scale, b, out,
+             rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
+             rm ? rm->run_part : nullptr, gate);
 }
 
 template <int MODE, bool PRE>
@@ -216,12 +259,28 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
 __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __restrict__ run_part,
                                                              const int* __restrict__ ptr,
                                                              const int* __restrict__ runs, int d,
+                                                             const int* __restrict__ long_ids,
+                                                             int nlong, int short_blocks,
                                                              double* __restrict__ s,
                                                              const int* __restrict__ gate) {
+  pdl_wait();
   if (gate != nullptr && *gate == 0) return;
-  const int L = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  if ((int)blockIdx.x < short_blocks) {
+    // one thread per column with at most kShortRuns runs, serial in run order
+    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    if (L >= d) return;
+    const int lo = ptr[L], hi = ptr[L + 1];
+    if (hi - lo > kShortRuns) return;
+    double acc = 0.0;
+    for (int k = lo; k < hi; ++k) acc += __ldcg(run_part + runs[k]);
+    s[L] = acc;
+    return;
+  }
+  // one warp per long column (lane-strided, fixed xor tree)
+  const int wl = ((blockIdx.x - short_blocks) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (L >= d) return;
+  if (wl >= nlong) return;
+  const int L = long_ids[wl];
   double acc = 0.0;
   const int lo = ptr[L], hi = ptr[L + 1];
   for (int k = lo + lane; k < hi; k += 32) acc += __ldcg(run_part + runs[k]);
@@ -231,10 +290,11 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
 
 void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s) {
   if (rm.d <= 0) return;
-  const long long threads = (long long)rm.d * 32;
-  const unsigned grid = (unsigned)((threads + kThreads - 1) / kThreads);
-  k_restrict_final<<<grid, kThreads, 0, s>>>(rm.run_part, rm.lab_run_ptr, rm.lab_runs, rm.d, s_out,
-                                             gate);
+  const int short_blocks = (rm.d + kThreads - 1) / kThreads;
+  const unsigned grid =
+      (unsigned)(short_blocks + ((long long)rm.nlong * 32 + kThreads - 1) / kThreads);
+  launch_pdl(k_restrict_final, dim3(grid), dim3(kThreads), 0, s, rm.run_part, rm.lab_run_ptr,
+             rm.lab_runs, rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, gate);
 }
 
 // ======================================================================================
@@ -362,39 +422,104 @@ __device__ void finish_iteration_block(const Scal& sc, int j, double hj1, double
 //     V^T (w - V h) = h - G h.
 // The test is evaluated up to O(eps ||w||), eight orders below its threshold.
 // ======================================================================================
+// Prolongation (A_p Z y)_i = sum over the row's coefficients of y[label of the column].
+// Precomputed per cell (k_prolong_setup): own = sum of the coefficients whose column carries
+// the cell's own label, and an 8-bit mask of the diagonals whose column carries another
+// label.  Interior cells of a region (mask 0) then cost one coefficient and one gather.
 template <bool AM>
-__device__ __forceinline__ double prolong_cell(const Dia& A, const int* __restrict__ lab,
-                                               const double* __restrict__ yc, long long c) {
-  double t = 0.0;
+__device__ __forceinline__ double prolong_cell(const Dia& A, const Prolong& P,
+                                               const double* __restrict__ yc, long long c,
+                                               int L, double own, unsigned msk) {
+  double t = (L >= 0) ? __dmul_rn(own, __ldg(yc + L)) : 0.0;
+  if (msk) {
 #pragma unroll
-  for (int q = 0; q < kMaxDiag; ++q) {
-    if (q < A.ndiag) {
-      const long long o = A.off[q];
-      const int L = __ldg(lab + c + o);
-      if (L >= 0) {
+    for (int q = 0; q < kMaxDiag; ++q) {
+      if ((msk >> q) & 1u) {
+        const long long o = A.off[q];
         double a = dia_coef(A, q, c);
         if (AM) a = __dmul_rn(a, __ldg(A.inv + c + o));
-        t = __dadd_rn(t, __dmul_rn(a, __ldg(yc + L)));
+        t = __dadd_rn(t, __dmul_rn(a, __ldg(yc + __ldg(P.lab + c + o))));
       }
     }
   }
   return t;
 }
 
+template <bool AM>
+__global__ void k_prolong_setup(Dia A, const int* __restrict__ lab, long long n_pad,
+                                double* __restrict__ own, unsigned char* __restrict__ mask) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int L = lab[i];
+    double s = 0.0;
+    unsigned m = 0;
+    for (int q = 0; q < A.ndiag; ++q) {
+      const int L2 = lab[i + A.off[q]];
+      if (L2 < 0) continue;
+      if (L2 == L) {
+        double a = dia_coef(A, q, i);
+        if (AM) a = __dmul_rn(a, A.inv[i + A.off[q]]);
+        s = __dadd_rn(s, a);
+      } else {
+        m |= 1u << q;
+      }
+    }
+    own[i] = s;
+    mask[i] = (unsigned char)m;
+  }
+}
+
+void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad, double* own,
+                          unsigned char* mask, cudaStream_t s) {
+  if (am) k_prolong_setup<true><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, mask);
+  else k_prolong_setup<false><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, mask);
+}
+
 __device__ __forceinline__ double gram_at(const double* Gm, int m, int i, int k) {
   return i <= k ? Gm[(size_t)k * (m + 1) + i] : Gm[(size_t)i * (m + 1) + k];
 }
 
+// Warp reduce-scatter of 8 per-lane values: returns, in lanes with (lane & 3) == 0, the warp
+// sum of value (lane >> 2).  9 shuffles instead of 8 x 5; fixed order (deterministic).
+__device__ __forceinline__ double reduce8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = (lane & 16) != 0;
+    const double send = up ? v[i] : v[i + 4];
+    const double keep = up ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = (lane & 8) != 0;
+    const double send = up ? v[i] : v[i + 2];
+    const double keep = up ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool up = (lane & 4) != 0;
+    const double send = up ? v[0] : v[1];
+    const double keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
 template <int MODE, bool DEFL, bool AM>
-__global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restrict__ lab,
+__global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
                                                       const double* __restrict__ yc,
                                                       const double* w_in, double* w_out,
                                                       const double* __restrict__ V,
                                                       long long vstride, int nvec, long long n_pad,
                                                       double* __restrict__ part, int G, Scal sc,
                                                       int j, const int* __restrict__ gate) {
+  pdl_wait();
   if (*gate == 0) return;
   extern __shared__ double red[];  // [nq][kWarps]
+  __shared__ __align__(16) double s_w[(MODE == PJ_ITER || MODE == PJ_REDOTS) ? kChunk : 2];
+  __shared__ __align__(16) double s_vj[MODE == PJ_ITER ? kChunk : 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // quantities: ITER: h[nvec], g[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
   const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
@@ -411,8 +536,11 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
       const long long i = cb + 512 * k;
       double2 x = (MODE == PJ_REDOTS) ? ld2cg(w_in + i) : ld2(w_in + i);
       if (DEFL) {
-        x.x = __dsub_rn(x.x, prolong_cell<AM>(A, lab, yc, i));
-        x.y = __dsub_rn(x.y, prolong_cell<AM>(A, lab, yc, i + 1));
+        const int2 L = *reinterpret_cast<const int2*>(P.lab + i);
+        const double2 ow = ld2(P.own + i);
+        const uchar2 mk = *reinterpret_cast<const uchar2*>(P.mask + i);
+        x.x = __dsub_rn(x.x, prolong_cell<AM>(A, P, yc, i, L.x, ow.x, mk.x));
+        x.y = __dsub_rn(x.y, prolong_cell<AM>(A, P, yc, i + 1, L.y, ow.y, mk.y));
       }
       w[2 * k] = x.x;
       w[2 * k + 1] = x.y;
@@ -425,50 +553,50 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
       nrm = warp_sum(nrm);
       if (lane == 0) red[nslot * kWarps + warp] += nrm;
     }
-    if (MODE == PJ_ITER) {
-      double vj[8];
+    if (MODE == PJ_ITER || MODE == PJ_REDOTS) {
+      // Stage w (and v_j) of the chunk in shared memory; the warps then stream the basis as
+      // (vector, quarter-chunk) items: 8 x 16 B loads in flight per lane and one warp
+      // reduction per 4 KB of V, instead of one per 128 B.  Item (v, q) goes to warp
+      // (4v + q) % 8 and its partial to that warp's slot: fixed order, deterministic.
+      double2* sw2 = reinterpret_cast<double2*>(s_w);
+      double2* sv2 = reinterpret_cast<double2*>(s_vj);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const double2 p = ld2(Vj + cb + 512 * k);
-        vj[2 * k] = p.x;
-        vj[2 * k + 1] = p.y;
+        sw2[threadIdx.x + 256 * k] = make_double2(w[2 * k], w[2 * k + 1]);
+        if (MODE == PJ_ITER) sv2[threadIdx.x + 256 * k] = ld2(Vj + cb + 512 * k);
       }
-#pragma unroll 2
-      for (int v = 0; v < nvec; ++v) {
-        const double* Vr = V + (long long)v * vstride + cb;
+      __syncthreads();
+      const long long c0 = ch * kChunk;
+      for (int it = warp; it < 4 * nvec; it += kWarps) {
+        const int v = it >> 2, qtr = it & 3;
+        const double* Vr = V + (long long)v * vstride + c0 + 512 * qtr + 2 * lane;
+        double2 p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p[i] = ld2(Vr + 64 * i);
         double ah = 0.0, ag = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double2 p = ld2(Vr + 512 * k);
-          ah = fma(p.x, w[2 * k], ah);
-          ah = fma(p.y, w[2 * k + 1], ah);
-          ag = fma(p.x, vj[2 * k], ag);
-          ag = fma(p.y, vj[2 * k + 1], ag);
+        for (int i = 0; i < 8; ++i) {
+          const int e = 256 * qtr + lane + 32 * i;
+          const double2 ww = sw2[e];
+          ah = fma(p[i].x, ww.x, ah);
+          ah = fma(p[i].y, ww.y, ah);
+          if (MODE == PJ_ITER) {
+            const double2 gg = sv2[e];
+            ag = fma(p[i].x, gg.x, ag);
+            ag = fma(p[i].y, gg.y, ag);
+          }
         }
         ah = warp_sum(ah);
-        ag = warp_sum(ag);
+        if (MODE == PJ_ITER) ag = warp_sum(ag);
         if (lane == 0) {
           red[v * kWarps + warp] += ah;
-          red[(nvec + v) * kWarps + warp] += ag;
+          if (MODE == PJ_ITER) red[(nvec + v) * kWarps + warp] += ag;
         }
       }
-    }
-    if (MODE == PJ_REDOTS) {
-#pragma unroll 2
-      for (int v = 0; v < nvec; ++v) {
-        const double* Vr = V + (long long)v * vstride + cb;
-        double ah = 0.0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double2 p = ld2(Vr + 512 * k);
-          ah = fma(p.x, w[2 * k], ah);
-          ah = fma(p.y, w[2 * k + 1], ah);
-        }
-        ah = warp_sum(ah);
-        if (lane == 0) red[v * kWarps + warp] += ah;
-      }
+      __syncthreads();  // the next chunk reuses s_w / s_vj
     }
   }
+  pdl_trigger();
   if (MODE == PJ_PLAIN) return;
   __syncthreads();
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
@@ -493,26 +621,37 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
     }
     return;
   }
-  // MODE == PJ_ITER
+  // MODE == PJ_ITER.  Shared scratch after red[0..2nvec]: h[nvec], G[nvec][nvec], |corr|[nvec]
   const double sj = sc.sigma[nvec - 1];
+  double* sh_h = red + 2 * nvec + 1;
+  double* sh_g = sh_h + nvec;
+  double* sh_c = sh_g + nvec * nvec;
   for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
     const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
     Hc[v] = h;
+    sh_h[v] = h;
     sc.coef[v] = h * sc.sigma[v];
-    sc.Gm[(size_t)j * (m + 1) + v] = red[nvec + v] * sc.sigma[v] * sj;
+    const double g = red[nvec + v] * sc.sigma[v] * sj;
+    sc.Gm[(size_t)j * (m + 1) + v] = g;
+    sh_g[v * nvec + (nvec - 1)] = g;
+    sh_g[(nvec - 1) * nvec + v] = g;
+  }
+  for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
+    const int i = e / (nvec - 1), k = e % (nvec - 1);
+    sh_g[i * nvec + k] = gram_at(sc.Gm, m, i, k);
   }
   __syncthreads();
-  // corr_i = h_i - sum_k G_ik h_k ; reuse red[nvec..2nvec) for |corr_i|
+  // corr_i = h_i - sum_k G_ik h_k
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    double c = Hc[i];
-    for (int k = 0; k < nvec; ++k) c -= gram_at(sc.Gm, m, i, k) * Hc[k];
-    red[nvec + i] = fabs(c);
+    double c = sh_h[i];
+    for (int k = 0; k < nvec; ++k) c -= sh_g[i * nvec + k] * sh_h[k];
+    sh_c[i] = fabs(c);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
     double mx = 0.0;
-    for (int i = 0; i < nvec; ++i) mx = fmax(mx, red[nvec + i]);
+    for (int i = 0; i < nvec; ++i) mx = fmax(mx, sh_c[i]);
     if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
       st->reorth = 1;
       st->reorths += 1;
@@ -523,19 +662,27 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, const int* __restri
 }
 
 template <int MODE, bool DEFL, bool AM>
-static void project_t(const Dia& A, const int* lab, const double* yc, const double* w_in,
+static void project_t(const Dia& A, const Prolong& lab, const double* yc, const double* w_in,
                       double* w_out, const double* V, long long vstride, int nvec,
                       long long n_pad, double* part, int G, const Scal& sc, int j,
                       const int* gate, cudaStream_t s) {
   const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
-  const int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
+  int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
+  const int tail = 4 * nvec + 1 + nvec * nvec;  // PJ_ITER re-orthogonalisation test scratch
+  if (MODE == PJ_ITER && tail > slots) slots = tail;
   const size_t smem = (size_t)slots * sizeof(double);
-  k_project<MODE, DEFL, AM><<<G, kThreads, smem, s>>>(A, lab, yc, w_in, w_out, V, vstride, nvec,
-                                                      n_pad, part, G, sc, j, gate);
+  static bool attr = false;  // one per instantiation: dynamic + 32 KB static > 48 KB default
+  if (!attr) {
+    cudaFuncSetAttribute(k_project<MODE, DEFL, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         160 * 1024);
+    attr = true;
+  }
+  launch_pdl(k_project<MODE, DEFL, AM>, dim3(G), dim3(kThreads), smem, s, A, lab, yc, w_in,
+             w_out, V, vstride, nvec, n_pad, part, G, sc, j, gate);
 }
 
 template <int MODE>
-static void project_m(bool defl, bool am, const Dia& A, const int* lab, const double* yc,
+static void project_m(bool defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                       const double* w_in, double* w_out, const double* V, long long vstride,
                       int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                       const int* gate, cudaStream_t s) {
@@ -550,7 +697,7 @@ static void project_m(bool defl, bool am, const Dia& A, const int* lab, const do
                                  gate, s);
 }
 
-void launch_project(int mode, bool defl, bool am, const Dia& A, const int* lab, const double* yc,
+void launch_project(int mode, bool defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                     const int* gate, cudaStream_t s) {
@@ -579,6 +726,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
                                                  int nvec, long long n_pad,
                                                  double* __restrict__ part, int G, Scal sc, int j,
                                                  const int* __restrict__ gate) {
+  pdl_wait();
   if (*gate == 0) return;
   extern __shared__ double sh[];
   double* cf = sh;                                  // [nvec]
@@ -597,7 +745,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
       u[2 * k] = x.x;
       u[2 * k + 1] = x.y;
     }
-#pragma unroll 4
+#pragma unroll 8
     for (int v = 0; v < nvec; ++v) {
       const double* Vr = V + (long long)v * vstride + cb;
       const double c = cf[v];
@@ -618,6 +766,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     nrm = warp_sum(nrm);
     if (lane == 0) red[warp] += nrm;
   }
+  pdl_trigger();
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
@@ -638,11 +787,11 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
   const int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
   const size_t smem = ((size_t)nvec + (size_t)slots) * sizeof(double);
   if (reorth)
-    k_gs<true><<<G, kThreads, smem, s>>>(w_in, u_out, V, vstride, nvec, n_pad, part, G, sc, j,
-                                         gate);
+    launch_pdl(k_gs<true>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
+               n_pad, part, G, sc, j, gate);
   else
-    k_gs<false><<<G, kThreads, smem, s>>>(w_in, u_out, V, vstride, nvec, n_pad, part, G, sc, j,
-                                          gate);
+    launch_pdl(k_gs<false>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
+               n_pad, part, G, sc, j, gate);
 }
 
 // ======================================================================================
@@ -651,6 +800,7 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
 // sequential loop), coefficients for x += M^-1 V y.
 // ======================================================================================
 __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
+  pdl_wait();
   State* st = sc.st;
   if (!st->cycle_open) return;
   extern __shared__ double sm[];
@@ -701,13 +851,14 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
 
 void launch_cycle_end(const Scal& sc, cudaStream_t s) {
   const size_t smem = ((size_t)sc.m * sc.m + sc.m + 1) * sizeof(double);
-  k_cycle_end<<<1, 32, smem, s>>>(sc);
+  launch_pdl(k_cycle_end, dim3(1), dim3(32), smem, s, sc);
 }
 // x += M^-1 (sum_{i<cols} y_i V_i)   (krylov.py:206)
 __global__ void __launch_bounds__(kThreads) k_xupdate(Dia A, double* __restrict__ x,
                                                       const double* __restrict__ V,
                                                       long long vstride, long long n_pad,
                                                       Scal sc) {
+  pdl_wait();
   State* st = sc.st;
   if (!st->xupdate) return;
   const int cols = st->last_cols;
@@ -738,7 +889,7 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(Dia A, double* __restrict_
 void launch_xupdate(const Dia& A, double* x, const double* V, long long vstride, long long n_pad,
                     const Scal& sc, cudaStream_t s) {
   const size_t smem = (size_t)(sc.m + 1) * sizeof(double);
-  k_xupdate<<<148 * 8, kThreads, smem, s>>>(A, x, V, vstride, n_pad, sc);
+  launch_pdl(k_xupdate, dim3(148 * 8), dim3(kThreads), smem, s, A, x, V, vstride, n_pad, sc);
 }
 
 // ======================================================================================

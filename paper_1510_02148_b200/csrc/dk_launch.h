@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "dk_internal.cuh"
 
 namespace dk {
@@ -20,7 +22,10 @@ struct RunMap {            // label-segmented restriction metadata (see DESIGN.m
   const int* lab_run_ptr;  // [d+1] CSR: runs of each label, run order
   const int* lab_runs;     // [nlabelled runs]
   int d;
+  const int* long_ids;     // columns with more than kShortRuns runs (summed by a warp)
+  int nlong;
 };
+constexpr int kShortRuns = 16;
 
 // w = (mode) ; if rm != nullptr also run sums of w.  pre: apply the Jacobi inverse.
 // scale (device scalar or nullptr) multiplies v first.  gate (device int or nullptr).
@@ -33,11 +38,20 @@ void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cud
 void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
                  cudaStream_t s);
 
+// Compact prolongation map of a deflation context (k_prolong_setup).
+struct Prolong {
+  const int* lab;             // guarded labels
+  const double* own;          // guarded: sum of a cell's coefficients into its own column
+  const unsigned char* mask;  // guarded: diagonals whose column carries another label
+};
+void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad, double* own,
+                          unsigned char* mask, cudaStream_t s);
+
 enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
 // w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w and Gram column V^T V_j, ||w_out||^2
 // -> H col j + re-orthogonalisation test; RESTART: ||w_out||^2 -> restart test;
 // REDOTS: corr = V^T u for the second Gram-Schmidt pass.  G = grid width (fixed per op).
-void launch_project(int mode, bool defl, bool am, const Dia& A, const int* lab, const double* yc,
+void launch_project(int mode, bool defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                     const int* gate, cudaStream_t s);
@@ -68,6 +82,10 @@ long long symv_tiles(int d);
 void launch_symv_pack(const double* Einv, int d, int ld, double* P, cudaStream_t s);
 void launch_symv(const double* P, int d, const double* x, double* rowpart, double* colpart,
                  double* y, const int* gate, cudaStream_t s);
+void launch_symv_reduce(int d, const double* rowpart, const double* colpart,
+                        const int* seg_ptr, const int* seg_slot, double* y, const int* gate,
+                        cudaStream_t s);
+void symv_segments(int d, std::vector<int>& ptr, std::vector<int>& slots);
 int coarse_is_symmetric(const double* E, int d, int ld, cudaStream_t s);
 // E (d x d, ld) = Z^T A_p Z, deterministic.  Returns 0 or a cuda error code.
 int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const RunMap& rm,

