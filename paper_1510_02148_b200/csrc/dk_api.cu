@@ -515,6 +515,8 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
     if (order[k].first == 0) op->center = k;
   }
   const long long nch = op->n_pad / kChunk;
+  // reduction grid: up to 4 blocks per SM stream the chunks (fixed block -> chunk map, so the
+  // per-block partial sums, and hence every reduction, are deterministic)
   op->G = (int)std::min<long long>(nch, 148 * 4);
   // all diagonals, guarded, ascending offsets
   DK_TRY(cudaMalloc(&op->dia, (size_t)ndiag * op->vlen * sizeof(double)));
