@@ -722,9 +722,90 @@ __global__ void __launch_bounds__(256) k_dgemm_sub(const double* __restrict__ Am
   }
 }
 
+// Large-tile variant: 128 x 128 block tile, 8 x 8 outputs per thread (two 4 x 4 quadrant
+// pairs so shared-memory fragments are read as 2 x 16 B), K in steps of 16 with the next
+// step's global tile prefetched into registers.  64 DFMA per 4 shared loads.
+constexpr int kBT = 128, kBK = 16;
+__global__ void __launch_bounds__(256) k_dgemm_big(const double* __restrict__ Am, int lda,
+                                                   const double* __restrict__ Bm, int ldb,
+                                                   double* __restrict__ C, int ldc, int M, int N,
+                                                   int K) {
+  __shared__ __align__(16) double sA[kBK][kBT];
+  __shared__ __align__(16) double sB[kBK][kBT];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int r0 = blockIdx.y * kBT, c0 = blockIdx.x * kBT;
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  double pa[8], pb[8];
+  auto load = [&](int kk) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + 256 * i;
+      const int ar = e >> 4, ac = e & 15;  // A tile: 128 rows x 16 k
+      const int gr = r0 + ar, gk = kk + ac;
+      pa[i] = (gr < M && gk < K) ? Am[(long long)gr * lda + gk] : 0.0;
+      const int br = e >> 7, bc = e & 127;  // B tile: 16 k x 128 cols
+      const int gbk = kk + br, gc = c0 + bc;
+      pb[i] = (gbk < K && gc < N) ? Bm[(long long)gbk * ldb + gc] : 0.0;
+    }
+  };
+  load(0);
+  for (int kk = 0; kk < K; kk += kBK) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + 256 * i;
+      sA[e & 15][e >> 4] = pa[i];
+      sB[e >> 7][e & 127] = pb[i];
+    }
+    __syncthreads();
+    if (kk + kBK < K) load(kk + kBK);
+#pragma unroll
+    for (int q = 0; q < kBK; ++q) {
+      double av[8], bv[8];
+      const double2 a0 = *reinterpret_cast<const double2*>(&sA[q][ty * 4]);
+      const double2 a1 = *reinterpret_cast<const double2*>(&sA[q][ty * 4 + 2]);
+      const double2 a2 = *reinterpret_cast<const double2*>(&sA[q][64 + ty * 4]);
+      const double2 a3 = *reinterpret_cast<const double2*>(&sA[q][64 + ty * 4 + 2]);
+      const double2 b0 = *reinterpret_cast<const double2*>(&sB[q][tx * 4]);
+      const double2 b1 = *reinterpret_cast<const double2*>(&sB[q][tx * 4 + 2]);
+      const double2 b2 = *reinterpret_cast<const double2*>(&sB[q][64 + tx * 4]);
+      const double2 b3 = *reinterpret_cast<const double2*>(&sB[q][64 + tx * 4 + 2]);
+      av[0] = a0.x; av[1] = a0.y; av[2] = a1.x; av[3] = a1.y;
+      av[4] = a2.x; av[5] = a2.y; av[6] = a3.x; av[7] = a3.y;
+      bv[0] = b0.x; bv[1] = b0.y; bv[2] = b1.x; bv[3] = b1.y;
+      bv[4] = b2.x; bv[5] = b2.y; bv[6] = b3.x; bv[7] = b3.y;
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int gr = r0 + (a < 4 ? ty * 4 + a : 64 + ty * 4 + a - 4);
+    if (gr >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int gc = c0 + (b < 4 ? tx * 4 + b : 64 + tx * 4 + b - 4);
+      if (gc < N) C[(long long)gr * ldc + gc] -= acc[a][b];
+    }
+  }
+}
+
+constexpr int kNB2 = 256;  // outer panel width of the two-level LU / triangular solves
+
 static void dgemm_sub(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
                       int M, int N, int K, cudaStream_t s) {
   if (M <= 0 || N <= 0 || K <= 0) return;
+  if (K >= 64 && (long long)M * N >= 256LL * 256) {
+    dim3 grid((N + kBT - 1) / kBT, (M + kBT - 1) / kBT);
+    k_dgemm_big<<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
+    return;
+  }
   dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT);
   k_dgemm_sub<<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
 }
@@ -849,20 +930,42 @@ int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min
   cudaMemcpyAsync(&dominant, dflag, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
   cudaFreeAsync(dflag, s);
-  for (int k = 0; k < d; k += kNB) {
-    const int nb = (d - k < kNB) ? d - k : kNB;
-    const int rest = d - k - nb;
-    if (dominant) {
-      k_diag_lu<<<1, 256, 0, s>>>(E, ld, k, nb, piv);
-      if (rest > 0) k_trsm_rows<<<(rest + 255) / 256, 256, 0, s>>>(E, d, ld, k, nb);
-    } else {
-      k_panel<<<1, 1024, 0, s>>>(E, d, ld, k, nb, piv);
-      k_laswp<<<cgrid, 256, 0, s>>>(E, d, ld, piv, k, k + nb, k, k + nb);
+  // Two-level right-looking LU: outer panels of kNB2 columns are factorised by kNB-wide
+  // steps whose rank-kNB updates stay inside the panel; the trailing matrix then receives
+  // one rank-kNB2 GEMM update per outer panel (compute-bound instead of C-traffic-bound).
+  auto at = [&](int r, int c) { return E + (long long)r * ld + c; };
+  for (int K0 = 0; K0 < d; K0 += kNB2) {
+    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
+    for (int k = K0; k < Kend; k += kNB) {
+      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
+      const int rest = d - k - nb;
+      if (dominant) {
+        k_diag_lu<<<1, 256, 0, s>>>(E, ld, k, nb, piv);
+        if (rest > 0) k_trsm_rows<<<(rest + 255) / 256, 256, 0, s>>>(E, d, ld, k, nb);
+      } else {
+        k_panel<<<1, 1024, 0, s>>>(E, d, ld, k, nb, piv);
+        k_laswp<<<cgrid, 256, 0, s>>>(E, d, ld, piv, k, k + nb, k, k + nb);
+      }
+      const int inpanel = Kend - k - nb;
+      if (inpanel > 0) {
+        k_trsm_block<false><<<(inpanel + 255) / 256, 256, 0, s>>>(E, ld, k, nb, E, ld, k + nb,
+                                                                   Kend);
+        dgemm_sub(at(k + nb, k), ld, at(k, k + nb), ld, at(k + nb, k + nb), ld, rest, inpanel,
+                  nb, s);
+      }
     }
-    if (rest > 0) {
-      k_trsm_block<false><<<(rest + 255) / 256, 256, 0, s>>>(E, ld, k, nb, E, ld, k + nb, d);
-      dgemm_sub(E + (long long)(k + nb) * ld + k, ld, E + (long long)k * ld + k + nb, ld,
-                E + (long long)(k + nb) * ld + k + nb, ld, rest, rest, nb, s);
+    const int right = d - Kend;
+    if (right > 0) {
+      // U12 = L11^-1 A12 for the columns right of the outer panel
+      for (int k = K0; k < Kend; k += kNB) {
+        const int nb = (Kend - k < kNB) ? Kend - k : kNB;
+        k_trsm_block<false><<<(right + 255) / 256, 256, 0, s>>>(E, ld, k, nb, E, ld, Kend, d);
+        if (k + nb < Kend)
+          dgemm_sub(at(k + nb, k), ld, at(k, Kend), ld, at(k + nb, Kend), ld, Kend - k - nb,
+                    right, nb, s);
+      }
+      dgemm_sub(at(Kend, K0), ld, at(K0, Kend), ld, at(Kend, Kend), ld, right, right,
+                Kend - K0, s);
     }
   }
   double* dmin = nullptr;
@@ -883,20 +986,31 @@ int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min
   // Einv = U^-1 L^-1 P I
   k_identity<<<148 * 8, 256, 0, s>>>(Einv, d, ld);
   k_laswp<<<cgrid, 256, 0, s>>>(Einv, d, ld, piv, 0, d, 0, 0);
-  for (int k = 0; k < d; k += kNB) {  // L Y = P
-    const int nb = (d - k < kNB) ? d - k : kNB;
-    k_trsm_block<false><<<cgrid, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, d);
-    const int rest = d - k - nb;
-    if (rest > 0)
-      dgemm_sub(E + (long long)(k + nb) * ld + k, ld, Einv + (long long)k * ld, ld,
-                Einv + (long long)(k + nb) * ld, ld, rest, d, nb, s);
+  auto xt = [&](int r, int c) { return Einv + (long long)r * ld + c; };
+  for (int K0 = 0; K0 < d; K0 += kNB2) {  // L Y = P, two-level
+    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
+    // without row interchanges Y = L^-1 is lower triangular: rows < Kend have nonzeros only
+    // in columns [0, Kend)
+    const int ncol = dominant ? Kend : d;
+    for (int k = K0; k < Kend; k += kNB) {
+      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
+      k_trsm_block<false><<<(ncol + 255) / 256, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, ncol);
+      if (k + nb < Kend)
+        dgemm_sub(at(k + nb, k), ld, xt(k, 0), ld, xt(k + nb, 0), ld, Kend - k - nb, ncol, nb, s);
+    }
+    if (Kend < d)
+      dgemm_sub(at(Kend, K0), ld, xt(K0, 0), ld, xt(Kend, 0), ld, d - Kend, ncol, Kend - K0, s);
   }
-  const int last = ((d - 1) / kNB) * kNB;
-  for (int k = last; k >= 0; k -= kNB) {  // U X = Y
-    const int nb = (d - k < kNB) ? d - k : kNB;
-    k_trsm_block<true><<<cgrid, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, d);
-    if (k > 0)
-      dgemm_sub(E + k, ld, Einv + (long long)k * ld, ld, Einv, ld, k, d, nb, s);
+  const int lastK0 = ((d - 1) / kNB2) * kNB2;
+  for (int K0 = lastK0; K0 >= 0; K0 -= kNB2) {  // U X = Y, two-level from the bottom
+    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
+    const int lastk = K0 + ((Kend - K0 - 1) / kNB) * kNB;
+    for (int k = lastk; k >= K0; k -= kNB) {
+      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
+      k_trsm_block<true><<<cgrid, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, d);
+      if (k > K0) dgemm_sub(at(K0, k), ld, xt(k, 0), ld, xt(K0, 0), ld, k - K0, d, nb, s);
+    }
+    if (K0 > 0) dgemm_sub(at(0, K0), ld, xt(K0, 0), ld, xt(0, 0), ld, K0, d, Kend - K0, s);
   }
   cudaEventRecord(e2, s);
   cudaStreamSynchronize(s);
