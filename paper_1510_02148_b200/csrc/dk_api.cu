@@ -108,6 +108,8 @@ struct dk_op {
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   unsigned long long g_ctx = ~0ull;
+  unsigned long long seen_ctx = ~0ull;  // (context, m) of the previous solve
+  int seen_m = -1;
   int g_m = -1;
   // profiling
   bool prof = false;
@@ -205,11 +207,11 @@ int download(dk_op* op, double* dst, const double* src, long long count) {
 
 int ensure_work(dk_op* op, int m, int max_iters) {
   if (op->v_rows < m + 1) {
-    if (op->V_base) DK_TRY(cudaFree(op->V_base));
+    if (op->V_base) DK_TRY(cudaFreeAsync(op->V_base, op->stream));
     op->V_base = nullptr;
     op->vstride = op->n_pad + op->guard;
     const size_t total = (size_t)op->guard + (size_t)(m + 1) * op->vstride;
-    DK_TRY(cudaMalloc(&op->V_base, total * sizeof(double)));
+    DK_TRY(cudaMallocAsync(&op->V_base, total * sizeof(double), op->stream));
     DK_TRY(cudaMemsetAsync(op->V_base, 0, total * sizeof(double), op->stream));
     op->v_rows = m + 1;
     op->g_m = -1;  // graph refers to the old basis
@@ -502,6 +504,14 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   dk_op* op = new dk_op();
   DK_TRY(cudaGetDevice(&op->dev));
   DK_TRY(cudaStreamCreateWithFlags(&op->own, cudaStreamNonBlocking));
+  {
+    // keep up to 16 GB of freed pool memory for the next context (E, E^-1, V are GB-sized)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, op->dev) == cudaSuccess) {
+      unsigned long long thr = 16ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   op->stream = op->own;
   op->n = n;
   op->n_pad = round_up(n, kTile);
@@ -637,8 +647,10 @@ int dk_op_destroy(dk_op* op) {
   cudaStreamSynchronize(op->stream);
   if (op->gexec) cudaGraphExecDestroy(op->gexec);
   for (auto e : op->ev_pool) cudaEventDestroy(e);
+  if (op->V_base) cudaFreeAsync(op->V_base, op->stream);
+  cudaStreamSynchronize(op->stream);
   void* bufs[] = {op->dia, op->inv_base, op->w_base, op->x_base, op->b_base, op->x0_base,
-                  op->t_base, op->V_base, op->part, op->nrm, op->tickets, op->one, op->st, op->scal,
+                  op->t_base, op->part, op->nrm, op->tickets, op->one, op->st, op->scal,
                   op->hist, op->rof};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -800,8 +812,9 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(cudaMalloc(&c->lab_runs, runs.size() * sizeof(int)));
   DKD(cudaMemcpyAsync(c->lab_runs, runs.data(), runs.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
-  DKD(cudaMalloc(&c->E, (size_t)d * c->ld * sizeof(double)));
-  DKD(cudaMalloc(&c->Einv, (size_t)d * c->ld * sizeof(double)));
+  // the O(d^2) buffers come from the stream-ordered pool (cached across contexts)
+  DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
+  DKD(cudaMallocAsync(&c->Einv, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMalloc(&c->piv, (size_t)d * sizeof(int)));
   DKD(cudaMalloc(&c->s, (size_t)c->ld * sizeof(double)));
   DKD(cudaMalloc(&c->y, (size_t)c->ld * sizeof(double)));
@@ -854,12 +867,12 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   if (err) return cleanup_fail((cudaError_t)err, "build_coarse");
   // keep a copy of E for inspection (the LU runs in place on E)
   double* Ework = nullptr;
-  DKD(cudaMalloc(&Ework, (size_t)d * c->ld * sizeof(double)));
+  DKD(cudaMallocAsync(&Ework, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMemcpyAsync(Ework, c->E, (size_t)d * c->ld * sizeof(double), cudaMemcpyDeviceToDevice,
                       s));
   double min_piv = 0.0;
   err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
-  cudaFree(Ework);
+  cudaFreeAsync(Ework, s);
   if (err) return cleanup_fail((cudaError_t)err, "lu_and_inverse");
   if (!(min_piv >= 1e-300)) {  // sparse.py:135-136 (NaN pivots are singular too)
     dk_defl_destroy(c);
@@ -869,7 +882,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   if (d >= kSymvMinD && d <= kSymvMaxD && !am && coarse_is_symmetric(c->E, d, c->ld, s)) {
     c->sym = 1;
     c->ntiles = symv_tiles(d);
-    DKD(cudaMalloc(&c->P, (size_t)c->ntiles * 1024 * sizeof(double)));
+    DKD(cudaMallocAsync(&c->P, (size_t)c->ntiles * 1024 * sizeof(double), s));
     DKD(cudaMalloc(&c->rowpart, (size_t)c->ntiles * 32 * sizeof(double)));
     DKD(cudaMalloc(&c->colpart, (size_t)c->ntiles * 32 * sizeof(double)));
     launch_symv_pack(c->Einv, d, c->ld, c->P, s);
@@ -907,13 +920,18 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
 
 int dk_defl_destroy(dk_defl* c) {
   if (!c) return DK_OK;
-  if (c->op) cudaStreamSynchronize(c->op->stream);
+  cudaStream_t s = c->op ? c->op->stream : nullptr;
+  if (c->op) cudaStreamSynchronize(s);
+  void* pooled[] = {c->E, c->Einv, c->P};  // stream-ordered pool allocations
+  for (void* p : pooled)
+    if (p) cudaFreeAsync(p, s);
   void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->lab_runs,
-                  c->E,        c->Einv,         c->piv,      c->xs_base,     c->s,
-                  c->y,        c->qv_base,      c->P,        c->rowpart,     c->colpart,
-                  c->own_base, c->mask_base,    c->seg_ptr,  c->seg_slot,    c->long_ids};
+                  c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
+                  c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->seg_ptr,
+                  c->seg_slot, c->long_ids};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  if (c->op) cudaStreamSynchronize(s);
   delete c;
   return DK_OK;
 }
@@ -1004,7 +1022,15 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
                          cudaMemcpyDeviceToDevice, op->stream));
   launch_init_state(op->sc, tol, m, max_iters, min_iters, op->stream);
   op->launches += 1;
-  if (!op->prof) {
+  // The cycle becomes a CUDA graph from the second solve with the same (context, m): a
+  // one-off solve (the public pdgmres path) launches eagerly and skips the instantiation.
+  const unsigned long long key = c ? c->serial : 0ull;
+  const bool use_graph =
+      !op->prof && ((op->gexec && op->g_m == m && op->g_ctx == key) ||
+                    (op->seen_m == m && op->seen_ctx == key));
+  op->seen_m = m;
+  op->seen_ctx = key;
+  if (use_graph) {
     rc = build_graph(op, c, m);
     if (rc) return rc;
   }
@@ -1016,9 +1042,16 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   const int per_cycle_launches = coarse_launches + 1 + m * (coarse_launches + 4) + 2;
   long long guard_cycles = (long long)max_iters + 2;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
-    if (!op->prof) {
+    if (use_graph) {
       DK_TRY(cudaGraphLaunch(op->gexec, op->stream));
       op->launches += per_cycle_launches;
+    } else if (!op->prof) {
+      const int l0 = op->launches;
+      issue_restart(op, c);
+      for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
+      issue_cycle_end(op);
+      op->launches = l0 + per_cycle_launches;
+      DK_TRY(launch_error());
     } else {
       issue_restart(op, c);
       if ((rc = read_state(op))) return rc;
