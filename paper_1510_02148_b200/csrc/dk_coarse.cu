@@ -160,15 +160,16 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void tma_tile(void* dst, const void* src, unsigned long long* bar) {
+__device__ __forceinline__ void tma_tile(void* dst, const void* src, unsigned long long* bar,
+                                         unsigned long long pol) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"((unsigned)kTileBytes)
                : "memory");
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"((unsigned)kTileBytes), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"((unsigned)kTileBytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(kSymvWarps * 32) k_symv(const double* __restri
   const long long w = (long long)blockIdx.x * kSymvWarps + wl;
   const long long ntiles = (long long)nb * (nb + 1) / 2;
   const long long t0 = w * ntiles / W, t1 = (w + 1) * ntiles / W;
+  const unsigned long long pol = l2_evict_first();
   if (lane == 0)
     for (int s = 0; s < kSymvStages; ++s) mbar_init(&bars[wl][s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(kSymvWarps * 32) k_symv(const double* __restri
   if (t0 >= t1) return;
   if (lane == 0)
     for (int s = 0; s < kSymvStages && t0 + s < t1; ++s)
-      tma_tile(buf + s * (kST * kST), P + (t0 + s) * (kST * kST), &bars[wl][s]);
+      tma_tile(buf + s * (kST * kST), P + (t0 + s) * (kST * kST), &bars[wl][s], pol);
   long long lo = 0, hi = nb - 1;
   while (lo < hi) {
     const long long mid = (lo + hi + 1) / 2;
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(kSymvWarps * 32) k_symv(const double* __restri
     }
     __syncwarp();
     if (lane == 0 && t + kSymvStages < t1)  // refill this stage
-      tma_tile(buf + s * (kST * kST), P + (t + kSymvStages) * (kST * kST), &bars[wl][s]);
+      tma_tile(buf + s * (kST * kST), P + (t + kSymvStages) * (kST * kST), &bars[wl][s], pol);
     const double* xJ = sx + J * kST;
     const double xr = sx[I * kST + lane];
 #pragma unroll

@@ -135,6 +135,21 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 __device__ __forceinline__ double2 ld2cg(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
 }
+// Streaming loads of the Krylov basis and of E^-1 (GB per iteration, each byte used once per
+// pass) carry an L2 evict-first policy so they do not push the small per-iteration vectors
+// (w, u, M^-1, labels, A's diagonals: ~70 MB at 1.1 M cells) out of the 126 MB L2.
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld2_stream(const double* ptr, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ void st2(double* p, double2 v) {
   *reinterpret_cast<double2*>(p) = v;
 }

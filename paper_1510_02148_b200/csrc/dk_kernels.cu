@@ -567,12 +567,13 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
       }
       __syncthreads();
       const long long c0 = ch * kChunk;
+      const unsigned long long pol = l2_evict_first();
       for (int it = warp; it < 4 * nvec; it += kWarps) {
         const int v = it >> 2, qtr = it & 3;
         const double* Vr = V + (long long)v * vstride + c0 + 512 * qtr + 2 * lane;
         double2 p[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) p[i] = ld2(Vr + 64 * i);
+        for (int i = 0; i < 8; ++i) p[i] = ld2_stream(Vr + 64 * i, pol);
         double ah = 0.0, ag = 0.0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -736,6 +737,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   for (int q = threadIdx.x; q < kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
+  const unsigned long long pol = l2_evict_first();
   for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long long cb = ch * kChunk + 2 * threadIdx.x;
     double u[8];
@@ -751,7 +753,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
       const double c = cf[v];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const double2 p = ld2(Vr + 512 * k);
+        const double2 p = ld2_stream(Vr + 512 * k, pol);
         u[2 * k] = __dsub_rn(u[2 * k], __dmul_rn(c, p.x));
         u[2 * k + 1] = __dsub_rn(u[2 * k + 1], __dmul_rn(c, p.y));
       }
