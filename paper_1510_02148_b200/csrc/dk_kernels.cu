@@ -507,6 +507,53 @@ __device__ __forceinline__ double reduce8(double (&v)[8], int lane) {
   return v[0];
 }
 
+// Last block of an Arnoldi projection: red[0..2nvec] holds the reduced V^T w, the reduced
+// Gram column V^T v_j and ||w||^2.  Writes the Hessenberg column, the update coefficients and
+// the Gram column, and evaluates the re-orthogonalisation test (krylov.py:162-170).
+// Shared scratch after red[0..2nvec]: h[nvec], G[nvec][nvec], |corr|[nvec].
+__device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
+  State* st = sc.st;
+  const int m = sc.m;
+  double* Hc = sc.H + (size_t)j * (m + 1);
+  const double sj = sc.sigma[nvec - 1];
+  double* sh_h = red + 2 * nvec + 1;
+  double* sh_g = sh_h + nvec;
+  double* sh_c = sh_g + nvec * nvec;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
+    Hc[v] = h;
+    sh_h[v] = h;
+    sc.coef[v] = h * sc.sigma[v];
+    const double g = red[nvec + v] * sc.sigma[v] * sj;
+    sc.Gm[(size_t)j * (m + 1) + v] = g;
+    sh_g[v * nvec + (nvec - 1)] = g;
+    sh_g[(nvec - 1) * nvec + v] = g;
+  }
+  for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
+    const int i = e / (nvec - 1), k = e % (nvec - 1);
+    sh_g[i * nvec + k] = gram_at(sc.Gm, m, i, k);
+  }
+  __syncthreads();
+  // corr_i = h_i - sum_k G_ik h_k
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    double c = sh_h[i];
+    for (int k = 0; k < nvec; ++k) c -= sh_g[i * nvec + k] * sh_h[k];
+    sh_c[i] = fabs(c);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
+    double mx = 0.0;
+    for (int i = 0; i < nvec; ++i) mx = fmax(mx, sh_c[i]);
+    if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
+      st->reorth = 1;
+      st->reorths += 1;
+    } else {
+      st->reorth = 0;
+    }
+  }
+}
+
 template <int MODE, bool DEFL, bool AM>
 __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
                                                       const double* __restrict__ yc,
@@ -622,44 +669,8 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
     }
     return;
   }
-  // MODE == PJ_ITER.  Shared scratch after red[0..2nvec]: h[nvec], G[nvec][nvec], |corr|[nvec]
-  const double sj = sc.sigma[nvec - 1];
-  double* sh_h = red + 2 * nvec + 1;
-  double* sh_g = sh_h + nvec;
-  double* sh_c = sh_g + nvec * nvec;
-  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
-    Hc[v] = h;
-    sh_h[v] = h;
-    sc.coef[v] = h * sc.sigma[v];
-    const double g = red[nvec + v] * sc.sigma[v] * sj;
-    sc.Gm[(size_t)j * (m + 1) + v] = g;
-    sh_g[v * nvec + (nvec - 1)] = g;
-    sh_g[(nvec - 1) * nvec + v] = g;
-  }
-  for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
-    const int i = e / (nvec - 1), k = e % (nvec - 1);
-    sh_g[i * nvec + k] = gram_at(sc.Gm, m, i, k);
-  }
-  __syncthreads();
-  // corr_i = h_i - sum_k G_ik h_k
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    double c = sh_h[i];
-    for (int k = 0; k < nvec; ++k) c -= sh_g[i * nvec + k] * sh_h[k];
-    sh_c[i] = fabs(c);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
-    double mx = 0.0;
-    for (int i = 0; i < nvec; ++i) mx = fmax(mx, sh_c[i]);
-    if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
-      st->reorth = 1;
-      st->reorths += 1;
-    } else {
-      st->reorth = 0;
-    }
-  }
+  (void)st;
+  iter_finish(sc, j, nvec, red);
 }
 
 template <int MODE, bool DEFL, bool AM>
