@@ -138,6 +138,23 @@ int dk_levelset_labels(int64_t nx, int64_t ny, int64_t nz, const int64_t* band, 
                        int32_t py, int32_t pz, int64_t* labels, int64_t* ncomp,
                        int64_t* comp_band);
 
+/* The same labels computed on the current device (lock-free union-find whose roots are the
+ * component minima, then a prefix scan over the roots); bit-identical to dk_levelset_labels.
+ * Pointers may be host or device memory. */
+int dk_levelset_labels_device(int64_t nx, int64_t ny, int64_t nz, const int64_t* band,
+                              int32_t px, int32_t py, int32_t pz, int64_t* labels,
+                              int64_t* ncomp, int64_t* comp_band);
+
+/* ---- operator assembly ------------------------------------------------------------- */
+/* TPFA pressure operator on the device (testbed.py:133-211 arithmetic): diags_out is 7 x n
+ * for offsets (-nx*ny, -nx, -1, 0, 1, nx, nx*ny), b_out is n.  q (sources) may be NULL.
+ * Dirichlet ghost faces are applied in the given order; face ids 0..5 = xmin, xmax, ymin,
+ * ymax, zmin, zmax (zmax is the reference's "top").  Host or device pointers. */
+int dk_assemble_tpfa(int32_t nx, int32_t ny, int32_t nz, double dx, double dy, double dz,
+                     const double* kx, const double* ky, const double* kz, const double* q,
+                     int32_t nfaces, const int32_t* face_ids, const double* face_values,
+                     double boundary_perm, double* diags_out, double* b_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1138,4 +1138,57 @@ int dk_last_basis_vector(dk_op* op, int32_t i, double* out) {
   return DK_OK;
 }
 
+int dk_levelset_labels_device(int64_t nx, int64_t ny, int64_t nz, const int64_t* band,
+                              int32_t px, int32_t py, int32_t pz, int64_t* labels,
+                              int64_t* ncomp, int64_t* comp_band) {
+  if (nx < 1 || ny < 1 || nz < 1) return fail(DK_EINVAL, "cell counts must be >= 1");
+  if (px < 1 || py < 1 || pz < 1 || px > nx || py > ny || pz > nz)
+    return fail(DK_EINVAL, "subdomain counts must be in [1, cells]");
+  if (!band || !labels || !ncomp || !comp_band) return fail(DK_EINVAL, "null argument");
+  if (nx * ny * nz >= (1ll << 31)) return fail(DK_EUNSUPPORTED, "grid too large for int32 ids");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt < 1) {
+    cudaGetLastError();
+    return fail(DK_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  cudaStream_t s;
+  DK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::string where;
+  long long nc = 0;
+  const int e = device_levelset_labels(nx, ny, nz, reinterpret_cast<const long long*>(band), px,
+                                       py, pz, reinterpret_cast<long long*>(labels), &nc,
+                                       reinterpret_cast<long long*>(comp_band), s, where);
+  cudaStreamDestroy(s);
+  if (e) return cuda_fail((cudaError_t)e, where.c_str());
+  *ncomp = nc;
+  return DK_OK;
+}
+
+int dk_assemble_tpfa(int32_t nx, int32_t ny, int32_t nz, double dx, double dy, double dz,
+                     const double* kx, const double* ky, const double* kz, const double* q,
+                     int32_t nfaces, const int32_t* face_ids, const double* face_values,
+                     double boundary_perm, double* diags_out, double* b_out) {
+  if (nx < 1 || ny < 1 || nz < 1) return fail(DK_EINVAL, "cell counts must be >= 1");
+  if (!(dx > 0 && dy > 0 && dz > 0)) return fail(DK_EINVAL, "cell sizes must be positive");
+  if (!kx || !ky || !kz || !diags_out || !b_out) return fail(DK_EINVAL, "null argument");
+  if (nfaces < 0 || nfaces > 6 || (nfaces > 0 && (!face_ids || !face_values)))
+    return fail(DK_EINVAL, "at most 6 Dirichlet faces");
+  for (int f = 0; f < nfaces; ++f)
+    if (face_ids[f] < 0 || face_ids[f] > 5) return fail(DK_EINVAL, "face id must be 0..5");
+  if ((long long)nx * ny * nz >= (1ll << 31)) return fail(DK_EUNSUPPORTED, "grid too large");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt < 1) {
+    cudaGetLastError();
+    return fail(DK_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  cudaStream_t s;
+  DK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::string where;
+  const int e = device_assemble_tpfa(nx, ny, nz, dx, dy, dz, kx, ky, kz, q, nfaces, face_ids,
+                                     face_values, boundary_perm, diags_out, b_out, s, where);
+  cudaStreamDestroy(s);
+  if (e) return cuda_fail((cudaError_t)e, where.c_str());
+  return DK_OK;
+}
+
 }  // extern "C"

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <string>
 #include <vector>
 
 #include "dk_internal.cuh"
@@ -75,6 +76,15 @@ void launch_norm(const double* v, long long n_pad, double* part, int G, unsigned
                  double* dst, cudaStream_t s);
 void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min_iters,
                        cudaStream_t s);
+
+// ---- set-up on the device (dk_setup.cu) ----
+int device_levelset_labels(long long nx, long long ny, long long nz, const long long* band_in,
+                           int px, int py, int pz, long long* labels_out, long long* ncomp,
+                           long long* comp_band_out, cudaStream_t s, std::string& err);
+int device_assemble_tpfa(int nx, int ny, int nz, double dx, double dy, double dz,
+                         const double* kx, const double* ky, const double* kz, const double* q,
+                         int nfaces, const int* face_ids, const double* face_values, double bperm,
+                         double* diags_out, double* b_out, cudaStream_t s, std::string& err);
 
 // ---- coarse operator (dk_coarse.cu) ----
 // symmetric coarse solve from the packed upper tile triangle of E^-1 (32 x 32 tiles)

@@ -168,3 +168,8 @@ if __name__ == "__main__":
     if "--big" in sys.argv:
         make_config3_labels()
         make_config2()
+
+
+# tests/golden/convergence.pdgmres.ref.csv is the reference CLI's own output for the sandwich
+# case (`defkrylov compare`, GMRES(40), levelset d=3), copied from the reference frontend
+# fixtures; make_sandwich() asserts that the reference run above reproduces its history.
