@@ -865,21 +865,43 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&c->ms[0], e0, e1);
   if (err) return cleanup_fail((cudaError_t)err, "build_coarse");
-  // keep a copy of E for inspection (the LU runs in place on E)
+  // keep a copy of E for inspection (the factorisations run in place on the copy)
+  const size_t ebytes = (size_t)d * c->ld * sizeof(double);
   double* Ework = nullptr;
-  DKD(cudaMallocAsync(&Ework, (size_t)d * c->ld * sizeof(double), s));
-  DKD(cudaMemcpyAsync(Ework, c->E, (size_t)d * c->ld * sizeof(double), cudaMemcpyDeviceToDevice,
-                      s));
-  double min_piv = 0.0;
-  err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
-  cudaFreeAsync(Ework, s);
-  if (err) return cleanup_fail((cudaError_t)err, "lu_and_inverse");
-  if (!(min_piv >= 1e-300)) {  // sparse.py:135-136 (NaN pivots are singular too)
-    dk_defl_destroy(c);
-    return fail(DK_ESINGULAR, "zero pivot in LU factorization");
+  DKD(cudaMallocAsync(&Ework, ebytes, s));
+  DKD(cudaMemcpyAsync(Ework, c->E, ebytes, cudaMemcpyDeviceToDevice, s));
+  const bool symmetric = !am && coarse_is_symmetric(c->E, d, c->ld, s);
+  bool inverted = false;
+  if (symmetric) {  // SPD E: Cholesky-based inverse (half the work of LU + solves)
+    double min_sq = 0.0;
+    err = spd_inverse(Ework, d, c->ld, c->Einv, &min_sq, &c->ms[1], &c->ms[2], s);
+    if (err) {
+      cudaFreeAsync(Ework, s);
+      return cleanup_fail((cudaError_t)err, "spd_inverse");
+    }
+    if (min_sq >= 1e-280) {  // E^-1 is in Ework: it becomes Einv, the W scratch is released
+      std::swap(Ework, c->Einv);
+      inverted = true;
+    } else {
+      DKD(cudaMemcpyAsync(Ework, c->E, ebytes, cudaMemcpyDeviceToDevice, s));
+    }
   }
+  if (!inverted) {
+    double min_piv = 0.0;
+    err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
+    if (err) {
+      cudaFreeAsync(Ework, s);
+      return cleanup_fail((cudaError_t)err, "lu_and_inverse");
+    }
+    if (!(min_piv >= 1e-300)) {  // sparse.py:135-136 (NaN pivots are singular too)
+      cudaFreeAsync(Ework, s);
+      dk_defl_destroy(c);
+      return fail(DK_ESINGULAR, "zero pivot in LU factorization");
+    }
+  }
+  cudaFreeAsync(Ework, s);
   // symmetric E (symmetric A, A_p = A): stream only the upper tile triangle of E^-1
-  if (d >= kSymvMinD && d <= kSymvMaxD && !am && coarse_is_symmetric(c->E, d, c->ld, s)) {
+  if (d >= kSymvMinD && d <= kSymvMaxD && symmetric) {
     c->sym = 1;
     c->ntiles = symv_tiles(d);
     DKD(cudaMallocAsync(&c->P, (size_t)c->ntiles * 1024 * sizeof(double), s));

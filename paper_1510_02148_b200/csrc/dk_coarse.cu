@@ -9,6 +9,8 @@
 // 8 d^2 fits in the 126 MB L2).  The inverse is formed once from the LU factors.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include <cub/cub.cuh>
 #include <vector>
 
@@ -724,88 +726,13 @@ __global__ void __launch_bounds__(256) k_dgemm_sub(const double* __restrict__ Am
   }
 }
 
-// Large-tile variant: 128 x 128 block tile, 8 x 8 outputs per thread (two 4 x 4 quadrant
-// pairs so shared-memory fragments are read as 2 x 16 B), K in steps of 16 with the next
-// step's global tile prefetched into registers.  64 DFMA per 4 shared loads.
-constexpr int kBT = 128, kBK = 16;
-__global__ void __launch_bounds__(256) k_dgemm_big(const double* __restrict__ Am, int lda,
-                                                   const double* __restrict__ Bm, int ldb,
-                                                   double* __restrict__ C, int ldc, int M, int N,
-                                                   int K) {
-  __shared__ __align__(16) double sA[kBK][kBT];
-  __shared__ __align__(16) double sB[kBK][kBT];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int r0 = blockIdx.y * kBT, c0 = blockIdx.x * kBT;
-  double acc[8][8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-  double pa[8], pb[8];
-  auto load = [&](int kk) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = tid + 256 * i;
-      const int ar = e >> 4, ac = e & 15;  // A tile: 128 rows x 16 k
-      const int gr = r0 + ar, gk = kk + ac;
-      pa[i] = (gr < M && gk < K) ? Am[(long long)gr * lda + gk] : 0.0;
-      const int br = e >> 7, bc = e & 127;  // B tile: 16 k x 128 cols
-      const int gbk = kk + br, gc = c0 + bc;
-      pb[i] = (gbk < K && gc < N) ? Bm[(long long)gbk * ldb + gc] : 0.0;
-    }
-  };
-  load(0);
-  for (int kk = 0; kk < K; kk += kBK) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = tid + 256 * i;
-      sA[e & 15][e >> 4] = pa[i];
-      sB[e >> 7][e & 127] = pb[i];
-    }
-    __syncthreads();
-    if (kk + kBK < K) load(kk + kBK);
-#pragma unroll
-    for (int q = 0; q < kBK; ++q) {
-      double av[8], bv[8];
-      const double2 a0 = *reinterpret_cast<const double2*>(&sA[q][ty * 4]);
-      const double2 a1 = *reinterpret_cast<const double2*>(&sA[q][ty * 4 + 2]);
-      const double2 a2 = *reinterpret_cast<const double2*>(&sA[q][64 + ty * 4]);
-      const double2 a3 = *reinterpret_cast<const double2*>(&sA[q][64 + ty * 4 + 2]);
-      const double2 b0 = *reinterpret_cast<const double2*>(&sB[q][tx * 4]);
-      const double2 b1 = *reinterpret_cast<const double2*>(&sB[q][tx * 4 + 2]);
-      const double2 b2 = *reinterpret_cast<const double2*>(&sB[q][64 + tx * 4]);
-      const double2 b3 = *reinterpret_cast<const double2*>(&sB[q][64 + tx * 4 + 2]);
-      av[0] = a0.x; av[1] = a0.y; av[2] = a1.x; av[3] = a1.y;
-      av[4] = a2.x; av[5] = a2.y; av[6] = a3.x; av[7] = a3.y;
-      bv[0] = b0.x; bv[1] = b0.y; bv[2] = b1.x; bv[3] = b1.y;
-      bv[4] = b2.x; bv[5] = b2.y; bv[6] = b3.x; bv[7] = b3.y;
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int gr = r0 + (a < 4 ? ty * 4 + a : 64 + ty * 4 + a - 4);
-    if (gr >= M) continue;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int gc = c0 + (b < 4 ? tx * 4 + b : 64 + tx * 4 + b - 4);
-      if (gc < N) C[(long long)gr * ldc + gc] -= acc[a][b];
-    }
-  }
-}
-
 constexpr int kNB2 = 256;  // outer panel width of the two-level LU / triangular solves
 
 static void dgemm_sub(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
                       int M, int N, int K, cudaStream_t s) {
   if (M <= 0 || N <= 0 || K <= 0) return;
-  if (K >= 64 && (long long)M * N >= 256LL * 256) {
-    dim3 grid((N + kBT - 1) / kBT, (M + kBT - 1) / kBT);
-    k_dgemm_big<<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
+  if (K >= 32 && (long long)M * N >= 256LL * 256) {  // fp64 tensor cores (dk_dense.cu)
+    gemm_mma(false, false, A, lda, B, ldb, C, ldc, M, N, K, -1.0, 1.0, 0, INT_MIN, s);
     return;
   }
   dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT);

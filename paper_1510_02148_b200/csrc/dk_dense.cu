@@ -1,0 +1,515 @@
+// dk_dense.cu — dense fp64 set-up algebra for the coarse operator E (d x d, row-major).
+//
+//   * k_dgemm_mma: C = beta C + alpha op(A) op(B) on the fp64 tensor cores (DMMA, mma.sync
+//     m16n8k4), 128 x 128 CTA tile, 8 warps of 64 x 32, K in steps of 16 through a 3-stage
+//     cp.async ring.  Options used by the factorisations: operand transposition, lower / upper
+//     tile triangle only, and a per-tile K start for a lower-triangular B (structural zeros
+//     are skipped, not multiplied).
+//   * spd_inverse: E^-1 of a symmetric positive definite E (the TPFA case: E = Z^T A Z with A
+//     SPD) by blocked Cholesky E = L L^T (lower tiles only), W = L^-1 (forward substitution
+//     exploiting W's triangle) and E^-1 = W^T W (upper tiles, K from the tile column): d^3/2
+//     multiply-adds instead of the d^3 of LU + two triangular solves.  The reference
+//     factorises E with partial-pivoting LU (sparse.py:121-145, deflation.py:86-87); the
+//     inverse is the same matrix up to rounding, and any E that is not numerically SPD goes
+//     through lu_and_inverse (dk_coarse.cu), which keeps the reference's pivoting and
+//     singularity semantics exactly.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "dk_launch.h"
+
+namespace dk {
+
+namespace {
+
+constexpr int GM = 128, GK = 16, GSTAGES = 3;
+constexpr int LDK = GK + 4;  // K-contiguous operand rows in shared memory (conflict-free)
+
+// operand tile of extent EXT (M or N) x GK per stage: K-contiguous [EXT][LDK] or
+// MN-contiguous [GK][EXT + 4] (both strides = 4 mod 16 doubles: conflict-free fragments)
+template <int EXT>
+__host__ __device__ constexpr int op_doubles() {
+  return EXT * LDK > GK * (EXT + 4) ? EXT * LDK : GK * (EXT + 4);
+}
+template <int NT>
+__host__ __device__ constexpr int gemm_smem() {
+  return GSTAGES * (op_doubles<GM>() + op_doubles<32 * NT>()) * (int)sizeof(double);
+}
+
+__device__ __forceinline__ unsigned sm32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sm32(dst)), "l"(src),
+               "r"(bytes));
+}
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Stage one GK-deep slice of an operand tile of extent EXT.  KCONT: the global operand is
+// stored with K contiguous (rows = the M or N index), else with M/N contiguous (rows = K).
+// `mn_lim` bounds the M/N index, `k_lim` the K index; invalid halves are zero-filled.
+template <bool KCONT, int EXT>
+__device__ __forceinline__ void stage_operand(double* s, const double* g, int ldg, int mn0,
+                                              int mn_lim, int k0, int k_lim) {
+  constexpr int LDM = EXT + 4;
+#pragma unroll
+  for (int i = 0; i < EXT / 32; ++i) {
+    const int e = threadIdx.x + 256 * i;  // 8 * EXT chunks of 16 B per slice
+    int mn, k, so;
+    if (KCONT) {
+      mn = e >> 3;
+      k = (e & 7) * 2;
+      so = mn * LDK + k;
+    } else {
+      k = e / (EXT / 2);
+      mn = (e % (EXT / 2)) * 2;
+      so = k * LDM + mn;
+    }
+    const int gmn = mn0 + mn, gk = k0 + k;
+    int valid;
+    const double* src;
+    if (KCONT) {
+      valid = (gmn < mn_lim) ? min(2, max(0, k_lim - gk)) : 0;
+      src = g + (long long)gmn * ldg + gk;
+    } else {
+      valid = (gk < k_lim) ? min(2, max(0, mn_lim - gmn)) : 0;
+      src = g + (long long)gk * ldg + gmn;
+    }
+    cp16(s + so, valid ? src : g, valid * 8);
+  }
+}
+
+// C[M x N] = beta C + alpha op(A) op(B), alpha != 0 (C enters the accumulators as
+// (beta / alpha) C).  TA: A is stored K x M (op = transpose); TB: B is stored N x K.
+// CTA tile 128 x (32 NT), 8 warps of 64 x (8 NT).  tri: 0 all tiles, 1 tiles touching the
+// lower triangle, 2 the upper.  With beta == 0, C may alias A (N <= tile width) or B
+// (M <= 128): a CTA then reads only the rows / columns it writes, and every operand load
+// completes before the epilogue.  kshift != INT_MIN: B is lower triangular in the sense
+// B[k][j] == 0 for k < j + kshift, so tile column c0 starts its K loop at c0 + kshift
+// (rounded down to GK).
+template <bool TA, bool TB, int NT>
+__global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
+    k_dgemm_mma(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
+                int N, int K, double alpha, double beta, int tri, int kshift) {
+  constexpr int BN = 32 * NT, LDMA = GM + 4, LDMB = BN + 4;
+  constexpr int OPA = op_doubles<GM>(), OPB = op_doubles<BN>();
+  extern __shared__ __align__(128) double smem[];
+  const int r0 = blockIdx.y * GM, c0 = blockIdx.x * BN;
+  if (tri == 1 && c0 > r0 + GM - 1) return;
+  if (tri == 2 && r0 > c0 + BN - 1) return;
+  int kbeg = 0;
+  if (kshift != INT_MIN) {
+    kbeg = c0 + kshift;
+    kbeg = kbeg < 0 ? 0 : (kbeg / GK) * GK;
+  }
+  const int nk = (K > kbeg) ? (K - kbeg + GK - 1) / GK : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * (8 * NT);
+  double acc[4][NT][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+  if (beta != 0.0) {  // C enters the accumulators (its loads overlap the operand prologue)
+    const double sc = beta / alpha;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = r0 + wm + i * 16 + g + 8 * h;
+        if (row >= M) continue;
+        const double* crow = C + (long long)row * ldc;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int col = c0 + wn + j * 8 + 2 * t;
+          if (col + 1 < N) {
+            const double2 cv = *reinterpret_cast<const double2*>(crow + col);
+            acc[i][j][2 * h] = sc * cv.x;
+            acc[i][j][2 * h + 1] = sc * cv.y;
+          } else if (col < N) {
+            acc[i][j][2 * h] = sc * crow[col];
+          }
+        }
+      }
+  }
+
+  auto load = [&](int it) {
+    double* sa = smem + (it % GSTAGES) * (OPA + OPB);
+    double* sb = sa + OPA;
+    const int k0 = kbeg + it * GK;
+    stage_operand<!TA, GM>(sa, A, lda, r0, M, k0, K);
+    stage_operand<TB, BN>(sb, B, ldb, c0, N, k0, K);
+  };
+#pragma unroll
+  for (int it = 0; it < GSTAGES - 1; ++it) {
+    if (it < nk) load(it);
+    cp_commit();
+  }
+  for (int it = 0; it < nk; ++it) {
+    cp_wait<GSTAGES - 2>();
+    __syncthreads();
+    if (it + GSTAGES - 1 < nk) load(it + GSTAGES - 1);
+    cp_commit();
+    const double* sa = smem + (it % GSTAGES) * (OPA + OPB);
+    const double* sb = sa + OPA;
+#pragma unroll
+    for (int kk = 0; kk < GK; kk += 4) {
+      double af[4][2], bf[NT];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm + i * 16 + g;
+        if (!TA) {
+          af[i][0] = sa[m * LDK + kk + t];
+          af[i][1] = sa[(m + 8) * LDK + kk + t];
+        } else {
+          af[i][0] = sa[(kk + t) * LDMA + m];
+          af[i][1] = sa[(kk + t) * LDMA + m + 8];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = wn + j * 8 + g;
+        bf[j] = TB ? sb[n * LDK + kk + t] : sb[(kk + t) * LDMB + n];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j], af[i][0], af[i][1], bf[j]);
+    }
+  }
+  cp_wait<0>();
+  // epilogue: c0,c1 at (g, 2t..2t+1), c2,c3 at (g+8, 2t..2t+1) of each 16 x 8 tile
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = r0 + wm + i * 16 + g + 8 * h;
+      if (row >= M) continue;
+      double* crow = C + (long long)row * ldc;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int col = c0 + wn + j * 8 + 2 * t;
+        if (col + 1 < N)
+          *reinterpret_cast<double2*>(crow + col) =
+              make_double2(alpha * acc[i][j][2 * h], alpha * acc[i][j][2 * h + 1]);
+        else if (col < N)
+          crow[col] = alpha * acc[i][j][2 * h];
+      }
+    }
+  }
+}
+
+template <bool TA, bool TB, int NT>
+void launch_mma(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
+                int N, int K, double alpha, double beta, int tri, int kshift, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dgemm_mma<TA, TB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         gemm_smem<NT>());
+    attr = true;
+  }
+  dim3 grid((N + 32 * NT - 1) / (32 * NT), (M + GM - 1) / GM);
+  k_dgemm_mma<TA, TB, NT><<<grid, 256, gemm_smem<NT>(), s>>>(A, lda, B, ldb, C, ldc, M, N, K,
+                                                            alpha, beta, tri, kshift);
+}
+
+template <bool TA, bool TB>
+void launch_mma_nt(int nt, const double* A, int lda, const double* B, int ldb, double* C,
+                   int ldc, int M, int N, int K, double alpha, double beta, int tri, int kshift,
+                   cudaStream_t s) {
+  if (nt == 2) launch_mma<TA, TB, 2>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+  else launch_mma<TA, TB, 4>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+}
+
+// ---- Cholesky pieces ---------------------------------------------------------------------
+constexpr int DB = 64;    // diagonal block (one CTA factorises and inverts it)
+constexpr int DNW = 8;    // warps of the diagonal-block kernel
+constexpr int GB = 256;   // blocks are grouped for the trailing updates (rank GB)
+constexpr int kDiagSmem = (DB * (DB + 1) + 5 * DB + 2) * (int)sizeof(double);
+
+template <int N>
+__device__ __forceinline__ double sel(const double (&v)[N], int k) {
+  double r = v[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) r = (k == i) ? v[i] : r;
+  return r;
+}
+
+// One CTA of 32 DNW threads: the nb x nb (nb <= DB) diagonal block at (k0, k0) of A (lower
+// triangle, already updated by the previous blocks) -> L11 = chol(block) -> L11^-1, written
+// to W[k0.., k0..] (full block, zeros above the diagonal).  L11 itself is not needed later:
+// the block column below becomes A21 L11^-T and W is built from L11^-1.
+// Warp w keeps rows RPW w .. RPW w + RPW - 1, lane l the columns l + 32 j, in registers.  The
+// block is factorised as L~ D L~^T (unit L~, right-looking, one barrier per column: the
+// owners of column c+1 publish it, and the owner of the next pivot its reciprocal, as soon as
+// step c has updated them; warps whose rows are all done sit out), then X = L~^-1 by a
+// right-looking sweep over rows, and L11^-1 = D^-1/2 X.  pmin[blk] = min pivot D_cc
+// (= L_cc^2); NaN if a pivot is not positive.
+__global__ void __launch_bounds__(32 * DNW, 1) k_chol_diag(const double* __restrict__ A, int ld,
+                                                          int k0, int nb, double* __restrict__ W,
+                                                          double* __restrict__ pmin, int blk) {
+  constexpr int RPW = DB / DNW, CPL = DB / 32;
+  extern __shared__ __align__(16) double dsm[];
+  double(*lt)[DB + 1] = reinterpret_cast<double(*)[DB + 1]>(dsm);  // L~ (unit lower)
+  double* buf = dsm + DB * (DB + 1);                                // 2 x DB columns
+  double* piv = buf + 2 * DB;                                       // D
+  double* rbuf = piv + DB;                                          // 2 x DB rows
+  double* ipb = rbuf + 2 * DB;                                      // 2 reciprocals
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, rb = RPW * w;
+  double a[RPW][CPL];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i)
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int r = rb + i, c = lane + 32 * j;
+      a[i][j] = (r < nb && c <= r) ? A[(long long)(k0 + r) * ld + k0 + c] : 0.0;
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) buf[rb + i] = a[i][0];
+  if (tid == 0) ipb[0] = 1.0 / a[0][0];
+  __syncthreads();
+  for (int c = 0; c < nb; ++c) {
+    const int n1 = c + 1;
+    if (rb + RPW - 1 > c) {  // warp-uniform: this warp still has rows below the pivot
+      const double* col = buf + (c & 1) * DB;
+      const double ip = ipb[c & 1];
+      double lr[RPW], lc[CPL];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) lr[i] = col[rb + i] * ip;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) lc[j] = col[lane + 32 * j];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        if (32 * j + 31 <= c) continue;  // warp-uniform
+        const int cc = lane + 32 * j;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i)
+          if (cc > c && cc <= rb + i) a[i][j] = fma(-lr[i], lc[j], a[i][j]);
+      }
+      if (lane < RPW && rb + lane > c) lt[rb + lane][c] = sel(lr, lane);
+      if (n1 < nb && lane == (n1 & 31)) {
+        double* nxt = buf + (n1 & 1) * DB;
+        const int q = n1 >> 5;
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const double v = sel(a[i], q);
+          nxt[rb + i] = v;
+          if (rb + i == n1) ipb[n1 & 1] = 1.0 / v;
+        }
+      }
+    }
+    if (tid == 0) piv[c] = buf[(c & 1) * DB + c];
+    __syncthreads();
+  }
+  if (tid < 32) {
+    double m = INFINITY;
+    bool bad = false;
+    for (int c = tid; c < nb; c += 32) {
+      const double p = piv[c];
+      if (!(p > 0.0)) bad = true;
+      m = fmin(m, p);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tid == 0) pmin[blk] = bad ? __longlong_as_double(0x7ff8000000000000ll) : m;
+  }
+  // X = L~^-1: row i0 is final once rows < i0 are applied; its owners publish it
+  double x[RPW][CPL];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i)
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) x[i][j] = (rb + i == lane + 32 * j) ? 1.0 : 0.0;
+  if (w == 0)
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) rbuf[lane + 32 * j] = x[0][j];
+  __syncthreads();
+  for (int i0 = 0; i0 < nb; ++i0) {
+    const int n1 = i0 + 1;
+    if (rb + RPW - 1 > i0) {
+      const double* row = rbuf + (i0 & 1) * DB;
+      double xr[CPL], lv[RPW];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) xr[j] = row[lane + 32 * j];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) lv[i] = (rb + i > i0) ? lt[rb + i][i0] : 0.0;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        if (32 * j > i0) continue;  // X[i0][col] == 0 for col > i0 (warp-uniform)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) x[i][j] = fma(-lv[i], xr[j], x[i][j]);
+      }
+      if (n1 < nb && n1 / RPW == w) {
+        double* nxt = rbuf + (n1 & 1) * DB;
+        const int q = n1 % RPW;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          double v = x[0][j];
+#pragma unroll
+          for (int i = 1; i < RPW; ++i) v = (q == i) ? x[i][j] : v;
+          nxt[lane + 32 * j] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = rb + i;
+    if (r >= nb) continue;
+    const double sc = 1.0 / sqrt(piv[r]);
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nb) W[(long long)(k0 + r) * ld + k0 + c] = (c <= r) ? x[i][j] * sc : 0.0;
+    }
+  }
+}
+
+// X[j][i] = X[i][j] for i < j (copy the upper triangle onto the lower), 32 x 32 tiles.
+__global__ void __launch_bounds__(256) k_mirror_upper(double* __restrict__ X, int d, int ld) {
+  __shared__ double tile[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = bi * 32 + r, j = bj * 32 + tx;
+    tile[r][tx] = (i < d && j < d) ? X[(long long)i * ld + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int j = bj * 32 + r, i = bi * 32 + tx;  // destination (j, i), source (i, j)
+    if (i < d && j < d && i < j) X[(long long)j * ld + i] = tile[tx][r];
+  }
+}
+
+}  // namespace
+
+int g_gemm_nt = 2;  // n8 tiles per warp of the set-up GEMM (2: 128 x 64 CTA tiles, 2 per SM)
+
+void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int ldb, double* C,
+              int ldc, int M, int N, int K, double alpha, double beta, int tri, int kshift,
+              cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  // N <= tile width: one tile column (the in-place TRSM relies on it)
+  const int nt = (N <= 64) ? 2 : (N <= 128) ? 4 : g_gemm_nt;
+  if (ta) {
+    if (tb) launch_mma_nt<true, true>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+    else launch_mma_nt<true, false>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+  } else {
+    if (tb) launch_mma_nt<false, true>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+    else launch_mma_nt<false, false>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+  }
+}
+
+int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
+                float* ms_inv, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
+    attr = true;
+  }
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventRecord(e0, s);
+  const int nblk = (d + DB - 1) / DB;
+  auto at = [&](double* X, int r, int c) { return X + (long long)r * ld + c; };
+  double* dpmin = nullptr;
+  cudaMallocAsync(&dpmin, nblk * sizeof(double), s);
+  cudaMemsetAsync(W, 0, (size_t)d * ld * sizeof(double), s);
+  // 1. E = L L^T, right-looking by DB-wide blocks in groups of GB columns: the diagonal block
+  //    is factorised and inverted by one CTA (L11^-1 lands on W's diagonal), the block column
+  //    below becomes L21 = A21 L11^-T (in place: one tile column, each CTA owns its rows);
+  //    inside a group only the group's remaining columns are updated (rank DB), and the
+  //    trailing lower triangle receives the group's rank-GB update when the group completes
+  //    (few passes over the trailing matrix).
+  for (int q = 0; q < nblk; ++q) {
+    const int K0 = q * DB, nb = (d - K0 < DB) ? d - K0 : DB, Kend = K0 + nb, rest = d - Kend;
+    const int G0 = (K0 / GB) * GB, gend = (d - G0 < GB) ? d : G0 + GB;
+    k_chol_diag<<<1, 32 * DNW, kDiagSmem, s>>>(L, ld, K0, nb, W, dpmin, q);
+    if (rest <= 0) break;
+    gemm_mma(false, true, at(L, Kend, K0), ld, at(W, K0, K0), ld, at(L, Kend, K0), ld, rest, nb,
+             nb, 1.0, 0.0, 0, INT_MIN, s);
+    if (Kend < gend)
+      gemm_mma(false, true, at(L, Kend, K0), ld, at(L, Kend, K0), ld, at(L, Kend, Kend), ld, rest,
+               gend - Kend, nb, -1.0, 1.0, 0, INT_MIN, s);
+    else
+      gemm_mma(false, true, at(L, Kend, G0), ld, at(L, Kend, G0), ld, at(L, Kend, Kend), ld, rest,
+               rest, Kend - G0, -1.0, 1.0, 1, INT_MIN, s);
+  }
+  std::vector<double> pm(nblk);
+  cudaMemcpyAsync(pm.data(), dpmin, nblk * sizeof(double), cudaMemcpyDeviceToHost, s);
+  cudaEventRecord(e1, s);
+  cudaStreamSynchronize(s);
+  cudaFreeAsync(dpmin, s);
+  double mn = INFINITY;
+  for (double v : pm) mn = (v != v || mn != mn) ? NAN : fmin(mn, v);
+  *min_diag_sq = mn;
+  if (!(mn >= 1e-280)) {  // not numerically SPD: the caller takes the LU path
+    cudaEventElapsedTime(ms_fac, e0, e1);
+    *ms_inv = 0.f;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    return (int)cudaGetLastError();
+  }
+  // 2. W = L^-1, right-looking by block rows: W[q, 0:K0] = L_qq^-1 W[q, 0:K0] (in place: one
+  //    tile row); inside a group, the group's remaining block rows receive q's contribution;
+  //    when the group completes, W[gend:, 0:gend] -= L[gend:, group] W[group, 0:gend]
+  //    (W[G0 + kk][j] == 0 for kk < j - G0: the K loop of tile column j starts there)
+  for (int q = 0; q < nblk; ++q) {
+    const int K0 = q * DB, nb = (d - K0 < DB) ? d - K0 : DB, Kend = K0 + nb, rest = d - Kend;
+    const int G0 = (K0 / GB) * GB, gend = (d - G0 < GB) ? d : G0 + GB;
+    if (K0 > 0)
+      gemm_mma(false, false, at(W, K0, K0), ld, at(W, K0, 0), ld, at(W, K0, 0), ld, nb, K0, nb,
+               1.0, 0.0, 0, INT_MIN, s);
+    if (rest <= 0) break;
+    if (Kend < gend)
+      gemm_mma(false, false, at(L, Kend, K0), ld, at(W, K0, 0), ld, at(W, Kend, 0), ld,
+               gend - Kend, Kend, nb, -1.0, 1.0, 0, -K0, s);
+    else
+      gemm_mma(false, false, at(L, Kend, G0), ld, at(W, G0, 0), ld, at(W, Kend, 0), ld, rest, Kend,
+               Kend - G0, -1.0, 1.0, 0, -G0, s);
+  }
+  // 3. E^-1 = W^T W: upper tiles into L's storage (A = W^T, B = W lower: K from the tile
+  //    column), then the lower triangle mirrored
+  gemm_mma(true, false, W, ld, W, ld, L, ld, d, d, d, 1.0, 0.0, 2, 0, s);
+  {
+    const int nt = (d + 31) / 32;
+    k_mirror_upper<<<dim3(nt, nt), 256, 0, s>>>(L, d, ld);
+  }
+  cudaEventRecord(e2, s);
+  cudaStreamSynchronize(s);
+  cudaEventElapsedTime(ms_fac, e0, e1);
+  cudaEventElapsedTime(ms_inv, e1, e2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace dk

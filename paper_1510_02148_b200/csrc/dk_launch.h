@@ -104,5 +104,16 @@ int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const R
 // min |U_kk| (host).  Returns 0 or a cuda error code.
 int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min_pivot,
                    float* ms_lu, float* ms_inv, cudaStream_t s);
+// C = beta C + alpha op(A) op(B) on the fp64 tensor cores (dk_dense.cu).  ta: A stored K x M;
+// tb: B stored N x K; tri 0/1/2 = all / lower / upper tiles; kshift (INT_MIN = off): B[k][j]
+// is structurally zero for k < j + kshift.
+void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int ldb, double* C,
+              int ldc, int M, int N, int K, double alpha, double beta, int tri, int kshift,
+              cudaStream_t s);
+// Symmetric positive definite E (in L, overwritten): Cholesky, W = L^-1 (into W), then
+// E^-1 = W^T W written back into L (full).  *min_diag_sq = min L_kk^2 (NaN if not SPD); when
+// it is below 1e-280 the inverse is not formed and the caller falls back to LU.
+int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
+                float* ms_inv, cudaStream_t s);
 
 }  // namespace dk

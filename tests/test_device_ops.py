@@ -142,3 +142,34 @@ def test_large_coarse_system_lu_matches_numpy(gpu):
     assert rel(ctx.apply_p1(v), defl.apply_p1(v)) < 1e-10
     assert rel(ctx.apply_p2(v), defl.apply_p2(v)) < 1e-10
     np.testing.assert_allclose(ctx.x_star, defl.x_star, rtol=1e-9, atol=1e-12)
+
+
+def test_large_nonsymmetric_coarse_system_lu(gpu):
+    """A_p = A M (nonsymmetric E, d = 1,500): the pivoted-LU inverse on the tensor-core GEMM."""
+    from paper_1510_02148_b200 import configs
+    c = configs.make_case(3)
+    A, b = c.problem()
+    lab = dk.partition_to_basis(c.partition()).labels.copy()
+    lab[lab >= 1500] = -1
+    ctx = dk.build_context(A, dk.Preconditioner.jacobi(A), dk.DeflationBasis(labels=lab, d=1500),
+                           b, A_p_choice="AM")
+    E, Einv = ctx.coarse_matrix()
+    assert np.abs(E - E.T).max() > 1e-8 * np.abs(E).max()
+    assert rel(Einv, np.linalg.inv(E)) < 1e-10
+
+
+def test_symmetric_indefinite_coarse_system_falls_back_to_lu(gpu):
+    """A symmetric but indefinite E fails the Cholesky attempt; the LU path inverts it."""
+    n = 3000
+    rng = np.random.default_rng(5)
+    main = rng.uniform(1.0, 2.0, n) * np.where(np.arange(n) % 3 == 0, -1.0, 1.0) * 4.0
+    off = rng.uniform(-0.5, 0.5, n)
+    A = dk.SparseMatrix.from_dia(n, [-1, 0, 1], np.vstack([np.r_[0.0, off[:-1]], main,
+                                                          np.r_[off[:-1], 0.0]]))
+    lab = (np.arange(n) // 2).astype(np.int32)  # 1,500 columns of two cells
+    ctx = dk.build_context(A, dk.Preconditioner.identity(), dk.DeflationBasis(labels=lab, d=1500),
+                           np.ones(n))
+    E, Einv = ctx.coarse_matrix()
+    np.testing.assert_array_equal(E, E.T)
+    assert np.linalg.eigvalsh(E).min() < 0 < np.linalg.eigvalsh(E).max()
+    assert rel(Einv, np.linalg.inv(E)) < 1e-10
