@@ -157,6 +157,7 @@ struct dk_defl {
   int* seg_slot = nullptr;
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
+  double nmasked = 0;  // foreign-label coefficients of the prolongation (byte accounting)
 };
 
 namespace {
@@ -216,7 +217,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
     op->v_rows = m + 1;
     op->g_m = -1;  // graph refers to the old basis
   }
-  // per-block partials: up to 2(m+1)+1 quantities (dots, Gram column, norm) per launch
+  // per-block partials: up to (m+1)+1 quantities (dots, norm) per launch
   if (op->part_q < 2 * m + 4) {
     if (op->part) DK_TRY(cudaFree(op->part));
     DK_TRY(cudaMalloc(&op->part, (size_t)(2 * m + 4) * op->G * sizeof(double)));
@@ -225,7 +226,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   }
   if (op->scal_m < m) {
     if (op->scal) DK_TRY(cudaFree(op->scal));
-    const size_t cnt = 5 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
+    const size_t cnt = 6 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
                        (size_t)(m + 1) * (m + 1);
     DK_TRY(cudaMalloc(&op->scal, cnt * sizeof(double)));
     DK_TRY(cudaMemsetAsync(op->scal, 0, cnt * sizeof(double), op->stream));
@@ -255,6 +256,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.cs = p; p += m;
   sc.sn = p; p += m;
   sc.Gm = p; p += (size_t)(m + 1) * (m + 1);
+  sc.gcol = p; p += m + 1;
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
@@ -314,7 +316,10 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
   const Dia A = make_dia(op, pre);
   const double n = (double)op->n;
   {
-    ProfScope ps(op, PC_STENCIL, (mode == ST_IDENT ? 12.0 : 8.0 * op->nstore + 20.0) * n);
+    // v, labels, the output if stored; the operator and M^-1 unless the identity
+    const double by = 12.0 + (write ? 8.0 : 0.0) +
+                      (mode == ST_IDENT ? 0.0 : 8.0 * op->nstore + (pre ? 8.0 : 0.0));
+    ProfScope ps(op, PC_STENCIL, by * n);
     launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream);
   }
   {
@@ -353,7 +358,10 @@ void issue_restart(dk_op* op, dk_defl* c) {
     launch_stencil(ST_RESID, false, true, A, op->n_pad, op->x, nullptr, op->b, op->w, nullptr,
                    &st->running, op->stream);
   }
-  ProfScope ps(op, PC_RESTART, c ? (8.0 * op->nstore + 20.0) * n : 16.0 * n);
+  // w in/out; with deflation the compact prolongation: labels 4, own 8, mask 1 per cell and
+  // one coefficient + label (+ M^-1 for A_p = AM) per foreign-label entry
+  const double pro_bytes = c ? 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked : 0.0;
+  ProfScope ps(op, PC_RESTART, 16.0 * n + pro_bytes);
   launch_project(PJ_RESTART, c != nullptr, am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                  op->w, op->V_base + op->guard, nullptr, op->vstride, 0, op->n_pad, op->part,
                  op->G, op->sc, 0, &st->running, op->stream);
@@ -370,6 +378,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   const double n = (double)op->n;
   double* V = op->V_base + op->guard;
   const int nvec = j + 1;
+  const double pro_bytes = c ? 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked : 0.0;
   if (c) {
     coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
                  nullptr, op->w, &st->active);
@@ -380,7 +389,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   }
   {
     ProfScope ps(op, PC_PROJECT,
-                 c ? (8.0 * op->nstore + 20.0 + 8.0 * nvec) * n : (8.0 + 8.0 * nvec) * n);
+                 c ? (16.0 + 8.0 * nvec) * n + pro_bytes : (8.0 + 8.0 * nvec) * n);
     launch_project(PJ_ITER, c != nullptr, am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                    op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
                    &st->active, op->stream);
@@ -832,8 +841,18 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   c->pro.lab = c->lab;
   c->pro.own = c->own_base + op->guard;
   c->pro.mask = c->mask_base + op->guard;
-  launch_prolong_setup(ap_choice == DK_AP_AM, make_dia(op, ap_choice == DK_AP_AM), c->lab, n_pad,
-                       c->own_base + op->guard, c->mask_base + op->guard, s);
+  {
+    unsigned long long* dcnt = nullptr;
+    unsigned long long hcnt = 0;
+    DKD(cudaMallocAsync(&dcnt, sizeof(unsigned long long), s));
+    DKD(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), s));
+    launch_prolong_setup(ap_choice == DK_AP_AM, make_dia(op, ap_choice == DK_AP_AM), c->lab, n_pad,
+                         c->own_base + op->guard, c->mask_base + op->guard, dcnt, s);
+    DKD(cudaMemcpyAsync(&hcnt, dcnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
+    DKD(cudaFreeAsync(dcnt, s));
+    DKD(cudaStreamSynchronize(s));
+    c->nmasked = (double)hcnt;
+  }
   DKD(cudaGetLastError());
   c->rm.lab = c->lab;
   c->rm.tile_run_off = c->tile_run_off;

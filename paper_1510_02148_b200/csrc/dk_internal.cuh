@@ -75,6 +75,8 @@ struct Scal {
   double* g;       // [m+1]
   double* y;       // [m+1]
   double* Gm;      // [(m+1)(m+1)] basis Gram matrix V^T V, column j holds rows 0..j
+  double* gcol;    // [m+1]  V^T u of the last Gram-Schmidt vector u (normalised basis rows):
+                   //        sigma_{j+1} gcol is the next Gram column (no extra pass over V)
   double* hist;    // [max_iters+1]
   int* restart_of; // [max_iters+1]
   int m;

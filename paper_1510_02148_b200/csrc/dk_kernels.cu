@@ -447,7 +447,9 @@ __device__ __forceinline__ double prolong_cell(const Dia& A, const Prolong& P,
 
 template <bool AM>
 __global__ void k_prolong_setup(Dia A, const int* __restrict__ lab, long long n_pad,
-                                double* __restrict__ own, unsigned char* __restrict__ mask) {
+                                double* __restrict__ own, unsigned char* __restrict__ mask,
+                                unsigned long long* __restrict__ nmasked) {
+  unsigned cnt = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
        i += (long long)gridDim.x * blockDim.x) {
     const int L = lab[i];
@@ -466,13 +468,18 @@ __global__ void k_prolong_setup(Dia A, const int* __restrict__ lab, long long n_
     }
     own[i] = s;
     mask[i] = (unsigned char)m;
+    cnt += __popc(m);
   }
+  // number of foreign-label coefficients (the gathers the prolongation pays beyond `own`)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nmasked, (unsigned long long)cnt);
 }
 
 void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad, double* own,
-                          unsigned char* mask, cudaStream_t s) {
-  if (am) k_prolong_setup<true><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, mask);
-  else k_prolong_setup<false><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, mask);
+                          unsigned char* mask, unsigned long long* nmasked, cudaStream_t s) {
+  if (am) k_prolong_setup<true><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, mask, nmasked);
+  else k_prolong_setup<false><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, mask, nmasked);
 }
 
 __device__ __forceinline__ double gram_at(const double* Gm, int m, int i, int k) {
@@ -507,16 +514,19 @@ __device__ __forceinline__ double reduce8(double (&v)[8], int lane) {
   return v[0];
 }
 
-// Last block of an Arnoldi projection: red[0..2nvec] holds the reduced V^T w, the reduced
-// Gram column V^T v_j and ||w||^2.  Writes the Hessenberg column, the update coefficients and
-// the Gram column, and evaluates the re-orthogonalisation test (krylov.py:162-170).
-// Shared scratch after red[0..2nvec]: h[nvec], G[nvec][nvec], |corr|[nvec].
+// Last block of an Arnoldi projection: red[0..nvec] holds the reduced V^T w and ||w||^2.
+// Writes the Hessenberg column, the update coefficients and the Gram column, and evaluates
+// the re-orthogonalisation test (krylov.py:162-170): corr = V^T u = h - G h for
+// u = w - V h.  The Gram column of v_j = sigma_j u_{j-1} is sigma_j V^T u_{j-1}, i.e. the
+// previous iteration's corr (or, after a second pass, corr2 - G corr2), kept in gcol: the
+// identity holds to rounding (~1e-13 relative, far below the 1e-8 test), and no pass over V
+// is spent on it.  Shared scratch after red[0..nvec]: h[nvec], G[nvec][nvec], |corr|[nvec].
 __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
   State* st = sc.st;
   const int m = sc.m;
   double* Hc = sc.H + (size_t)j * (m + 1);
   const double sj = sc.sigma[nvec - 1];
-  double* sh_h = red + 2 * nvec + 1;
+  double* sh_h = red + nvec + 1;
   double* sh_g = sh_h + nvec;
   double* sh_c = sh_g + nvec * nvec;
   for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
@@ -524,7 +534,7 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
     Hc[v] = h;
     sh_h[v] = h;
     sc.coef[v] = h * sc.sigma[v];
-    const double g = red[nvec + v] * sc.sigma[v] * sj;
+    const double g = (v < nvec - 1) ? sj * sc.gcol[v] : 1.0;  // |v_j| = 1
     sc.Gm[(size_t)j * (m + 1) + v] = g;
     sh_g[v * nvec + (nvec - 1)] = g;
     sh_g[(nvec - 1) * nvec + v] = g;
@@ -539,10 +549,11 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
     double c = sh_h[i];
     for (int k = 0; k < nvec; ++k) c -= sh_g[i * nvec + k] * sh_h[k];
     sh_c[i] = fabs(c);
+    sc.gcol[i] = c;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
+    st->wnorm0 = sqrt(red[nvec]);  // krylov.py:162
     double mx = 0.0;
     for (int i = 0; i < nvec; ++i) mx = fmax(mx, sh_c[i]);
     if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
@@ -566,15 +577,13 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
   if (*gate == 0) return;
   extern __shared__ double red[];  // [nq][kWarps]
   __shared__ __align__(16) double s_w[(MODE == PJ_ITER || MODE == PJ_REDOTS) ? kChunk : 2];
-  __shared__ __align__(16) double s_vj[MODE == PJ_ITER ? kChunk : 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // quantities: ITER: h[nvec], g[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
-  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
-  const int nslot = (MODE == PJ_ITER) ? 2 * nvec : 0;
+  // quantities: ITER: h[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
+  const int nq = (MODE == PJ_ITER) ? nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+  const int nslot = (MODE == PJ_ITER) ? nvec : 0;
   for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
-  const double* Vj = V + (long long)(nvec - 1) * vstride;
   for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long long cb = ch * kChunk + 2 * threadIdx.x;
     double w[8];
@@ -601,17 +610,14 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
       if (lane == 0) red[nslot * kWarps + warp] += nrm;
     }
     if (MODE == PJ_ITER || MODE == PJ_REDOTS) {
-      // Stage w (and v_j) of the chunk in shared memory; the warps then stream the basis as
+      // Stage w of the chunk in shared memory; the warps then stream the basis as
       // (vector, quarter-chunk) items: 8 x 16 B loads in flight per lane and one warp
       // reduction per 4 KB of V, instead of one per 128 B.  Item (v, q) goes to warp
       // (4v + q) % 8 and its partial to that warp's slot: fixed order, deterministic.
       double2* sw2 = reinterpret_cast<double2*>(s_w);
-      double2* sv2 = reinterpret_cast<double2*>(s_vj);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 4; ++k)
         sw2[threadIdx.x + 256 * k] = make_double2(w[2 * k], w[2 * k + 1]);
-        if (MODE == PJ_ITER) sv2[threadIdx.x + 256 * k] = ld2(Vj + cb + 512 * k);
-      }
       __syncthreads();
       const long long c0 = ch * kChunk;
       const unsigned long long pol = l2_evict_first();
@@ -621,27 +627,17 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
         double2 p[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) p[i] = ld2_stream(Vr + 64 * i, pol);
-        double ah = 0.0, ag = 0.0;
+        double ah = 0.0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int e = 256 * qtr + lane + 32 * i;
-          const double2 ww = sw2[e];
+          const double2 ww = sw2[256 * qtr + lane + 32 * i];
           ah = fma(p[i].x, ww.x, ah);
           ah = fma(p[i].y, ww.y, ah);
-          if (MODE == PJ_ITER) {
-            const double2 gg = sv2[e];
-            ag = fma(p[i].x, gg.x, ag);
-            ag = fma(p[i].y, gg.y, ag);
-          }
         }
         ah = warp_sum(ah);
-        if (MODE == PJ_ITER) ag = warp_sum(ag);
-        if (lane == 0) {
-          red[v * kWarps + warp] += ah;
-          if (MODE == PJ_ITER) red[(nvec + v) * kWarps + warp] += ag;
-        }
+        if (lane == 0) red[v * kWarps + warp] += ah;
       }
-      __syncthreads();  // the next chunk reuses s_w / s_vj
+      __syncthreads();  // the next chunk reuses s_w
     }
   }
   pdl_trigger();
@@ -662,10 +658,18 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
   }
   double* Hc = sc.H + (size_t)j * (m + 1);
   if (MODE == PJ_REDOTS) {  // second Gram-Schmidt pass coefficients (krylov.py:169-170)
+    double* cr = red + nvec;
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-      const double cr = red[v] * sc.sigma[v];
-      Hc[v] += cr;
-      sc.corr[v] = cr * sc.sigma[v];
+      cr[v] = red[v] * sc.sigma[v];
+      Hc[v] += cr[v];
+      sc.corr[v] = cr[v] * sc.sigma[v];
+    }
+    __syncthreads();
+    // V^T u' for u' = u - V corr2: corr2 - G corr2 (the next Gram column, up to sigma)
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+      double c = cr[i];
+      for (int k = 0; k < nvec; ++k) c -= gram_at(sc.Gm, m, i, k) * cr[k];
+      sc.gcol[i] = c;
     }
     return;
   }
@@ -678,9 +682,9 @@ static void project_t(const Dia& A, const Prolong& lab, const double* yc, const 
                       double* w_out, const double* V, long long vstride, int nvec,
                       long long n_pad, double* part, int G, const Scal& sc, int j,
                       const int* gate, cudaStream_t s) {
-  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+  const int nq = (MODE == PJ_ITER) ? nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
   int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
-  const int tail = 4 * nvec + 1 + nvec * nvec;  // PJ_ITER re-orthogonalisation test scratch
+  const int tail = 3 * nvec + 1 + nvec * nvec;  // PJ_ITER re-orthogonalisation test scratch
   if (MODE == PJ_ITER && tail > slots) slots = tail;
   const size_t smem = (size_t)slots * sizeof(double);
   static bool attr = false;  // one per instantiation: dynamic + 32 KB static > 48 KB default

@@ -46,7 +46,7 @@ struct Prolong {
   const unsigned char* mask;  // guarded: diagonals whose column carries another label
 };
 void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad, double* own,
-                          unsigned char* mask, cudaStream_t s);
+                          unsigned char* mask, unsigned long long* nmasked, cudaStream_t s);
 
 enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
 // w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w and Gram column V^T V_j, ||w_out||^2
