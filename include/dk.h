@@ -102,9 +102,10 @@ int dk_op_profile_read(dk_op* op, int32_t cap, const char** names, double* ms, i
 
 /* ---- deflation -------------------------------------------------------------------- */
 /* col_of_cell[i] in [0, d) is the deflation column of cell i (indicator basis), or -1 when
- * the cell belongs to no column.  Assembles E = Z^T A_p Z on the device, factorises it
- * (LU, partial pivoting; DK_ESINGULAR if min |U_kk| < 1e-300, sparse.py:135-136), forms
- * E^-1, and the coarse solution x* = Z E^-1 Z^T b.  b may be NULL (x* = 0). */
+ * the cell belongs to no column.  Assembles E = Z^T A_p Z on the device, factorises it —
+ * Cholesky when E is symmetric and numerically positive definite, otherwise LU with partial
+ * pivoting (DK_ESINGULAR if min |U_kk| < 1e-300, sparse.py:135-136) — forms E^-1 on the fp64
+ * tensor cores, and the coarse solution x* = Z E^-1 Z^T b.  b may be NULL (x* = 0). */
 int dk_defl_create(dk_defl** ctx, dk_op* op, const int32_t* col_of_cell, int32_t d,
                    int32_t ap_choice, const double* b);
 int dk_defl_destroy(dk_defl* ctx);
@@ -114,7 +115,8 @@ int dk_defl_reconstruct(dk_defl* ctx, const double* xhat, double* out); /* x* + 
 int dk_defl_x_star(dk_defl* ctx, double* out);
 /* Copies E (d x d row-major, may be NULL) and E^-1 (may be NULL) out for inspection. */
 int dk_defl_coarse(dk_defl* ctx, double* E, double* Einv);
-/* Setup timings in ms: [assemble E, LU, inverse, x*]. */
+/* Setup timings in ms: [assemble E, factorisation (Cholesky if E is SPD, else pivoted LU),
+   forming E^-1, x*]. */
 int dk_defl_setup_ms(dk_defl* ctx, double* ms4);
 
 /* ---- solver ----------------------------------------------------------------------- */

@@ -133,7 +133,7 @@ struct dk_defl {
   int* tile_run_off = nullptr;
   double* run_part = nullptr;
   int* lab_run_ptr = nullptr;
-  int* lab_runs = nullptr;
+  int* run_slot = nullptr;
   int* long_ids = nullptr;
   long long nruns = 0, nlabelled = 0;
   double* E = nullptr;
@@ -783,11 +783,14 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   for (long long r = 0; r < nruns; ++r)
     if (run_label[r] >= 0) ptr[run_label[r] + 1]++;
   for (int L = 0; L < d; ++L) ptr[L + 1] += ptr[L];
-  std::vector<int> runs(std::max(ptr[d], 1));
+  // label-major slot of every run: the stencil writes run partials there, so each column's
+  // runs are contiguous (in run order) for the restriction's final sum
+  std::vector<int> slot(std::max<long long>(nruns, 1));
   {
     std::vector<int> fillp(ptr.begin(), ptr.end() - 1);
+    int spare = ptr[d];
     for (long long r = 0; r < nruns; ++r)
-      if (run_label[r] >= 0) runs[fillp[run_label[r]]++] = (int)r;
+      slot[r] = run_label[r] >= 0 ? fillp[run_label[r]]++ : spare++;
   }
   dk_defl* c = new dk_defl();
   c->op = op;
@@ -818,8 +821,8 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(cudaMalloc(&c->lab_run_ptr, ptr.size() * sizeof(int)));
   DKD(cudaMemcpyAsync(c->lab_run_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
-  DKD(cudaMalloc(&c->lab_runs, runs.size() * sizeof(int)));
-  DKD(cudaMemcpyAsync(c->lab_runs, runs.data(), runs.size() * sizeof(int), cudaMemcpyHostToDevice,
+  DKD(cudaMalloc(&c->run_slot, slot.size() * sizeof(int)));
+  DKD(cudaMemcpyAsync(c->run_slot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
   // the O(d^2) buffers come from the stream-ordered pool (cached across contexts)
   DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
@@ -858,7 +861,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   c->rm.tile_run_off = c->tile_run_off;
   c->rm.run_part = c->run_part;
   c->rm.lab_run_ptr = c->lab_run_ptr;
-  c->rm.lab_runs = c->lab_runs;
+  c->rm.run_slot = c->run_slot;
   c->rm.d = d;
   {
     std::vector<int> long_ids;
@@ -966,7 +969,7 @@ int dk_defl_destroy(dk_defl* c) {
   void* pooled[] = {c->E, c->Einv, c->P};  // stream-ordered pool allocations
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, s);
-  void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->lab_runs,
+  void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
                   c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
                   c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->seg_ptr,
                   c->seg_slot, c->long_ids};

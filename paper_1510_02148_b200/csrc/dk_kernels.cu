@@ -20,7 +20,7 @@ namespace dk {
 // ======================================================================================
 // Segmented (run-wise) restriction of one kTile tile held in shared memory.
 // A run is a maximal range of equal labels in linear cell order; every tile start is a
-// run head.  Each run's sum is written to out[run index within the tile].  The summation
+// run head.  Each run's sum is written to out[slot[run index within the tile]].  The summation
 // order is fixed (serial within a thread, fixed Hillis-Steele tree across threads), so the
 // result is bitwise deterministic.
 // ======================================================================================
@@ -29,7 +29,8 @@ namespace dk {
 __device__ __forceinline__ int pidx(int c) { return c + (c >> 3); }
 constexpr int kTilePad = kTile + kTile / 8;
 
-__device__ void tile_restrict(const double* sw, const int* sl, double* out) {
+__device__ void tile_restrict(const double* sw, const int* sl, double* out,
+                              const int* __restrict__ slot) {
   __shared__ int wf[kWarps];
   __shared__ double ws[kWarps];
   __shared__ int wc[kWarps];
@@ -103,7 +104,7 @@ __device__ void tile_restrict(const double* sw, const int* sl, double* out) {
     run = __dadd_rn(run, val[e]);
     const bool is_tail = (e < 7) ? ((heads >> (e + 1)) & 1u) != 0
                                  : (c0 + 8 >= kTile || next != lb[7]);
-    if (is_tail) out[ridx] = run;
+    if (is_tail) out[__ldg(slot + ridx)] = run;
   }
 }
 
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
                                                       double* __restrict__ out,
                                                       const int* __restrict__ lab,
                                                       const int* __restrict__ tile_run_off,
+                                                      const int* __restrict__ run_slot,
                                                       double* __restrict__ run_part,
                                                       const int* __restrict__ gate) {
   pdl_wait();
@@ -208,11 +210,11 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
       if (threadIdx.x == 0) {
         double s = 0.0;
         for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
-        run_part[tile_run_off[blockIdx.x]] = s;
+        run_part[run_slot[tile_run_off[blockIdx.x]]] = s;
       }
     } else {
       __syncthreads();
-      tile_restrict(sw, sl, run_part + tile_run_off[blockIdx.x]);
+      tile_restrict(sw, sl, run_part, run_slot + tile_run_off[blockIdx.x]);
     }
   }
 }
@@ -224,7 +226,7 @@ static void stencil_t(const Dia& A, long long n_pad, const double* v, const doub
   const unsigned grid = (unsigned)(n_pad / kTile);
   launch_pdl(k_stencil<MODE, PRE, R, W>, dim3(grid), dim3(kThreads), 0, s, A, v, scale, b, out,
              rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
-             rm ? rm->run_part : nullptr, gate);
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate);
 }
 
 template <int MODE, bool PRE>
@@ -257,8 +259,7 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
 // K2: per-column sum of run partials (one warp per deflation column, fixed order).
 // ======================================================================================
 __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __restrict__ run_part,
-                                                             const int* __restrict__ ptr,
-                                                             const int* __restrict__ runs, int d,
+                                                             const int* __restrict__ ptr, int d,
                                                              const int* __restrict__ long_ids,
                                                              int nlong, int short_blocks,
                                                              double* __restrict__ s,
@@ -272,7 +273,8 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
     const int lo = ptr[L], hi = ptr[L + 1];
     if (hi - lo > kShortRuns) return;
     double acc = 0.0;
-    for (int k = lo; k < hi; ++k) acc += __ldcg(run_part + runs[k]);
+#pragma unroll 4
+    for (int k = lo; k < hi; ++k) acc += __ldcg(run_part + k);
     s[L] = acc;
     return;
   }
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
   const int L = long_ids[wl];
   double acc = 0.0;
   const int lo = ptr[L], hi = ptr[L + 1];
-  for (int k = lo + lane; k < hi; k += 32) acc += __ldcg(run_part + runs[k]);
+  for (int k = lo + lane; k < hi; k += 32) acc += __ldcg(run_part + k);
   acc = warp_sum(acc);
   if (lane == 0) s[L] = acc;
 }
@@ -294,7 +296,7 @@ void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cud
   const unsigned grid =
       (unsigned)(short_blocks + ((long long)rm.nlong * 32 + kThreads - 1) / kThreads);
   launch_pdl(k_restrict_final, dim3(grid), dim3(kThreads), 0, s, rm.run_part, rm.lab_run_ptr,
-             rm.lab_runs, rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, gate);
+             rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, gate);
 }
 
 // ======================================================================================

@@ -19,9 +19,9 @@ enum StencilMode {
 struct RunMap {            // label-segmented restriction metadata
   const int* lab;          // guarded labels
   const int* tile_run_off; // [ntiles+1] first run id of each tile
-  double* run_part;        // [nruns] per-run partial sums
-  const int* lab_run_ptr;  // [d+1] CSR: runs of each label, run order
-  const int* lab_runs;     // [nlabelled runs]
+  double* run_part;        // [nruns] per-run partial sums, label-major (slot order)
+  const int* lab_run_ptr;  // [d+1] CSR: slots of each label's runs, in run order
+  const int* run_slot;     // [nruns] slot of each run (unlabelled runs after the labelled)
   int d;
   const int* long_ids;     // columns with more than kShortRuns runs (summed by a warp)
   int nlong;

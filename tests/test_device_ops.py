@@ -158,6 +158,25 @@ def test_large_nonsymmetric_coarse_system_lu(gpu):
     assert rel(Einv, np.linalg.inv(E)) < 1e-10
 
 
+@pytest.mark.parametrize("d", [1, 2, 63, 64, 65, 255, 256, 257, 300, 513, 777])
+def test_spd_coarse_inverse_block_edges(gpu, d):
+    """Cholesky-based inverse across the diagonal-block (64) and group (256) edges."""
+    rng = np.random.default_rng(d)
+    n = 4 * d + 7
+    main = rng.uniform(2.5, 4.0, n)
+    off = -rng.uniform(0.2, 1.0, n)
+    A = dk.SparseMatrix.from_dia(n, [-1, 0, 1], np.vstack([np.r_[0.0, off[:-1]], main,
+                                                          np.r_[off[:-1], 0.0]]))
+    lab = np.sort(rng.integers(0, d, n)).astype(np.int32)
+    lab[:d] = np.arange(d)  # every column used
+    lab = np.sort(lab)
+    ctx = dk.build_context(A, dk.Preconditioner.identity(), dk.DeflationBasis(labels=lab, d=d),
+                           np.ones(n))
+    E, Einv = ctx.coarse_matrix()
+    assert rel(Einv, np.linalg.inv(E)) < 1e-11
+    np.testing.assert_array_equal(Einv, Einv.T)
+
+
 def test_symmetric_indefinite_coarse_system_falls_back_to_lu(gpu):
     """A symmetric but indefinite E fails the Cholesky attempt; the LU path inverts it."""
     n = 3000
