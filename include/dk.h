@@ -108,6 +108,16 @@ int dk_op_profile_read(dk_op* op, int32_t cap, const char** names, double* ms, i
  * tensor cores, and the coarse solution x* = Z E^-1 Z^T b.  b may be NULL (x* = 0). */
 int dk_defl_create(dk_defl** ctx, dk_op* op, const int32_t* col_of_cell, int32_t d,
                    int32_t ap_choice, const double* b);
+/* Dense (non-indicator) basis, 1 <= d <= 64 (DK_EUNSUPPORTED beyond): Z is d x n row-major
+ * (row k = basis vector k), host or device.  E = Z^T A_p Z, LU with partial pivoting
+ * (DK_ESINGULAR as above), E^-1, x*  (deflation.py:71-89). */
+int dk_defl_create_dense(dk_defl** ctx, dk_op* op, const double* Z, int32_t d, int32_t ap_choice,
+                         const double* b);
+/* Dense basis Z = V_rows Y from the operator's last Arnoldi cycle (harmonic.py:91-94: the
+ * harmonic Ritz vectors), formed on the device; Y is rows x d column-major (host or device),
+ * rows <= the last cycle's columns. */
+int dk_defl_create_ritz(dk_defl** ctx, dk_op* op, const double* Y, int32_t rows, int32_t d,
+                        int32_t ap_choice, const double* b);
 int dk_defl_destroy(dk_defl* ctx);
 int dk_defl_apply_p1(dk_defl* ctx, const double* v, double* out);  /* v - A_p Z E^-1 Z^T v */
 int dk_defl_apply_p2(dk_defl* ctx, const double* v, double* out);  /* v - Z E^-1 Z^T A_p v */
@@ -127,6 +137,31 @@ int dk_defl_setup_ms(dk_defl* ctx, double* ms4);
 int dk_gmres(dk_op* op, dk_defl* ctx, const double* b, const double* x0, int32_t m, double tol,
              int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
              int32_t* restart_of, double* hbar, dk_solve_info* info);
+/* Cycle control for multi-phase solves (RDGMRES: harmonic.py:163-178 switches the deflation
+ * context after the first cycle).  in: stop after max_cycles cycles of this call (<= 0: no
+ * limit); resume != 0 continues the counters / denominator below instead of starting a new
+ * solve — with x0 == NULL from the operator's device-resident iterate of the previous call
+ * (x_out of a deflated call is the reconstructed solution, the iterate stays on the device),
+ * and the final relative residual keeps referring to the first call's x0.
+ * out: the state to resume from. */
+typedef struct dk_cycle_ctl {
+  int32_t max_cycles;
+  int32_t resume;
+  int32_t iterations;
+  int32_t cycles;
+  int32_t warning;    /* 1: breakdown recorded */
+  int32_t has_prev;   /* a previous restart residual exists */
+  int32_t converged;  /* out */
+  int32_t running;    /* out: another cycle would run */
+  double denom;       /* convergence denominator: the first restart residual norm */
+  double prev_beta;   /* the last restart residual norm */
+} dk_cycle_ctl;
+/* dk_gmres with cycle control; gram (may be NULL) receives V_{cols+1}^T V_cols of the last
+ * cycle, (m+1) x m column-major (the re-orthogonalisation test's Gram matrix). */
+int dk_gmres_ex(dk_op* op, dk_defl* ctx, const double* b, const double* x0, int32_t m, double tol,
+                int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
+                int32_t* restart_of, double* hbar, double* gram, dk_solve_info* info,
+                const dk_cycle_ctl* ctl_in, dk_cycle_ctl* ctl_out);
 /* Copies basis vector i of the last cycle (normalised, length n) out; i <= last_cols. */
 int dk_last_basis_vector(dk_op* op, int32_t i, double* out);
 

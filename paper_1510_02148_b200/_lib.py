@@ -26,8 +26,9 @@ EXPORTS = (
     "dk_op_profile_read",
     "dk_defl_create", "dk_defl_destroy", "dk_defl_apply_p1", "dk_defl_apply_p2",
     "dk_defl_reconstruct", "dk_defl_x_star", "dk_defl_coarse", "dk_defl_setup_ms",
-    "dk_gmres", "dk_last_basis_vector", "dk_levelset_labels", "dk_levelset_labels_device",
-    "dk_assemble_tpfa",
+    "dk_gmres", "dk_gmres_ex", "dk_last_basis_vector", "dk_levelset_labels",
+    "dk_levelset_labels_device", "dk_assemble_tpfa", "dk_defl_create_dense",
+    "dk_defl_create_ritz",
 )
 
 
@@ -45,6 +46,16 @@ class SolveInfo(C.Structure):
         ("converged", C.c_int32), ("warning", C.c_int32), ("last_cols", C.c_int32),
         ("reorths", C.c_int32), ("kernel_launches", C.c_int32),
         ("final_relres", C.c_double), ("solve_seconds", C.c_double),
+    ]
+
+
+class CycleCtl(C.Structure):
+    """dk_cycle_ctl: cycle limit and resumable solve state (include/dk.h)."""
+    _fields_ = [
+        ("max_cycles", C.c_int32), ("resume", C.c_int32), ("iterations", C.c_int32),
+        ("cycles", C.c_int32), ("warning", C.c_int32), ("has_prev", C.c_int32),
+        ("converged", C.c_int32), ("running", C.c_int32),
+        ("denom", C.c_double), ("prev_beta", C.c_double),
     ]
 
 
@@ -80,6 +91,12 @@ def _declare(lib):
         "dk_defl_setup_ms": (C.c_int, [_P, _D]),
         "dk_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int32, C.c_int32,
                                _P, _P, _P, _P, C.POINTER(SolveInfo)]),
+        "dk_gmres_ex": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int32, C.c_int32,
+                                  _P, _P, _P, _P, _P, C.POINTER(SolveInfo), C.POINTER(CycleCtl),
+                                  C.POINTER(CycleCtl)]),
+        "dk_defl_create_dense": (C.c_int, [C.POINTER(_P), _P, _P, C.c_int32, C.c_int32, _P]),
+        "dk_defl_create_ritz": (C.c_int, [C.POINTER(_P), _P, _P, C.c_int32, C.c_int32, C.c_int32,
+                                          _P]),
         "dk_last_basis_vector": (C.c_int, [_P, C.c_int32, _P]),
         "dk_levelset_labels": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _P, C.c_int32,
                                          C.c_int32, C.c_int32, _P, _I64, _P]),

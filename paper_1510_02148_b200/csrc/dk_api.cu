@@ -65,6 +65,8 @@ unsigned long long g_ctx_serial = 0;
 constexpr int kSymvMinD = 256;
 // the packed solve stages s in shared memory next to its tile buffers (227 KB per CTA)
 constexpr int kSymvMaxD = 12288;
+// largest dense (non-indicator) deflation basis
+constexpr int kDenseMaxD = 64;
 
 }  // namespace
 
@@ -158,6 +160,13 @@ struct dk_defl {
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
   double nmasked = 0;  // foreign-label coefficients of the prolongation (byte accounting)
+  // dense basis (non-indicator Z, d <= kDenseMaxD): rows Z_k and A_p Z_k, guarded like V
+  int dense = 0;
+  double* Z_base = nullptr;
+  double* AZ_base = nullptr;
+  double* Z = nullptr;
+  double* AZ = nullptr;
+  long long zs = 0;
 };
 
 namespace {
@@ -174,6 +183,8 @@ Dia make_dia(const dk_op* op, bool with_inv) {
   A.inv = with_inv ? op->inv : nullptr;
   return A;
 }
+
+int defl_kind(const dk_defl* c) { return !c ? DK_NONE : c->dense ? DK_DENSE : DK_LABELS; }
 
 // flag <- 0 unless lo[i + o] == up[i] for i in [0, count)  (bitwise symmetry of a pair)
 __global__ void k_check_pair(const double* __restrict__ up, const double* __restrict__ lo,
@@ -206,6 +217,17 @@ int download(dk_op* op, double* dst, const double* src, long long count) {
   return DK_OK;
 }
 
+// per-block partials: room for q quantities per launch
+int ensure_part(dk_op* op, int q) {
+  if (op->part_q < q) {
+    if (op->part) DK_TRY(cudaFree(op->part));
+    DK_TRY(cudaMalloc(&op->part, (size_t)q * op->G * sizeof(double)));
+    op->part_q = q;
+    op->g_m = -1;  // the graph refers to the old buffer
+  }
+  return DK_OK;
+}
+
 int ensure_work(dk_op* op, int m, int max_iters) {
   if (op->v_rows < m + 1) {
     if (op->V_base) DK_TRY(cudaFreeAsync(op->V_base, op->stream));
@@ -218,11 +240,9 @@ int ensure_work(dk_op* op, int m, int max_iters) {
     op->g_m = -1;  // graph refers to the old basis
   }
   // per-block partials: up to (m+1)+1 quantities (dots, norm) per launch
-  if (op->part_q < 2 * m + 4) {
-    if (op->part) DK_TRY(cudaFree(op->part));
-    DK_TRY(cudaMalloc(&op->part, (size_t)(2 * m + 4) * op->G * sizeof(double)));
-    op->part_q = 2 * m + 4;
-    op->g_m = -1;
+  {
+    const int rc = ensure_part(op, std::max(2 * m + 4, kDenseMaxD + 4));
+    if (rc) return rc;
   }
   if (op->scal_m < m) {
     if (op->scal) DK_TRY(cudaFree(op->scal));
@@ -315,6 +335,21 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
                   const double* scale, const double* b, double* out, const int* gate) {
   const Dia A = make_dia(op, pre);
   const double n = (double)op->n;
+  if (c->dense) {  // stencil (stored), then s = Z^T w and y = E^-1 s in one multi-dot kernel
+    const double* src = v;
+    if (mode != ST_IDENT) {
+      double* dst = write ? out : c->qv_base + op->guard;
+      ProfScope ps(op, PC_STENCIL,
+                   (16.0 + 8.0 * op->nstore + (pre ? 8.0 : 0.0) + (mode == ST_RESID ? 8.0 : 0.0)) *
+                       n);
+      launch_stencil(mode, pre, true, A, op->n_pad, v, scale, b, dst, nullptr, gate, op->stream);
+      src = dst;
+    }
+    ProfScope ps(op, PC_RESTRICT, 8.0 * (c->d + 1) * n);
+    launch_zdots(src, c->Z, c->zs, c->d, op->n_pad, op->part, op->G, op->tickets + 2, c->Einv,
+                 c->ld, c->y, 1, gate, op->stream);
+    return;
+  }
   {
     // v, labels, the output if stored; the operator and M^-1 unless the identity
     const double by = 12.0 + (write ? 8.0 : 0.0) +
@@ -359,10 +394,11 @@ void issue_restart(dk_op* op, dk_defl* c) {
                    &st->running, op->stream);
   }
   // w in/out; with deflation the compact prolongation: labels 4, own 8, mask 1 per cell and
-  // one coefficient + label (+ M^-1 for A_p = AM) per foreign-label entry
-  const double pro_bytes = c ? 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked : 0.0;
+  // one coefficient + label (+ M^-1 for A_p = AM) per foreign-label entry; dense: A_p Z rows
+  const double pro_bytes = !c ? 0.0 : c->dense ? 8.0 * c->d * n
+                                               : 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
   ProfScope ps(op, PC_RESTART, 16.0 * n + pro_bytes);
-  launch_project(PJ_RESTART, c != nullptr, am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
+  launch_project(PJ_RESTART, defl_kind(c), am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                  op->w, op->V_base + op->guard, nullptr, op->vstride, 0, op->n_pad, op->part,
                  op->G, op->sc, 0, &st->running, op->stream);
 }
@@ -378,7 +414,8 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   const double n = (double)op->n;
   double* V = op->V_base + op->guard;
   const int nvec = j + 1;
-  const double pro_bytes = c ? 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked : 0.0;
+  const double pro_bytes = !c ? 0.0 : c->dense ? 8.0 * c->d * n
+                                               : 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
   if (c) {
     coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
                  nullptr, op->w, &st->active);
@@ -390,7 +427,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   {
     ProfScope ps(op, PC_PROJECT,
                  c ? (16.0 + 8.0 * nvec) * n + pro_bytes : (8.0 + 8.0 * nvec) * n);
-    launch_project(PJ_ITER, c != nullptr, am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
+    launch_project(PJ_ITER, defl_kind(c), am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                    op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
                    &st->active, op->stream);
   }
@@ -405,7 +442,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   }
   {
     ProfScope ps(op, PC_REORTH, (16.0 + 16.0 * nvec) * n);
-    launch_project(PJ_REDOTS, false, false, A, Prolong{}, nullptr,
+    launch_project(PJ_REDOTS, DK_NONE, false, A, Prolong{}, nullptr,
                    V + (long long)(j + 1) * op->vstride, nullptr, V, op->vstride, nvec, op->n_pad,
                    op->part, op->G, op->sc, j, &st->reorth, op->stream);
     launch_gs(true, V + (long long)(j + 1) * op->vstride, V + (long long)(j + 1) * op->vstride, V,
@@ -962,11 +999,158 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   return DK_OK;
 }
 
+// Dense basis context (deflation.py:71-89 for a general n x d Z, d <= kDenseMaxD): rows Z_k
+// (written by `fill`), A_p Z_k by the stencil, E_ik = Z_i . A_p Z_k by multi-dots, pivoted
+// LU + E^-1 (the reference's singularity rule), x* = Z E^-1 Z^T b.
+}  // extern "C"
+template <class Fill>
+static int defl_create_dense(dk_defl** out, dk_op* op, int32_t d, int32_t ap_choice,
+                             const double* b, Fill fill) {
+  if (!out || !op) return fail(DK_EINVAL, "null argument");
+  *out = nullptr;
+  if (d < 1) return fail(DK_EINVAL, "Z must be n x d with d >= 1");
+  if (d > kDenseMaxD)
+    return fail(DK_EUNSUPPORTED, "dense deflation bases are limited to 64 columns");
+  if (ap_choice != DK_AP_A && ap_choice != DK_AP_AM)
+    return fail(DK_EINVAL, "A_p_choice must be 'A' or 'AM'");
+  if (ap_choice == DK_AP_AM && op->inv == nullptr) ap_choice = DK_AP_A;
+  cudaStream_t s = op->stream;
+  {
+    int rc = ensure_part(op, kDenseMaxD + 4);
+    if (rc) return rc;
+  }
+  dk_defl* c = new dk_defl();
+  c->op = op;
+  c->serial = ++g_ctx_serial;
+  c->d = d;
+  c->ld = (int)round_up(d, 2);
+  c->ap = ap_choice;
+  c->dense = 1;
+  c->zs = op->n_pad + op->guard;
+  auto cleanup_fail = [&](cudaError_t e, const char* where) {
+    dk_defl_destroy(c);
+    return cuda_fail(e, where);
+  };
+#define DKD(x)                                           \
+  do {                                                   \
+    cudaError_t _e = (x);                                \
+    if (_e != cudaSuccess) return cleanup_fail(_e, #x);  \
+  } while (0)
+  const size_t rows_bytes = ((size_t)op->guard + (size_t)d * c->zs) * sizeof(double);
+  DKD(cudaMallocAsync(&c->Z_base, rows_bytes, s));
+  DKD(cudaMallocAsync(&c->AZ_base, rows_bytes, s));
+  DKD(cudaMemsetAsync(c->Z_base, 0, rows_bytes, s));
+  DKD(cudaMemsetAsync(c->AZ_base, 0, rows_bytes, s));
+  c->Z = c->Z_base + op->guard;
+  c->AZ = c->AZ_base + op->guard;
+  DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
+  DKD(cudaMallocAsync(&c->Einv, (size_t)d * c->ld * sizeof(double), s));
+  DKD(cudaMemsetAsync(c->E, 0, (size_t)d * c->ld * sizeof(double), s));
+  DKD(cudaMalloc(&c->piv, (size_t)d * sizeof(int)));
+  DKD(cudaMalloc(&c->s, (size_t)c->ld * sizeof(double)));
+  DKD(cudaMalloc(&c->y, (size_t)c->ld * sizeof(double)));
+  DKD(cudaMemsetAsync(c->y, 0, (size_t)c->ld * sizeof(double), s));
+  DKD(cudaMalloc(&c->xs_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMemsetAsync(c->xs_base, 0, (size_t)op->vlen * sizeof(double), s));
+  c->xs = c->xs_base + op->guard;
+  DKD(cudaMalloc(&c->qv_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMemsetAsync(c->qv_base, 0, (size_t)op->vlen * sizeof(double), s));
+  {
+    const int rc = fill(c);
+    if (rc) {
+      dk_defl_destroy(c);
+      return rc;
+    }
+  }
+  c->pro.az = c->AZ;
+  c->pro.azs = c->zs;
+  c->pro.dz = d;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  const bool am = ap_choice == DK_AP_AM;
+  const Dia Ap = make_dia(op, am);
+  for (int k = 0; k < d; ++k)  // A_p Z_k
+    launch_stencil(ST_APPLY, am, true, Ap, op->n_pad, c->Z + (long long)k * c->zs, nullptr,
+                   nullptr, c->AZ + (long long)k * c->zs, nullptr, nullptr, s);
+  for (int k = 0; k < d; ++k)  // column k of E: Z_i . A_p Z_k
+    launch_zdots(c->AZ + (long long)k * c->zs, c->Z, c->zs, d, op->n_pad, op->part, op->G,
+                 op->tickets + 2, nullptr, 0, c->E + k, c->ld, nullptr, s);
+  DKD(cudaGetLastError());
+  cudaEventRecord(e1, s);
+  DKD(cudaEventSynchronize(e1));
+  cudaEventElapsedTime(&c->ms[0], e0, e1);
+  double* Ework = nullptr;
+  DKD(cudaMallocAsync(&Ework, (size_t)d * c->ld * sizeof(double), s));
+  DKD(cudaMemcpyAsync(Ework, c->E, (size_t)d * c->ld * sizeof(double), cudaMemcpyDeviceToDevice,
+                      s));
+  double min_piv = 0.0;
+  int err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
+  cudaFreeAsync(Ework, s);
+  if (err) return cleanup_fail((cudaError_t)err, "lu_and_inverse");
+  if (!(min_piv >= 1e-300)) {  // sparse.py:135-136
+    dk_defl_destroy(c);
+    return fail(DK_ESINGULAR, "zero pivot in LU factorization");
+  }
+  cudaEventRecord(e0, s);
+  if (b) {  // x* = Z E^-1 Z^T b  (deflation.py:88)
+    int rc = upload(op, op->t, b);
+    if (rc) {
+      dk_defl_destroy(c);
+      return rc;
+    }
+    launch_zdots(op->t, c->Z, c->zs, d, op->n_pad, op->part, op->G, op->tickets + 2, c->Einv,
+                 c->ld, c->y, 1, nullptr, s);
+    launch_dense_recon(c->Z, c->zs, d, c->y, nullptr, nullptr, c->xs, op->n_pad, 1, s);
+  }
+  cudaEventRecord(e1, s);
+  DKD(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&c->ms[3], e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  DKD(cudaGetLastError());
+  *out = c;
+#undef DKD
+  return DK_OK;
+}
+extern "C" {
+
+int dk_defl_create_dense(dk_defl** out, dk_op* op, const double* Z, int32_t d, int32_t ap_choice,
+                         const double* b) {
+  if (!Z) return fail(DK_EINVAL, "null argument");
+  return defl_create_dense(out, op, d, ap_choice, b, [&](dk_defl* c) -> int {
+    DK_TRY(cudaMemcpy2DAsync(c->Z, (size_t)c->zs * sizeof(double), Z,
+                             (size_t)op->n * sizeof(double), (size_t)op->n * sizeof(double), d,
+                             cudaMemcpyDefault, op->stream));
+    return DK_OK;
+  });
+}
+
+int dk_defl_create_ritz(dk_defl** out, dk_op* op, const double* Y, int32_t rows, int32_t d,
+                        int32_t ap_choice, const double* b) {
+  if (!Y || !op) return fail(DK_EINVAL, "null argument");
+  if (!op->has_last) return fail(DK_EINVAL, "no Arnoldi cycle to combine");
+  if (rows < 1 || rows > op->st_host->last_cols)
+    return fail(DK_EINVAL, "coefficient rows must be in [1, last cycle columns]");
+  return defl_create_dense(out, op, d, ap_choice, b, [&](dk_defl* c) -> int {
+    double* Yd = nullptr;
+    DK_TRY(cudaMallocAsync(&Yd, (size_t)rows * d * sizeof(double), op->stream));
+    DK_TRY(cudaMemcpyAsync(Yd, Y, (size_t)rows * d * sizeof(double), cudaMemcpyDefault,
+                           op->stream));
+    launch_combine_rows(op->V_base + op->guard, op->vstride, op->sc.sigma, rows, Yd, d, c->Z,
+                        c->zs, op->n_pad, op->stream);
+    DK_TRY(cudaGetLastError());
+    DK_TRY(cudaFreeAsync(Yd, op->stream));
+    return DK_OK;
+  });
+}
+
 int dk_defl_destroy(dk_defl* c) {
   if (!c) return DK_OK;
   cudaStream_t s = c->op ? c->op->stream : nullptr;
   if (c->op) cudaStreamSynchronize(s);
-  void* pooled[] = {c->E, c->Einv, c->P};  // stream-ordered pool allocations
+  void* pooled[] = {c->E, c->Einv, c->P, c->Z_base, c->AZ_base};  // stream-ordered pool
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, s);
   void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
@@ -987,7 +1171,7 @@ int dk_defl_apply_p1(dk_defl* c, const double* v, double* out) {
   if (rc) return rc;
   coarse_solve(op, c, ST_IDENT, false, false, op->t, nullptr, nullptr, nullptr, nullptr);
   const bool am = c->ap == DK_AP_AM;
-  launch_project(PJ_PLAIN, true, am, make_dia(op, am), c->pro, c->y, op->t, op->w, nullptr, 0, 0,
+  launch_project(PJ_PLAIN, defl_kind(c), am, make_dia(op, am), c->pro, c->y, op->t, op->w, nullptr, 0, 0,
                  op->n_pad, op->part, op->G, op->sc, 0, op->one, op->stream);
   DK_TRY(cudaGetLastError());
   rc = download(op, out, op->w, op->n);
@@ -1002,7 +1186,10 @@ static int p2_into(dk_defl* c, const double* v, double* dst, bool add_xstar) {
   if (rc) return rc;
   const bool am = c->ap == DK_AP_AM;
   coarse_solve(op, c, ST_APPLY, am, false, op->t, nullptr, nullptr, nullptr, nullptr);
-  if (add_xstar) launch_recon(c->lab, c->y, c->xs, op->t, op->w, op->n_pad, op->stream);
+  if (c->dense)
+    launch_dense_recon(c->Z, c->zs, c->d, c->y, c->xs, op->t, op->w, op->n_pad,
+                       add_xstar ? 0 : 2, op->stream);
+  else if (add_xstar) launch_recon(c->lab, c->y, c->xs, op->t, op->w, op->n_pad, op->stream);
   else launch_sub_bcast(c->lab, c->y, op->t, op->w, op->n_pad, op->stream);
   DK_TRY(cudaGetLastError());
   rc = download(op, dst, op->w, op->n);
@@ -1050,9 +1237,10 @@ int dk_defl_setup_ms(dk_defl* c, double* ms4) {
 }
 
 // ---- solver -------------------------------------------------------------------------------
-int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m, double tol,
-             int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
-             int32_t* restart_of, double* hbar, dk_solve_info* info) {
+int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m, double tol,
+                int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
+                int32_t* restart_of, double* hbar, double* gram, dk_solve_info* info,
+                const dk_cycle_ctl* ctl_in, dk_cycle_ctl* ctl_out) {
   if (!op || !b || !x_out || !info) return fail(DK_EINVAL, "null argument");
   if (c && c->op != op) return fail(DK_EINVAL, "deflation context belongs to another operator");
   if (m < 1) return fail(DK_EINVAL, "cycle size must be >= 1");
@@ -1061,11 +1249,24 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   if (rc) return rc;
   op->launches = 0;
   if ((rc = upload(op, op->b, b))) return rc;
-  if ((rc = upload(op, op->x0, x0))) return rc;
-  DK_TRY(cudaMemcpyAsync(op->x, op->x0, (size_t)op->n_pad * sizeof(double),
-                         cudaMemcpyDeviceToDevice, op->stream));
+  // resuming with x0 == NULL continues from the device-resident iterate (and keeps the
+  // original x0 for the final relative residual)
+  if (!(ctl_in && ctl_in->resume && x0 == nullptr)) {
+    if ((rc = upload(op, op->x0, x0))) return rc;
+    DK_TRY(cudaMemcpyAsync(op->x, op->x0, (size_t)op->n_pad * sizeof(double),
+                           cudaMemcpyDeviceToDevice, op->stream));
+  }
   launch_init_state(op->sc, tol, m, max_iters, min_iters, op->stream);
   op->launches += 1;
+  const bool resume = ctl_in && ctl_in->resume;
+  if (resume) {  // continue a solve: counters, convergence denominator, restart history
+    launch_resume_state(op->sc, ctl_in->iterations, ctl_in->cycles, ctl_in->warning,
+                        ctl_in->has_prev, ctl_in->denom, ctl_in->prev_beta, op->stream);
+    op->launches += 1;
+  }
+  const int max_cycles = ctl_in ? ctl_in->max_cycles : 0;
+  // krylov.py:127: no cycle starts once max_iters is reached (the caller's earlier calls)
+  const bool run_cycles = !(resume && ctl_in->iterations >= max_iters);
   // The cycle becomes a CUDA graph from the second solve with the same (context, m): a
   // one-off solve (the public pdgmres path) launches eagerly and skips the instantiation.
   const unsigned long long key = c ? c->serial : 0ull;
@@ -1082,9 +1283,11 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, op->stream);
-  const int coarse_launches = c ? (c->sym ? 4 : 3) : 1;  // stencil (+ restrict + E^-1 s)
+  // stencil (+ restrict + E^-1 s; dense: one multi-dot)
+  const int coarse_launches = c ? (c->dense ? 2 : c->sym ? 4 : 3) : 1;
   const int per_cycle_launches = coarse_launches + 1 + m * (coarse_launches + 4) + 2;
-  long long guard_cycles = (long long)max_iters + 2;
+  long long guard_cycles = run_cycles ? (long long)max_iters + 2 : 0;
+  if (max_cycles > 0 && guard_cycles > max_cycles) guard_cycles = max_cycles;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
     if (use_graph) {
       DK_TRY(cudaGraphLaunch(op->gexec, op->stream));
@@ -1121,7 +1324,10 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   if (c) {
     const bool am = c->ap == DK_AP_AM;
     coarse_solve(op, c, ST_APPLY, am, false, op->x, nullptr, nullptr, nullptr, nullptr);
-    launch_recon(c->lab, c->y, c->xs, op->x, op->t, op->n_pad, op->stream);
+    if (c->dense)
+      launch_dense_recon(c->Z, c->zs, c->d, c->y, c->xs, op->x, op->t, op->n_pad, 0, op->stream);
+    else
+      launch_recon(c->lab, c->y, c->xs, op->x, op->t, op->n_pad, op->stream);
     xf = op->t;
     op->launches += 4;
   }
@@ -1147,7 +1353,34 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   if (hbar)
     DK_TRY(cudaMemcpyAsync(hbar, op->sc.H, (size_t)(m + 1) * m * sizeof(double),
                            cudaMemcpyDefault, op->stream));
+  std::vector<double> gm, gc, sg;
+  if (gram) {
+    gm.resize((size_t)(m + 1) * (m + 1));
+    gc.resize(m + 1);
+    sg.resize(m + 1);
+    DK_TRY(cudaMemcpyAsync(gm.data(), op->sc.Gm, gm.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, op->stream));
+    DK_TRY(cudaMemcpyAsync(gc.data(), op->sc.gcol, gc.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, op->stream));
+    DK_TRY(cudaMemcpyAsync(sg.data(), op->sc.sigma, sg.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, op->stream));
+  }
   DK_TRY(cudaStreamSynchronize(op->stream));
+  if (gram) {
+    // V_{cols+1}^T V_cols of the last cycle, (m+1) x m column-major: the Gram matrix the
+    // re-orthogonalisation test maintains, last row sigma_cols V^T u (0 if the cycle stopped
+    // before storing that vector, as the reference leaves V[cols] zero)
+    const int cols = S.last_cols;
+    for (size_t e = 0; e < (size_t)(m + 1) * m; ++e) gram[e] = 0.0;
+    for (int k = 0; k < cols; ++k)
+      for (int i = 0; i <= cols; ++i) {
+        double g;
+        if (i == cols && cols == S.cycle_cols) g = S.last_broke ? 0.0 : sg[cols] * gc[k];
+        else if (i <= k) g = gm[(size_t)k * (m + 1) + i];
+        else g = gm[(size_t)i * (m + 1) + k];
+        gram[(size_t)k * (m + 1) + i] = g;
+      }
+  }
   info->iterations = S.iterations;
   info->cycles = S.cycle;
   info->restarts = std::max(S.cycle - 1, 0);
@@ -1159,7 +1392,26 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
   info->final_relres = nr[0] / (nr[1] > 0 ? nr[1] : 1.0);
   info->solve_seconds = solve_ms * 1e-3;
   op->has_last = S.cycle > 0;
+  if (ctl_out) {
+    ctl_out->max_cycles = max_cycles;
+    ctl_out->resume = 1;
+    ctl_out->iterations = S.iterations;
+    ctl_out->cycles = S.cycle;
+    ctl_out->warning = S.warning;
+    ctl_out->has_prev = S.has_prev;
+    ctl_out->converged = S.converged;
+    ctl_out->running = S.running && !S.converged && S.iterations < max_iters && S.last_cols > 0;
+    ctl_out->denom = S.denom;
+    ctl_out->prev_beta = S.prev_beta;
+  }
   return DK_OK;
+}
+
+int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m, double tol,
+             int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
+             int32_t* restart_of, double* hbar, dk_solve_info* info) {
+  return dk_gmres_ex(op, c, b, x0, m, tol, max_iters, min_iters, x_out, hist, restart_of, hbar,
+                     nullptr, info, nullptr, nullptr);
 }
 
 int dk_last_basis_vector(dk_op* op, int32_t i, double* out) {

@@ -567,7 +567,7 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
   }
 }
 
-template <int MODE, bool DEFL, bool AM>
+template <int MODE, int DEFL, bool AM>
 __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
                                                       const double* __restrict__ yc,
                                                       const double* w_in, double* w_out,
@@ -593,16 +593,26 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
     for (int k = 0; k < 4; ++k) {
       const long long i = cb + 512 * k;
       double2 x = (MODE == PJ_REDOTS) ? ld2cg(w_in + i) : ld2(w_in + i);
-      if (DEFL) {
+      if (DEFL == DK_LABELS) {
         const int2 L = *reinterpret_cast<const int2*>(P.lab + i);
         const double2 ow = ld2(P.own + i);
         const uchar2 mk = *reinterpret_cast<const uchar2*>(P.mask + i);
         x.x = __dsub_rn(x.x, prolong_cell<AM>(A, P, yc, i, L.x, ow.x, mk.x));
         x.y = __dsub_rn(x.y, prolong_cell<AM>(A, P, yc, i + 1, L.y, ow.y, mk.y));
+      } else if (DEFL == DK_DENSE) {  // w -= (A_p Z) y   (deflation.py:61-62)
+        double t0 = 0.0, t1 = 0.0;
+        for (int q = 0; q < P.dz; ++q) {
+          const double yq = __ldg(yc + q);
+          const double2 a = ld2(P.az + (long long)q * P.azs + i);
+          t0 = fma(yq, a.x, t0);
+          t1 = fma(yq, a.y, t1);
+        }
+        x.x = __dsub_rn(x.x, t0);
+        x.y = __dsub_rn(x.y, t1);
       }
       w[2 * k] = x.x;
       w[2 * k + 1] = x.y;
-      if (MODE != PJ_REDOTS && (DEFL || w_out != w_in)) st2(w_out + i, x);
+      if (MODE != PJ_REDOTS && (DEFL != DK_NONE || w_out != w_in)) st2(w_out + i, x);
     }
     if (MODE == PJ_ITER || MODE == PJ_RESTART) {
       double nrm = 0.0;
@@ -679,7 +689,7 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
   iter_finish(sc, j, nvec, red);
 }
 
-template <int MODE, bool DEFL, bool AM>
+template <int MODE, int DEFL, bool AM>
 static void project_t(const Dia& A, const Prolong& lab, const double* yc, const double* w_in,
                       double* w_out, const double* V, long long vstride, int nvec,
                       long long n_pad, double* part, int G, const Scal& sc, int j,
@@ -700,22 +710,25 @@ static void project_t(const Dia& A, const Prolong& lab, const double* yc, const 
 }
 
 template <int MODE>
-static void project_m(bool defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
+static void project_m(int defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                       const double* w_in, double* w_out, const double* V, long long vstride,
                       int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                       const int* gate, cudaStream_t s) {
-  if (!defl)
-    project_t<MODE, false, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
-                                  j, gate, s);
+  if (defl == DK_NONE)
+    project_t<MODE, DK_NONE, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
+                                    sc, j, gate, s);
+  else if (defl == DK_DENSE)
+    project_t<MODE, DK_DENSE, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
+                                     sc, j, gate, s);
   else if (am)
-    project_t<MODE, true, true>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc, j,
-                                gate, s);
+    project_t<MODE, DK_LABELS, true>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
+                                     sc, j, gate, s);
   else
-    project_t<MODE, true, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc, j,
-                                 gate, s);
+    project_t<MODE, DK_LABELS, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
+                                      sc, j, gate, s);
 }
 
-void launch_project(int mode, bool defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
+void launch_project(int mode, int defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                     const int* gate, cudaStream_t s) {
@@ -726,11 +739,135 @@ void launch_project(int mode, bool defl, bool am, const Dia& A, const Prolong& l
     project_m<PJ_RESTART>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
                           j, gate, s);
   else if (mode == PJ_REDOTS)
-    project_t<PJ_REDOTS, false, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
-                                       sc, j, gate, s);
+    project_t<PJ_REDOTS, DK_NONE, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part,
+                                         G, sc, j, gate, s);
   else
     project_m<PJ_PLAIN>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc,
                         j, gate, s);
+}
+
+// ======================================================================================
+// Dense deflation basis (RDGMRES harmonic-Ritz vectors, harmonic.py:97-180, or any n x d
+// basis with d <= kDenseMaxD): s = Z^T v by the same (row, quarter-chunk) item sweep as the
+// Arnoldi dots, y = E^-1 s in the last block; fixed order, deterministic.
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads) k_zdots(const double* __restrict__ v,
+                                                    const double* __restrict__ Z, long long zs,
+                                                    int nz, long long n_pad,
+                                                    double* __restrict__ part, int G,
+                                                    unsigned int* ticket,
+                                                    const double* __restrict__ Einv, int ld,
+                                                    double* __restrict__ y, long long ystride,
+                                                    const int* __restrict__ gate) {
+  pdl_wait();
+  if (gate != nullptr && *gate == 0) return;
+  extern __shared__ double red[];  // [nz][kWarps], later s[nz]
+  __shared__ __align__(16) double s_v[kChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = threadIdx.x; q < nz * kWarps; q += blockDim.x) red[q] = 0.0;
+  __syncthreads();
+  const long long nchunks = n_pad / kChunk;
+  double2* sv2 = reinterpret_cast<double2*>(s_v);
+  for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long long c0 = ch * kChunk;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sv2[threadIdx.x + 256 * k] = ld2(v + c0 + 2 * threadIdx.x + 512 * k);
+    __syncthreads();
+    for (int it = warp; it < 4 * nz; it += kWarps) {
+      const int r = it >> 2, qtr = it & 3;
+      const double* Zr = Z + (long long)r * zs + c0 + 512 * qtr + 2 * lane;
+      double2 p[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p[i] = ld2(Zr + 64 * i);
+      double a = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 vv = sv2[256 * qtr + lane + 32 * i];
+        a = fma(p[i].x, vv.x, a);
+        a = fma(p[i].y, vv.y, a);
+      }
+      a = warp_sum(a);
+      if (lane == 0) red[r * kWarps + warp] += a;
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+  for (int q = threadIdx.x; q < nz; q += blockDim.x) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) t += red[q * kWarps + w2];
+    part[(size_t)q * G + blockIdx.x] = t;
+  }
+  if (!last_block(ticket)) return;
+  reduce_partials(part, nz, G, red);
+  for (int i = threadIdx.x; i < nz; i += blockDim.x) {
+    double t = red[i];
+    if (Einv != nullptr) {
+      t = 0.0;
+      for (int k = 0; k < nz; ++k) t = fma(Einv[(size_t)i * ld + k], red[k], t);
+    }
+    y[(long long)i * ystride] = t;
+  }
+}
+
+void launch_zdots(const double* v, const double* Z, long long zs, int nz, long long n_pad,
+                  double* part, int G, unsigned int* ticket, const double* Einv, int ld,
+                  double* y, long long ystride, const int* gate, cudaStream_t s) {
+  const size_t smem = (size_t)(nz * kWarps > 64 ? nz * kWarps : 64) * sizeof(double);
+  launch_pdl(k_zdots, dim3(G), dim3(kThreads), smem, s, v, Z, zs, nz, n_pad, part, G, ticket,
+             Einv, ld, y, ystride, gate);
+}
+
+__global__ void k_dense_recon(const double* __restrict__ Z, long long zs, int nz,
+                              const double* __restrict__ y, const double* __restrict__ xs,
+                              const double* __restrict__ xh, double* __restrict__ out,
+                              long long n_pad, int mode) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    double zy = 0.0;
+    for (int q = 0; q < nz; ++q) zy = fma(__ldg(y + q), Z[(long long)q * zs + i], zy);
+    if (mode == 0) out[i] = __dadd_rn(xs[i], __dsub_rn(xh[i], zy));  // x* + (xh - Z y)
+    else if (mode == 1) out[i] = zy;                                  // Z y
+    else out[i] = __dsub_rn(xh[i], zy);                               // v - Z y
+  }
+}
+
+void launch_dense_recon(const double* Z, long long zs, int nz, const double* y, const double* xs,
+                        const double* xh, double* out, long long n_pad, int mode,
+                        cudaStream_t s) {
+  k_dense_recon<<<148 * 8, kThreads, 0, s>>>(Z, zs, nz, y, xs, xh, out, n_pad, mode);
+}
+
+// out_j = sum_i Y[i + j nrows] sigma_i R_i, eight outputs per sweep over the rows
+__global__ void __launch_bounds__(kThreads) k_combine_rows(const double* __restrict__ R,
+                                                           long long rs,
+                                                           const double* __restrict__ sigma,
+                                                           int nrows,
+                                                           const double* __restrict__ Y,
+                                                           int nout, double* __restrict__ out,
+                                                           long long os, long long n_pad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    for (int j0 = 0; j0 < nout; j0 += 8) {
+      double acc[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) acc[jj] = 0.0;
+      for (int r = 0; r < nrows; ++r) {
+        const double v = __ldg(sigma + r) * R[(long long)r * rs + i];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (j0 + jj < nout) acc[jj] = fma(__ldg(Y + r + (long long)(j0 + jj) * nrows), v, acc[jj]);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (j0 + jj < nout) out[(long long)(j0 + jj) * os + i] = acc[jj];
+    }
+  }
+}
+
+void launch_combine_rows(const double* R, long long rs, const double* sigma, int nrows,
+                         const double* Y, int nout, double* out, long long os, long long n_pad,
+                         cudaStream_t s) {
+  k_combine_rows<<<148 * 8, kThreads, 0, s>>>(R, rs, sigma, nrows, Y, nout, out, os, n_pad);
 }
 
 // ======================================================================================
@@ -1006,6 +1143,25 @@ __global__ void k_init_state(Scal sc, double tol, int m, int max_iters, int min_
 void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min_iters,
                        cudaStream_t s) {
   k_init_state<<<1, 1, 0, s>>>(sc, tol, m, max_iters, min_iters);
+}
+
+// continue a solve across calls (RDGMRES switches the deflation context between cycles,
+// harmonic.py:163-178): the counters, the convergence denominator and the restart history
+__global__ void k_resume_state(Scal sc, int iterations, int cycles, int warning, int has_prev,
+                               double denom, double prev_beta) {
+  State* st = sc.st;
+  st->iterations = iterations;
+  st->cycle = cycles;
+  st->warning = warning;
+  st->has_prev = has_prev;
+  st->denom = denom;
+  st->denom_set = 1;
+  st->prev_beta = prev_beta;
+}
+
+void launch_resume_state(const Scal& sc, int iterations, int cycles, int warning, int has_prev,
+                         double denom, double prev_beta, cudaStream_t s) {
+  k_resume_state<<<1, 1, 0, s>>>(sc, iterations, cycles, warning, has_prev, denom, prev_beta);
 }
 
 }  // namespace dk

@@ -44,7 +44,12 @@ struct Prolong {
   const int* lab;             // guarded labels
   const double* own;          // guarded: sum of a cell's coefficients into its own column
   const unsigned char* mask;  // guarded: diagonals whose column carries another label
+  const double* az;           // dense basis: rows A_p Z_k (stride azs), k < dz
+  long long azs;
+  int dz;
 };
+// deflation kind of a projection: none, indicator (labels), dense basis rows
+enum DeflKind { DK_NONE = 0, DK_LABELS = 1, DK_DENSE = 2 };
 void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad, double* own,
                           unsigned char* mask, unsigned long long* nmasked, cudaStream_t s);
 
@@ -52,10 +57,24 @@ enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
 // w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w and Gram column V^T V_j, ||w_out||^2
 // -> H col j + re-orthogonalisation test; RESTART: ||w_out||^2 -> restart test;
 // REDOTS: corr = V^T u for the second Gram-Schmidt pass.  G = grid width (fixed per op).
-void launch_project(int mode, bool defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
+void launch_project(int mode, int defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                     const int* gate, cudaStream_t s);
+// dense deflation basis (rows of stride zs): s_k = Z_k . v for k < nz; y[k * ystride] = s_k,
+// or y = Einv s (nz x nz, ld) when Einv != nullptr.  ticket: a zeroed device counter.
+void launch_zdots(const double* v, const double* Z, long long zs, int nz, long long n_pad,
+                  double* part, int G, unsigned int* ticket, const double* Einv, int ld,
+                  double* y, long long ystride, const int* gate, cudaStream_t s);
+// out = mode 0: xs + (xh - sum_k y_k Z_k) ; 1: sum_k y_k Z_k ; 2: xh - sum_k y_k Z_k
+void launch_dense_recon(const double* Z, long long zs, int nz, const double* y, const double* xs,
+                        const double* xh, double* out, long long n_pad, int mode,
+                        cudaStream_t s);
+// out_j = sum_{i < nrows} Y[i + j * nrows] * sigma_i * R_i for j < nout (rows R of stride rs,
+// outputs of stride os): Z = V_m Y from the stored, lazily normalised Arnoldi basis
+void launch_combine_rows(const double* R, long long rs, const double* sigma, int nrows,
+                         const double* Y, int nout, double* out, long long os, long long n_pad,
+                         cudaStream_t s);
 // u = w - sum coef_i u_i (+ corr dots, norm) or the re-orthogonalisation pass.
 void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
                int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
@@ -76,6 +95,8 @@ void launch_norm(const double* v, long long n_pad, double* part, int G, unsigned
                  double* dst, cudaStream_t s);
 void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min_iters,
                        cudaStream_t s);
+void launch_resume_state(const Scal& sc, int iterations, int cycles, int warning, int has_prev,
+                         double denom, double prev_beta, cudaStream_t s);
 
 // ---- set-up on the device (dk_setup.cu) ----
 int device_levelset_labels(long long nx, long long ny, long long nz, const long long* band_in,

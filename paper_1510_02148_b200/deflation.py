@@ -1,10 +1,12 @@
 """Deflation projectors P1, P2, the coarse matrix E and the coarse solution — on the device.
 
-Reference: defkrylov/deflation.py:19-104.  The basis is an indicator (piecewise-constant)
-basis stored as one int32 column label per cell, never as a dense n x d matrix; E, its LU,
-E^-1 and x* = Z E^-1 Z^T b are built in HBM by dk_defl_create.  A dense Z is accepted when
-every row has at most one nonzero equal to 1 (it is converted to labels); other bases are
-outside the device path and raise UnsupportedOperator.
+Reference: defkrylov/deflation.py:19-104.  An indicator (piecewise-constant) basis — the
+physics-based PSL basis — is stored as one int32 column label per cell, never as a dense
+n x d matrix; E, its factorisation, E^-1 and x* = Z E^-1 Z^T b are built in HBM by
+dk_defl_create.  A dense Z whose rows have at most one nonzero equal to 1 is converted to
+labels.  Any other (dense) basis with d <= 64 columns — harmonic Ritz vectors (RDGMRES) or a
+user basis — is kept as dense rows on the device (dk_defl_create_dense); wider dense bases
+raise UnsupportedOperator.
 """
 from __future__ import annotations
 
@@ -19,6 +21,7 @@ from .errors import SingularCoarseMatrix
 from .sparse import SparseMatrix
 
 _DENSE_LIMIT = 1 << 26  # materialise Z / AZ densely only below this many entries
+DENSE_MAX_D = 64        # widest dense (non-indicator) basis of the device path
 
 
 class DeflationBasis:
@@ -74,16 +77,9 @@ class DeflationBasis:
         Z[np.flatnonzero(keep), self.labels[keep]] = 1.0
         return Z
 
-    def _require_indicator(self) -> np.ndarray:
-        if self.labels is not None:
-            return self.labels
-        Zd = self._dense
-        # two equal columns make E exactly singular (the reference's LU reports it)
-        cols = {Zd[:, j].tobytes() for j in range(Zd.shape[1])}
-        if len(cols) < Zd.shape[1]:
-            raise SingularCoarseMatrix("zero pivot in LU factorization")
-        raise UnsupportedOperator(
-            "the device path supports indicator bases (at most one unit entry per row)")
+    @property
+    def is_indicator(self) -> bool:
+        return self.labels is not None
 
 
 class DeflationContext:
@@ -176,14 +172,66 @@ def build_context(A: SparseMatrix, M, Z: DeflationBasis, b, A_p_choice: str = "A
     b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
     if b.shape != (A.n,):
         raise ValueError("right-hand side has wrong length")
-    labels = Z._require_indicator()
     op = A.device()
     op.set_precond(M)
     h = C.c_void_p()
     ap = _lib.DK_AP_AM if A_p_choice == "AM" else _lib.DK_AP_A
-    _lib.check(op._lib.dk_defl_create(C.byref(h), op.h, _lib.ptr(labels), Z.d, ap,
-                                      _lib.ptr(b)), "dk_defl_create")
+    if Z.is_indicator:
+        _lib.check(op._lib.dk_defl_create(C.byref(h), op.h, _lib.ptr(Z.labels), Z.d, ap,
+                                          _lib.ptr(b)), "dk_defl_create")
+    else:
+        if Z.d > DENSE_MAX_D:
+            raise UnsupportedOperator(
+                f"dense (non-indicator) deflation bases are limited to {DENSE_MAX_D} columns")
+        rows = np.ascontiguousarray(Z.Z.T)  # d x n: row k = basis vector k
+        _lib.check(op._lib.dk_defl_create_dense(C.byref(h), op.h, _lib.ptr(rows), Z.d, ap,
+                                                _lib.ptr(b)), "dk_defl_create_dense")
     return DeflationContext(Z, A, M, A_p_choice, h, op._lib)
+
+
+class _RitzBasis(DeflationBasis):
+    """Z = V_m Y formed on the device from the operator's last Arnoldi cycle; the dense view
+    is computed on demand from the cycle data (harmonic.py:91-94)."""
+
+    __slots__ = ("_data", "_Y")
+
+    def __init__(self, data, Y: np.ndarray):
+        self._data, self._Y = data, Y
+        self.labels = None
+        self._n = data._n
+        self._d = Y.shape[1]
+        self._dense = None
+
+    @property
+    def Z(self) -> np.ndarray:
+        if self._dense is None:
+            self._dense = self._data.V[:self._data.m].T @ self._Y
+        return self._dense
+
+
+def build_ritz_context(A: SparseMatrix, M, data, Y: np.ndarray, b,
+                       A_p_choice: str = "A") -> DeflationContext:
+    """Deflation context of the harmonic Ritz vectors Z = V_m Y of the last device cycle
+    (build_context(A, M, DeflationBasis(V_m Y), b) without moving V to the host)."""
+    if A_p_choice not in ("A", "AM"):
+        raise ValueError("A_p_choice must be 'A' or 'AM'")
+    Y = np.asfortranarray(np.asarray(Y, dtype=np.float64))
+    if Y.ndim != 2 or Y.shape[1] < 1:
+        raise ValueError("Z must be n x d with d >= 1")
+    rows, d = Y.shape
+    if d > DENSE_MAX_D:
+        raise UnsupportedOperator(
+            f"dense (non-indicator) deflation bases are limited to {DENSE_MAX_D} columns")
+    if not data.on_device():
+        raise RuntimeError("the Arnoldi basis was overwritten by a later solve")
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    op = A.device()
+    op.set_precond(M)
+    h = C.c_void_p()
+    ap = _lib.DK_AP_AM if A_p_choice == "AM" else _lib.DK_AP_A
+    _lib.check(op._lib.dk_defl_create_ritz(C.byref(h), op.h, Y.ctypes.data, rows, d, ap,
+                                           _lib.ptr(b)), "dk_defl_create_ritz")
+    return DeflationContext(_RitzBasis(data, Y), A, M, A_p_choice, h, op._lib)
 
 
 def apply_p1(ctx: DeflationContext | None, v) -> np.ndarray:

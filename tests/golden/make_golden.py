@@ -161,10 +161,65 @@ def make_config3_labels():
     print(f"config3 labels: d={part.d} ({sec:.1f}s)")
 
 
+def make_harmonic():
+    """RDGMRES, harmonic Ritz extraction and capture_ritz traces (harmonic.py, krylov.py)."""
+    out = {}
+    g, f, q, p = sandwich()
+    M = R.Preconditioner.jacobi(p.A)
+    for tag, kw in (("s3", dict(m=40, d=3, tol=1e-6)), ("s2", dict(m=40, d=2, tol=1e-8)),
+                    ("s3j", dict(M=M, m=40, d=3, tol=1e-6))):
+        rep = R.rdgmres(p.A, p.b, max_iters=300, **kw)
+        out[f"{tag}_iters"] = rep.iterations
+        out[f"{tag}_history"] = rep.residual_history
+        out[f"{tag}_x"] = rep.x
+        out[f"{tag}_flags"] = rep.deflated_flags
+        out[f"{tag}_from"] = -1 if rep.deflated_from_cycle is None else rep.deflated_from_cycle
+        out[f"{tag}_warning"] = rep.warning or ""
+        out[f"{tag}_relres"] = rep.final_relres
+    # hetero: Jacobi, A_p = A and AM, tight tolerance, several deflated cycles
+    h = np.load(HERE / "hetero.npz")
+    A = R.SparseMatrix(len(h["b"]), h["ro"], h["ci"], h["va"])
+    Mh = R.Preconditioner.jacobi(A)
+    for tag, ap in (("h", "A"), ("hAM", "AM")):
+        rep = R.rdgmres(A, h["b"], M=Mh, m=20, d=4, tol=1e-10, max_iters=2000, A_p_choice=ap)
+        out[f"{tag}_iters"] = rep.iterations
+        out[f"{tag}_history"] = rep.residual_history
+        out[f"{tag}_x"] = rep.x
+        out[f"{tag}_flags"] = rep.deflated_flags
+        out[f"{tag}_warning"] = rep.warning or ""
+    # capture_ritz traces of plain GMRES(20) on hetero (three cycles)
+    rep = R.gmres(A, h["b"], M=Mh, m=20, tol=1e-10, max_iters=60, capture_ritz=True)
+    out["cr_iters"] = rep.iterations
+    out["cr_cycles"] = np.array([len(t) for t in rep.ritz_trace])
+    out["cr_trace"] = np.concatenate(rep.ritz_trace)
+    out["cr_iter_trace"] = np.concatenate([np.asarray(t) for t in rep.ritz_iter_trace])
+    # extraction on fixed cycle data (the reference's own Arnoldi output)
+    data = rep.arnoldi
+    out["ad_V"], out["ad_H"], out["ad_m"] = data.V, data.Hbar, data.m
+    for d in (1, 4, 7):
+        hb = R.harmonic_ritz_b(data, d)
+        ha = R.harmonic_ritz_a(data, d)
+        out[f"hb{d}_thetas"], out[f"hb{d}_Y"], out[f"hb{d}_Z"] = hb.thetas, hb.Y, hb.Zvecs
+        out[f"ha{d}_thetas"], out[f"ha{d}_Y"] = ha.thetas, ha.Y
+    # a dense (non-indicator) basis through pdgmres: 3 smooth random columns
+    rng = np.random.default_rng(21)
+    Zd = np.cumsum(rng.standard_normal((A.n, 3)), axis=0) / np.sqrt(A.n)
+    basis = R.DeflationBasis(Zd)
+    ctx = R.build_context(A, Mh, basis, h["b"])
+    v = rng.standard_normal(A.n)
+    rep = R.pdgmres(A, h["b"], M=Mh, m=20, basis=basis, tol=1e-10, max_iters=2000)
+    out.update(dz_Z=Zd, dz_v=v, dz_p1v=ctx.apply_p1(v), dz_p2v=ctx.apply_p2(v),
+               dz_xs=ctx.x_star, dz_E=Zd.T @ ctx.AZ, dz_iters=rep.iterations,
+               dz_history=rep.residual_history, dz_x=rep.x)
+    np.savez_compressed(HERE / "harmonic.npz", **out)
+    print("harmonic:", {k: int(v) for k, v in out.items() if k.endswith("_iters")})
+
+
 if __name__ == "__main__":
     make_sandwich()
     make_random_hetero()
     make_config1()
+    make_harmonic()
     if "--big" in sys.argv:
         make_config3_labels()
         make_config2()
