@@ -97,6 +97,8 @@ struct dk_op {
   int part_q = 0;
   double* nrm = nullptr;  // [4] device norms
   unsigned int* tickets = nullptr;
+  unsigned int* gticket = nullptr;  // reduce_grouped counters
+  double* gpart = nullptr;          // reduce_grouped group partials [part_q x kGroupTickets]
   int* one = nullptr;  // device constant 1 (gate of ungated launches)
   // solver state
   State* st = nullptr;
@@ -221,7 +223,9 @@ int download(dk_op* op, double* dst, const double* src, long long count) {
 int ensure_part(dk_op* op, int q) {
   if (op->part_q < q) {
     if (op->part) DK_TRY(cudaFree(op->part));
+    if (op->gpart) DK_TRY(cudaFree(op->gpart));
     DK_TRY(cudaMalloc(&op->part, (size_t)q * op->G * sizeof(double)));
+    DK_TRY(cudaMalloc(&op->gpart, (size_t)q * kGroupTickets * sizeof(double)));
     op->part_q = q;
     op->g_m = -1;  // the graph refers to the old buffer
   }
@@ -277,6 +281,8 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.sn = p; p += m;
   sc.Gm = p; p += (size_t)(m + 1) * (m + 1);
   sc.gcol = p; p += m + 1;
+  sc.gticket = op->gticket;
+  sc.gpart = op->gpart;
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
@@ -675,6 +681,8 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   DK_TRY(cudaMallocHost(&op->st_host, sizeof(State)));
   DK_TRY(cudaMalloc(&op->nrm, 4 * sizeof(double)));
   DK_TRY(cudaMalloc(&op->tickets, 4 * sizeof(unsigned int)));
+  DK_TRY(cudaMalloc(&op->gticket, kGroupTickets * sizeof(unsigned int)));
+  DK_TRY(cudaMemsetAsync(op->gticket, 0, kGroupTickets * sizeof(unsigned int), op->stream));
   {
     const int one_h = 1;
     DK_TRY(cudaMalloc(&op->one, sizeof(int)));
@@ -697,7 +705,7 @@ int dk_op_destroy(dk_op* op) {
   cudaStreamSynchronize(op->stream);
   void* bufs[] = {op->dia, op->inv_base, op->w_base, op->x_base, op->b_base, op->x0_base,
                   op->t_base, op->part, op->nrm, op->tickets, op->one, op->st, op->scal,
-                  op->hist, op->rof};
+                  op->hist, op->rof, op->gticket, op->gpart};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (op->st_host) cudaFreeHost(op->st_host);

@@ -77,6 +77,8 @@ struct Scal {
   double* Gm;      // [(m+1)(m+1)] basis Gram matrix V^T V, column j holds rows 0..j
   double* gcol;    // [m+1]  V^T u of the last Gram-Schmidt vector u (normalised basis rows):
                    //        sigma_{j+1} gcol is the next Gram column (no extra pass over V)
+  unsigned int* gticket;  // [kGroupTickets] counters of reduce_grouped
+  double* gpart;          // [quantities x kGroupTickets] group partials of reduce_grouped
   double* hist;    // [max_iters+1]
   int* restart_of; // [max_iters+1]
   int m;
@@ -220,6 +222,78 @@ __device__ __forceinline__ void reduce_partials(const double* part, int nq, int 
     if (lane == 0) out[q] = s;
   }
   __syncthreads();
+}
+
+// Two-level deterministic reduction of per-block partials part[q * G + b], q < nq <= 64 per
+// pass: blocks are grouped by kGroup consecutive ids; the last block of a group sums its
+// group's partials (four threads per quantity, eight independent loads each) into
+// gpart[q * ng + g]; the last group to finish sums the group partials into out[q].  Returns
+// true in that one block.  One L2 round trip per level instead of G / 32 dependent loads per
+// quantity for a single-level sweep.  gticket: kGroupTickets zeroed counters (reset on exit).
+constexpr int kGroup = 32, kGroupTickets = 32;
+__device__ __forceinline__ bool reduce_grouped(const double* part, int nq, int G,
+                                               unsigned int* gticket, double* gpart,
+                                               double* out) {
+  __shared__ int s_flag;
+  const int ng = (G + kGroup - 1) / kGroup;
+  const int g = blockIdx.x / kGroup, gb = g * kGroup;
+  const int gsz = (G - gb < kGroup) ? G - gb : kGroup;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_flag = (atomicAdd(&gticket[g], 1u) == (unsigned)(gsz - 1));
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  if (threadIdx.x == 0) gticket[g] = 0u;
+  for (int q0 = 0; q0 < nq; q0 += (int)blockDim.x / 4) {
+    const int q = q0 + (int)threadIdx.x / 4, h = threadIdx.x & 3;
+    if (q < nq) {
+      const double* p = part + (size_t)q * G + gb + 8 * h;
+      double v[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) v[b] = (8 * h + b < gsz) ? __ldcg(p + b) : 0.0;
+      double t = 0.0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) t += v[b];
+      out[4 * (q - q0) + h] = t;
+    }
+    __syncthreads();
+    if (h == 0 && q < nq) {
+      const double* t = out + 4 * (q - q0);
+      __stcg(gpart + (size_t)q * ng + g, ((t[0] + t[1]) + t[2]) + t[3]);
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    s_flag = (atomicAdd(&gticket[kGroupTickets - 1], 1u) == (unsigned)(ng - 1));
+  __syncthreads();
+  if (!s_flag) return false;
+  __threadfence();
+  if (threadIdx.x == 0) gticket[kGroupTickets - 1] = 0u;
+  // ng <= 31 group partials per quantity, in group order
+  double* tmp = out + nq;
+  for (int q0 = 0; q0 < nq; q0 += (int)blockDim.x / 4) {
+    const int q = q0 + (int)threadIdx.x / 4, h = threadIdx.x & 3;
+    if (q < nq) {
+      const double* p = gpart + (size_t)q * ng + 8 * h;
+      double v[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) v[b] = (8 * h + b < ng) ? __ldcg(p + b) : 0.0;
+      double t = 0.0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) t += v[b];
+      tmp[4 * (q - q0) + h] = t;
+    }
+    __syncthreads();
+    if (h == 0 && q < nq) {
+      const double* t = tmp + 4 * (q - q0);
+      out[q] = ((t[0] + t[1]) + t[2]) + t[3];
+    }
+    __syncthreads();
+  }
+  return true;
 }
 
 }  // namespace dk

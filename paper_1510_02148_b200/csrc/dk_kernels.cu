@@ -660,8 +660,7 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
     for (int w2 = 0; w2 < kWarps; ++w2) s += red[q * kWarps + w2];
     part[(size_t)q * G + blockIdx.x] = s;
   }
-  if (!last_block(&sc.st->ticket[MODE == PJ_REDOTS ? 3 : 0])) return;
-  reduce_partials(part, nq, G, red);
+  if (!reduce_grouped(part, nq, G, sc.gticket, sc.gpart, red)) return;
   State* st = sc.st;
   const int m = sc.m;
   if (MODE == PJ_RESTART) {
@@ -698,6 +697,7 @@ static void project_t(const Dia& A, const Prolong& lab, const double* yc, const 
   int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
   const int tail = 3 * nvec + 1 + nvec * nvec;  // PJ_ITER re-orthogonalisation test scratch
   if (MODE == PJ_ITER && tail > slots) slots = tail;
+  if (nq + 260 > slots) slots = nq + 260;  // reduce_grouped scratch
   const size_t smem = (size_t)slots * sizeof(double);
   static bool attr = false;  // one per instantiation: dynamic + 32 KB static > 48 KB default
   if (!attr) {
@@ -929,8 +929,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     for (int w2 = 0; w2 < kWarps; ++w2) s += red[w2];
     part[blockIdx.x] = s;
   }
-  if (!last_block(&sc.st->ticket[REORTH ? 2 : 1])) return;
-  reduce_partials(part, 1, G, red);
+  if (!reduce_grouped(part, 1, G, sc.gticket, sc.gpart, red)) return;
   const double hj1 = sqrt(red[0]);
   __syncthreads();
   if (!REORTH && sc.st->reorth) return;  // the second pass finishes the iteration
@@ -940,7 +939,8 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
 void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
                int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                const int* gate, cudaStream_t s) {
-  const int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
+  int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
+  if (slots < 261) slots = 261;  // reduce_grouped scratch
   const size_t smem = ((size_t)nvec + (size_t)slots) * sizeof(double);
   if (reorth)
     launch_pdl(k_gs<true>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
