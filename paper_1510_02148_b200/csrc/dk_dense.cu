@@ -15,6 +15,7 @@
 //     singularity semantics exactly.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <vector>
@@ -388,6 +389,26 @@ __global__ void __launch_bounds__(32 * DNW, 1) k_chol_diag(const double* __restr
   }
 }
 
+// f[r] = first column with E[r][c] != 0 (c <= r; r when none): the row profile.  Cholesky
+// keeps it (no fill left of the first nonzero), so panel products touch only the rows whose
+// profile reaches the panel.  One warp per row, 32 columns per step.
+__global__ void k_row_first_nz(const double* __restrict__ E, int d, int ld, int* __restrict__ f) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < d;
+       r += gridDim.x * (blockDim.x >> 5)) {
+    int first = r;
+    for (int c0 = 0; c0 < r; c0 += 32) {
+      const int c = c0 + lane;
+      const unsigned nz = __ballot_sync(0xffffffffu, c < r && E[(long long)r * ld + c] != 0.0);
+      if (nz) {
+        first = c0 + __ffs(nz) - 1;
+        break;
+      }
+    }
+    if (lane == 0) f[r] = first;
+  }
+}
+
 // X[j][i] = X[i][j] for i < j (copy the upper triangle onto the lower), 32 x 32 tiles.
 __global__ void __launch_bounds__(256) k_mirror_upper(double* __restrict__ X, int d, int ld) {
   __shared__ double tile[32][33];
@@ -441,6 +462,25 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
   double* dpmin = nullptr;
   cudaMallocAsync(&dpmin, nblk * sizeof(double), s);
   cudaMemsetAsync(W, 0, (size_t)d * ld * sizeof(double), s);
+  // row profile -> reach(t) = 1 + the last row whose profile starts left of column t: the rows
+  // of L that can be nonzero in columns < t lie in [t, reach(t))
+  std::vector<int> reach(d + 1, 0);
+  {
+    int* df = nullptr;
+    std::vector<int> f(d);
+    cudaMallocAsync(&df, (size_t)d * sizeof(int), s);
+    k_row_first_nz<<<148 * 4, 256, 0, s>>>(L, d, ld, df);
+    cudaMemcpyAsync(f.data(), df, (size_t)d * sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(df, s);
+    cudaStreamSynchronize(s);
+    std::vector<int> last(d, -1);  // last row whose profile starts at column c
+    for (int r = 0; r < d; ++r) last[f[r]] = std::max(last[f[r]], r);
+    int mx = -1;
+    for (int t = 1; t <= d; ++t) {
+      mx = std::max(mx, last[t - 1]);
+      reach[t] = std::max(t, mx + 1);
+    }
+  }
   // 1. E = L L^T, right-looking by DB-wide blocks in groups of GB columns: the diagonal block
   //    is factorised and inverted by one CTA (L11^-1 lands on W's diagonal), the block column
   //    below becomes L21 = A21 L11^-T (in place: one tile column, each CTA owns its rows);
@@ -452,14 +492,20 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
     const int G0 = (K0 / GB) * GB, gend = (d - G0 < GB) ? d : G0 + GB;
     k_chol_diag<<<1, 32 * DNW, kDiagSmem, s>>>(L, ld, K0, nb, W, dpmin, q);
     if (rest <= 0) break;
-    gemm_mma(false, true, at(L, Kend, K0), ld, at(W, K0, K0), ld, at(L, Kend, K0), ld, rest, nb,
-             nb, 1.0, 0.0, 0, INT_MIN, s);
-    if (Kend < gend)
-      gemm_mma(false, true, at(L, Kend, K0), ld, at(L, Kend, K0), ld, at(L, Kend, Kend), ld, rest,
-               gend - Kend, nb, -1.0, 1.0, 0, INT_MIN, s);
-    else
-      gemm_mma(false, true, at(L, Kend, G0), ld, at(L, Kend, G0), ld, at(L, Kend, Kend), ld, rest,
-               rest, Kend - G0, -1.0, 1.0, 1, INT_MIN, s);
+    const int rq = reach[Kend] - Kend;  // rows below the block inside the profile
+    if (rq > 0)
+      gemm_mma(false, true, at(L, Kend, K0), ld, at(W, K0, K0), ld, at(L, Kend, K0), ld, rq, nb,
+               nb, 1.0, 0.0, 0, INT_MIN, s);
+    if (Kend < gend) {
+      if (rq > 0)
+        gemm_mma(false, true, at(L, Kend, K0), ld, at(L, Kend, K0), ld, at(L, Kend, Kend), ld, rq,
+                 gend - Kend, nb, -1.0, 1.0, 0, INT_MIN, s);
+    } else {
+      const int rg = reach[Kend] - Kend;
+      if (rg > 0)
+        gemm_mma(false, true, at(L, Kend, G0), ld, at(L, Kend, G0), ld, at(L, Kend, Kend), ld, rg,
+                 rg, Kend - G0, -1.0, 1.0, 1, INT_MIN, s);
+    }
   }
   std::vector<double> pm(nblk);
   cudaMemcpyAsync(pm.data(), dpmin, nblk * sizeof(double), cudaMemcpyDeviceToHost, s);
@@ -488,11 +534,14 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
       gemm_mma(false, false, at(W, K0, K0), ld, at(W, K0, 0), ld, at(W, K0, 0), ld, nb, K0, nb,
                1.0, 0.0, 0, INT_MIN, s);
     if (rest <= 0) break;
+    // L's rows below the profile reach are zero in these columns: no contribution
+    const int rq = std::min(reach[Kend], Kend < gend ? gend : d) - Kend;
+    if (rq <= 0) continue;
     if (Kend < gend)
-      gemm_mma(false, false, at(L, Kend, K0), ld, at(W, K0, 0), ld, at(W, Kend, 0), ld,
-               gend - Kend, Kend, nb, -1.0, 1.0, 0, -K0, s);
+      gemm_mma(false, false, at(L, Kend, K0), ld, at(W, K0, 0), ld, at(W, Kend, 0), ld, rq, Kend,
+               nb, -1.0, 1.0, 0, -K0, s);
     else
-      gemm_mma(false, false, at(L, Kend, G0), ld, at(W, G0, 0), ld, at(W, Kend, 0), ld, rest, Kend,
+      gemm_mma(false, false, at(L, Kend, G0), ld, at(W, G0, 0), ld, at(W, Kend, 0), ld, rq, Kend,
                Kend - G0, -1.0, 1.0, 0, -G0, s);
   }
   // 3. E^-1 = W^T W: upper tiles into L's storage (A = W^T, B = W lower: K from the tile

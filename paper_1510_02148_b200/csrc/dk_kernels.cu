@@ -131,11 +131,9 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
   const long long base = (long long)blockIdx.x * kTile;
   const bool has_scale = (MODE == ST_APPLY) && scale != nullptr;
   const double sc = has_scale ? *scale : 1.0;
-  // a tile inside one region is a single run: plain block sum instead of the segmented scan
-  const bool one_run =
-      RESTRICT && (tile_run_off[blockIdx.x + 1] - tile_run_off[blockIdx.x] == 1);
-  double tsum = 0.0;
-#pragma unroll 2
+  double rr[8];
+  int2 lb[4];
+#pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int loc = 2 * threadIdx.x + 512 * k;
     const long long i = base + loc;
@@ -189,16 +187,25 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
       }
     }
     if (WRITE) st2(out + i, make_double2(r0, r1));
-    if (RESTRICT) {
+    rr[2 * k] = r0;
+    rr[2 * k + 1] = r1;
+    if (RESTRICT) lb[k] = *reinterpret_cast<const int2*>(lab + i);
+  }
+  // a tile inside one region is a single run: plain block sum instead of the segmented scan
+  const bool one_run =
+      RESTRICT && (tile_run_off[blockIdx.x + 1] - tile_run_off[blockIdx.x] == 1);
+  double tsum = 0.0;
+  if (RESTRICT) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
       if (one_run) {
-        tsum = __dadd_rn(tsum, __dadd_rn(r0, r1));
+        tsum = __dadd_rn(tsum, __dadd_rn(rr[2 * k], rr[2 * k + 1]));
       } else {
-        const int p = pidx(loc);
-        sw[p] = r0;
-        sw[p + 1] = r1;
-        const int2 l = *reinterpret_cast<const int2*>(lab + i);
-        sl[p] = l.x;
-        sl[p + 1] = l.y;
+        const int p = pidx(2 * threadIdx.x + 512 * k);
+        sw[p] = rr[2 * k];
+        sw[p + 1] = rr[2 * k + 1];
+        sl[p] = lb[k].x;
+        sl[p + 1] = lb[k].y;
       }
     }
   }
