@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -188,6 +189,28 @@ Dia make_dia(const dk_op* op, bool with_inv) {
 
 int defl_kind(const dk_defl* c) { return !c ? DK_NONE : c->dense ? DK_DENSE : DK_LABELS; }
 
+// pinned State mirrors are recycled across operators: cudaFreeHost / cudaMallocHost are slow
+// and synchronising, and an operator is created per matrix
+std::mutex g_pinned_mu;
+std::vector<State*> g_pinned_free;
+
+cudaError_t pinned_state(State** out) {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      *out = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaMallocHost(out, sizeof(State));
+}
+
+void pinned_state_release(State* p) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
 // flag <- 0 unless lo[i + o] == up[i] for i in [0, count)  (bitwise symmetry of a pair)
 __global__ void k_check_pair(const double* __restrict__ up, const double* __restrict__ lo,
                              long long o, long long count, int* flag) {
@@ -197,7 +220,7 @@ __global__ void k_check_pair(const double* __restrict__ up, const double* __rest
 }
 
 int alloc_vec(dk_op* op, double** base, double** ptr) {
-  DK_TRY(cudaMalloc(base, (size_t)op->vlen * sizeof(double)));
+  DK_TRY(cudaMallocAsync(base, (size_t)op->vlen * sizeof(double), op->stream));
   DK_TRY(cudaMemsetAsync(*base, 0, (size_t)op->vlen * sizeof(double), op->stream));
   *ptr = *base + op->guard;
   return DK_OK;
@@ -222,10 +245,10 @@ int download(dk_op* op, double* dst, const double* src, long long count) {
 // per-block partials: room for q quantities per launch
 int ensure_part(dk_op* op, int q) {
   if (op->part_q < q) {
-    if (op->part) DK_TRY(cudaFree(op->part));
-    if (op->gpart) DK_TRY(cudaFree(op->gpart));
-    DK_TRY(cudaMalloc(&op->part, (size_t)q * op->G * sizeof(double)));
-    DK_TRY(cudaMalloc(&op->gpart, (size_t)q * kGroupTickets * sizeof(double)));
+    if (op->part) DK_TRY(cudaFreeAsync(op->part, op->stream));
+    if (op->gpart) DK_TRY(cudaFreeAsync(op->gpart, op->stream));
+    DK_TRY(cudaMallocAsync(&op->part, (size_t)q * op->G * sizeof(double), op->stream));
+    DK_TRY(cudaMallocAsync(&op->gpart, (size_t)q * kGroupTickets * sizeof(double), op->stream));
     op->part_q = q;
     op->g_m = -1;  // the graph refers to the old buffer
   }
@@ -249,19 +272,19 @@ int ensure_work(dk_op* op, int m, int max_iters) {
     if (rc) return rc;
   }
   if (op->scal_m < m) {
-    if (op->scal) DK_TRY(cudaFree(op->scal));
+    if (op->scal) DK_TRY(cudaFreeAsync(op->scal, op->stream));
     const size_t cnt = 6 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
                        (size_t)(m + 1) * (m + 1);
-    DK_TRY(cudaMalloc(&op->scal, cnt * sizeof(double)));
+    DK_TRY(cudaMallocAsync(&op->scal, cnt * sizeof(double), op->stream));
     DK_TRY(cudaMemsetAsync(op->scal, 0, cnt * sizeof(double), op->stream));
     op->scal_m = m;
     op->g_m = -1;
   }
   if (op->hist_cap < max_iters + 1) {
-    if (op->hist) DK_TRY(cudaFree(op->hist));
-    if (op->rof) DK_TRY(cudaFree(op->rof));
-    DK_TRY(cudaMalloc(&op->hist, (size_t)(max_iters + 1) * sizeof(double)));
-    DK_TRY(cudaMalloc(&op->rof, (size_t)(max_iters + 1) * sizeof(int)));
+    if (op->hist) DK_TRY(cudaFreeAsync(op->hist, op->stream));
+    if (op->rof) DK_TRY(cudaFreeAsync(op->rof, op->stream));
+    DK_TRY(cudaMallocAsync(&op->hist, (size_t)(max_iters + 1) * sizeof(double), op->stream));
+    DK_TRY(cudaMallocAsync(&op->rof, (size_t)(max_iters + 1) * sizeof(int), op->stream));
     op->hist_cap = max_iters + 1;
     op->g_m = -1;
   }
@@ -581,7 +604,7 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   // per-block partial sums, and hence every reduction, are deterministic)
   op->G = (int)std::min<long long>(nch, 148 * 4);
   // all diagonals, guarded, ascending offsets
-  DK_TRY(cudaMalloc(&op->dia, (size_t)ndiag * op->vlen * sizeof(double)));
+  DK_TRY(cudaMallocAsync(&op->dia, (size_t)ndiag * op->vlen * sizeof(double), op->stream));
   DK_TRY(cudaMemsetAsync(op->dia, 0, (size_t)ndiag * op->vlen * sizeof(double), op->stream));
   for (int k = 0; k < ndiag; ++k) {
     DK_TRY(cudaMemcpyAsync(op->dia + (size_t)k * op->vlen + op->guard,
@@ -603,15 +626,15 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
       }
       int* f = nullptr;
       int one_h = 1;
-      DK_TRY(cudaMalloc(&f, sizeof(int)));
-      DK_TRY(cudaMemcpy(f, &one_h, sizeof(int), cudaMemcpyHostToDevice));
+      DK_TRY(cudaMallocAsync(&f, sizeof(int), op->stream));
+      DK_TRY(cudaMemcpyAsync(f, &one_h, sizeof(int), cudaMemcpyHostToDevice, op->stream));
       k_check_pair<<<148 * 4, 256, 0, op->stream>>>(op->dia + (size_t)k * op->vlen + op->guard,
                                                     op->dia + (size_t)partner * op->vlen +
                                                         op->guard,
                                                     o, n - o, f);
       DK_TRY(cudaMemcpyAsync(&one_h, f, sizeof(int), cudaMemcpyDeviceToHost, op->stream));
       DK_TRY(cudaStreamSynchronize(op->stream));
-      cudaFree(f);
+      cudaFreeAsync(f, op->stream);
       sym = one_h;
     }
     int npos = 0, nneg = 0;
@@ -638,7 +661,7 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
       int nst = 0;
       for (int k = 0; k < ndiag; ++k)
         if (op->off[k] >= 0) ++nst;
-      DK_TRY(cudaMalloc(&compact, (size_t)nst * op->vlen * sizeof(double)));
+      DK_TRY(cudaMallocAsync(&compact, (size_t)nst * op->vlen * sizeof(double), op->stream));
       int slot = 0;
       long long pos_slot[kMaxDiag];
       for (int k = 0; k < ndiag; ++k) {
@@ -656,8 +679,7 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
             if (op->off[q] == -o) src = q;
         op->co[k] = compact + (size_t)pos_slot[src] * op->vlen + op->guard;
       }
-      DK_TRY(cudaStreamSynchronize(op->stream));
-      cudaFree(op->dia);
+      cudaFreeAsync(op->dia, op->stream);
       op->dia = compact;
       op->nstore = nst;
     } else {
@@ -676,17 +698,17 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   if ((rc = alloc_vec(op, &op->b_base, &op->b))) return rc;
   if ((rc = alloc_vec(op, &op->x0_base, &op->x0))) return rc;
   if ((rc = alloc_vec(op, &op->t_base, &op->t))) return rc;
-  DK_TRY(cudaMalloc(&op->st, sizeof(State)));
+  DK_TRY(cudaMallocAsync(&op->st, sizeof(State), op->stream));
   DK_TRY(cudaMemsetAsync(op->st, 0, sizeof(State), op->stream));
-  DK_TRY(cudaMallocHost(&op->st_host, sizeof(State)));
-  DK_TRY(cudaMalloc(&op->nrm, 4 * sizeof(double)));
-  DK_TRY(cudaMalloc(&op->tickets, 4 * sizeof(unsigned int)));
-  DK_TRY(cudaMalloc(&op->gticket, kGroupTickets * sizeof(unsigned int)));
+  DK_TRY(pinned_state(&op->st_host));
+  DK_TRY(cudaMallocAsync(&op->nrm, 4 * sizeof(double), op->stream));
+  DK_TRY(cudaMallocAsync(&op->tickets, 4 * sizeof(unsigned int), op->stream));
+  DK_TRY(cudaMallocAsync(&op->gticket, kGroupTickets * sizeof(unsigned int), op->stream));
   DK_TRY(cudaMemsetAsync(op->gticket, 0, kGroupTickets * sizeof(unsigned int), op->stream));
   {
     const int one_h = 1;
-    DK_TRY(cudaMalloc(&op->one, sizeof(int)));
-    DK_TRY(cudaMemcpy(op->one, &one_h, sizeof(int), cudaMemcpyHostToDevice));
+    DK_TRY(cudaMallocAsync(&op->one, sizeof(int), op->stream));
+    DK_TRY(cudaMemcpyAsync(op->one, &one_h, sizeof(int), cudaMemcpyHostToDevice, op->stream));
   }
   DK_TRY(cudaMemsetAsync(op->tickets, 0, 4 * sizeof(unsigned int), op->stream));
   rc = ensure_work(op, 1, 1);
@@ -701,14 +723,14 @@ int dk_op_destroy(dk_op* op) {
   cudaStreamSynchronize(op->stream);
   if (op->gexec) cudaGraphExecDestroy(op->gexec);
   for (auto e : op->ev_pool) cudaEventDestroy(e);
-  if (op->V_base) cudaFreeAsync(op->V_base, op->stream);
-  cudaStreamSynchronize(op->stream);
-  void* bufs[] = {op->dia, op->inv_base, op->w_base, op->x_base, op->b_base, op->x0_base,
-                  op->t_base, op->part, op->nrm, op->tickets, op->one, op->st, op->scal,
-                  op->hist, op->rof, op->gticket, op->gpart};
+  // all device buffers of an operator come from the stream-ordered pool
+  void* bufs[] = {op->V_base, op->dia,     op->inv_base, op->w_base, op->x_base, op->b_base,
+                  op->x0_base, op->t_base, op->part,     op->nrm,    op->tickets, op->one,
+                  op->st,     op->scal,    op->hist,     op->rof,    op->gticket, op->gpart};
   for (void* p : bufs)
-    if (p) cudaFree(p);
-  if (op->st_host) cudaFreeHost(op->st_host);
+    if (p) cudaFreeAsync(p, op->stream);
+  cudaStreamSynchronize(op->stream);
+  if (op->st_host) pinned_state_release(op->st_host);
   if (op->own) cudaStreamDestroy(op->own);
   delete op;
   return DK_OK;
@@ -855,36 +877,36 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     cudaError_t _e = (x);                                \
     if (_e != cudaSuccess) return cleanup_fail(_e, #x);  \
   } while (0)
-  DKD(cudaMalloc(&c->lab_base, (size_t)op->vlen * sizeof(int)));
+  DKD(cudaMallocAsync(&c->lab_base, (size_t)op->vlen * sizeof(int), s));
   DKD(cudaMemsetAsync(c->lab_base, 0xff, (size_t)op->vlen * sizeof(int), s));  // -1
   c->lab = c->lab_base + op->guard;
   DKD(cudaMemcpyAsync(c->lab, lab.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice, s));
-  DKD(cudaMalloc(&c->tile_run_off, tile_off.size() * sizeof(int)));
+  DKD(cudaMallocAsync(&c->tile_run_off, tile_off.size() * sizeof(int), s));
   DKD(cudaMemcpyAsync(c->tile_run_off, tile_off.data(), tile_off.size() * sizeof(int),
                       cudaMemcpyHostToDevice, s));
-  DKD(cudaMalloc(&c->run_part, (size_t)nruns * sizeof(double)));
-  DKD(cudaMalloc(&c->lab_run_ptr, ptr.size() * sizeof(int)));
+  DKD(cudaMallocAsync(&c->run_part, (size_t)nruns * sizeof(double), s));
+  DKD(cudaMallocAsync(&c->lab_run_ptr, ptr.size() * sizeof(int), s));
   DKD(cudaMemcpyAsync(c->lab_run_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
-  DKD(cudaMalloc(&c->run_slot, slot.size() * sizeof(int)));
+  DKD(cudaMallocAsync(&c->run_slot, slot.size() * sizeof(int), s));
   DKD(cudaMemcpyAsync(c->run_slot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
   // the O(d^2) buffers come from the stream-ordered pool (cached across contexts)
   DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMallocAsync(&c->Einv, (size_t)d * c->ld * sizeof(double), s));
-  DKD(cudaMalloc(&c->piv, (size_t)d * sizeof(int)));
-  DKD(cudaMalloc(&c->s, (size_t)c->ld * sizeof(double)));
-  DKD(cudaMalloc(&c->y, (size_t)c->ld * sizeof(double)));
+  DKD(cudaMallocAsync(&c->piv, (size_t)d * sizeof(int), s));
+  DKD(cudaMallocAsync(&c->s, (size_t)c->ld * sizeof(double), s));
+  DKD(cudaMallocAsync(&c->y, (size_t)c->ld * sizeof(double), s));
   DKD(cudaMemsetAsync(c->s, 0, (size_t)c->ld * sizeof(double), s));
   DKD(cudaMemsetAsync(c->y, 0, (size_t)c->ld * sizeof(double), s));
-  DKD(cudaMalloc(&c->xs_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMallocAsync(&c->xs_base, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMemsetAsync(c->xs_base, 0, (size_t)op->vlen * sizeof(double), s));
   c->xs = c->xs_base + op->guard;
-  DKD(cudaMalloc(&c->qv_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMallocAsync(&c->qv_base, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMemsetAsync(c->qv_base, 0, (size_t)op->vlen * sizeof(double), s));
-  DKD(cudaMalloc(&c->own_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMallocAsync(&c->own_base, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMemsetAsync(c->own_base, 0, (size_t)op->vlen * sizeof(double), s));
-  DKD(cudaMalloc(&c->mask_base, (size_t)op->vlen));
+  DKD(cudaMallocAsync(&c->mask_base, (size_t)op->vlen, s));
   DKD(cudaMemsetAsync(c->mask_base, 0, (size_t)op->vlen, s));
   c->pro.lab = c->lab;
   c->pro.own = c->own_base + op->guard;
@@ -914,7 +936,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
       if (ptr[L + 1] - ptr[L] > kShortRuns) long_ids.push_back(L);
     c->rm.nlong = (int)long_ids.size();
     if (!long_ids.empty()) {
-      DKD(cudaMalloc(&c->long_ids, long_ids.size() * sizeof(int)));
+      DKD(cudaMallocAsync(&c->long_ids, long_ids.size() * sizeof(int), s));
       DKD(cudaMemcpyAsync(c->long_ids, long_ids.data(), long_ids.size() * sizeof(int),
                           cudaMemcpyHostToDevice, s));
       DKD(cudaStreamSynchronize(s));
@@ -972,14 +994,14 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     c->sym = 1;
     c->ntiles = symv_tiles(d);
     DKD(cudaMallocAsync(&c->P, (size_t)c->ntiles * 1024 * sizeof(double), s));
-    DKD(cudaMalloc(&c->rowpart, (size_t)c->ntiles * 32 * sizeof(double)));
-    DKD(cudaMalloc(&c->colpart, (size_t)c->ntiles * 32 * sizeof(double)));
+    DKD(cudaMallocAsync(&c->rowpart, (size_t)c->ntiles * 32 * sizeof(double), s));
+    DKD(cudaMallocAsync(&c->colpart, (size_t)c->ntiles * 32 * sizeof(double), s));
     launch_symv_pack(c->Einv, d, c->ld, c->P, s);
     DKD(cudaGetLastError());
     std::vector<int> sp, ss;
     symv_segments(d, sp, ss);
-    DKD(cudaMalloc(&c->seg_ptr, sp.size() * sizeof(int)));
-    DKD(cudaMalloc(&c->seg_slot, ss.size() * sizeof(int)));
+    DKD(cudaMallocAsync(&c->seg_ptr, sp.size() * sizeof(int), s));
+    DKD(cudaMallocAsync(&c->seg_slot, ss.size() * sizeof(int), s));
     DKD(cudaMemcpyAsync(c->seg_ptr, sp.data(), sp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
     DKD(cudaMemcpyAsync(c->seg_slot, ss.data(), ss.size() * sizeof(int), cudaMemcpyHostToDevice,
                         s));
@@ -1054,14 +1076,14 @@ static int defl_create_dense(dk_defl** out, dk_op* op, int32_t d, int32_t ap_cho
   DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMallocAsync(&c->Einv, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMemsetAsync(c->E, 0, (size_t)d * c->ld * sizeof(double), s));
-  DKD(cudaMalloc(&c->piv, (size_t)d * sizeof(int)));
-  DKD(cudaMalloc(&c->s, (size_t)c->ld * sizeof(double)));
-  DKD(cudaMalloc(&c->y, (size_t)c->ld * sizeof(double)));
+  DKD(cudaMallocAsync(&c->piv, (size_t)d * sizeof(int), s));
+  DKD(cudaMallocAsync(&c->s, (size_t)c->ld * sizeof(double), s));
+  DKD(cudaMallocAsync(&c->y, (size_t)c->ld * sizeof(double), s));
   DKD(cudaMemsetAsync(c->y, 0, (size_t)c->ld * sizeof(double), s));
-  DKD(cudaMalloc(&c->xs_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMallocAsync(&c->xs_base, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMemsetAsync(c->xs_base, 0, (size_t)op->vlen * sizeof(double), s));
   c->xs = c->xs_base + op->guard;
-  DKD(cudaMalloc(&c->qv_base, (size_t)op->vlen * sizeof(double)));
+  DKD(cudaMallocAsync(&c->qv_base, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMemsetAsync(c->qv_base, 0, (size_t)op->vlen * sizeof(double), s));
   {
     const int rc = fill(c);
@@ -1158,15 +1180,15 @@ int dk_defl_destroy(dk_defl* c) {
   if (!c) return DK_OK;
   cudaStream_t s = c->op ? c->op->stream : nullptr;
   if (c->op) cudaStreamSynchronize(s);
-  void* pooled[] = {c->E, c->Einv, c->P, c->Z_base, c->AZ_base};  // stream-ordered pool
-  for (void* p : pooled)
-    if (p) cudaFreeAsync(p, s);
-  void* bufs[] = {c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
+  // every buffer of a context comes from the stream-ordered pool: no device-wide
+  // synchronisation or OS-level free on destruction
+  void* bufs[] = {c->E,        c->Einv,         c->P,        c->Z_base,      c->AZ_base,
+                  c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
                   c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
                   c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->seg_ptr,
                   c->seg_slot, c->long_ids};
   for (void* p : bufs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   if (c->op) cudaStreamSynchronize(s);
   delete c;
   return DK_OK;

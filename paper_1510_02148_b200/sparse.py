@@ -60,7 +60,8 @@ class SparseMatrix:
         offsets = np.asarray(offsets, dtype=np.int64)
         diags = np.ascontiguousarray(np.asarray(diags, dtype=np.float64))
         order = np.argsort(offsets, kind="stable")
-        offsets, diags = offsets[order], diags[order]
+        if np.any(order != np.arange(len(order))):  # reorder (copies) only when needed
+            offsets, diags = offsets[order], diags[order]
         if diags.shape != (len(offsets), n):
             raise ValueError("diags must be ndiag x n")
         if len(offsets) > MAX_DIAGONALS or len(np.unique(offsets)) != len(offsets):
