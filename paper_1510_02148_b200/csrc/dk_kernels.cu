@@ -128,9 +128,32 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
   __shared__ double sw[RESTRICT ? kTilePad : 2];
   __shared__ int sl[RESTRICT ? kTilePad : 2];
   __shared__ double wsum[kWarps];
+  // ST_APPLY: the scaled, Jacobi-preconditioned input p = (sigma v) M^-1 of the tile and a
+  // +-kHalo halo is staged in shared memory once; the in-plane neighbours (|offset| <= kHalo:
+  // +-1, +-nx) read it there, the z-plane neighbours straight from L2
+  constexpr int kHalo = 128;
+  constexpr bool STAGE = (MODE == ST_APPLY);
+  __shared__ __align__(16) double sp[STAGE ? kTile + 2 * kHalo : 2];
   const long long base = (long long)blockIdx.x * kTile;
   const bool has_scale = (MODE == ST_APPLY) && scale != nullptr;
   const double sc = has_scale ? *scale : 1.0;
+  if (STAGE) {
+    for (int e = threadIdx.x; e < (kTile + 2 * kHalo) / 2; e += kThreads) {
+      const long long i = base - kHalo + 2 * e;
+      double2 x = ld2(v + i);
+      if (has_scale) {
+        x.x = __dmul_rn(x.x, sc);
+        x.y = __dmul_rn(x.y, sc);
+      }
+      if (PRE) {
+        const double2 m = ld2(A.inv + i);
+        x.x = __dmul_rn(x.x, m.x);
+        x.y = __dmul_rn(x.y, m.y);
+      }
+      reinterpret_cast<double2*>(sp)[e] = x;
+    }
+    __syncthreads();
+  }
   double rr[8];
   int2 lb[4];
 #pragma unroll
@@ -150,6 +173,12 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
           const double2 a = (A.csh[q] & 1)
                                 ? make_double2(dia_coef(A, q, i), dia_coef(A, q, i + 1))
                                 : ld2(A.co[q] + i + A.csh[q]);
+          if (STAGE && o >= -kHalo && o <= kHalo) {
+            const double* pp = sp + kHalo + loc + o;
+            r0 = __dadd_rn(r0, __dmul_rn(a.x, pp[0]));
+            r1 = __dadd_rn(r1, __dmul_rn(a.y, pp[1]));
+            continue;
+          }
           double x0, x1, m0 = 1.0, m1 = 1.0;
           if ((o & 1) == 0) {  // even offset: aligned 16 B loads of the neighbour pair
             const double2 xv = ld2(v + i + o);
