@@ -9,7 +9,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -189,6 +191,80 @@ Dia make_dia(const dk_op* op, bool with_inv) {
 
 int defl_kind(const dk_defl* c) { return !c ? DK_NONE : c->dense ? DK_DENSE : DK_LABELS; }
 
+// Cache of GB-sized device buffers (Krylov basis, E, E^-1, the packed E^-1): kept across
+// operators and contexts instead of returned to the pool, whose re-growth (mapping fresh
+// memory for a 1 GB block) occasionally took 0.03-1 s.  Same-stream reuse only (the library
+// stream of the device), so stream order alone protects a recycled block.
+struct BigBlock {
+  void* p;
+  size_t bytes;
+  int dev;
+};
+std::mutex g_big_mu;
+std::vector<BigBlock> g_big_free;
+std::vector<BigBlock> g_big_live;
+constexpr size_t kBigMin = 64ull << 20;
+constexpr size_t kBigCacheCap = 48ull << 30;
+
+cudaError_t big_alloc(void** out, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (bytes >= kBigMin) {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_big_free.size(); ++i) {
+      const BigBlock& b = g_big_free[i];
+      if (b.dev == dev && b.bytes >= bytes && b.bytes <= 2 * bytes &&
+          (best < 0 || b.bytes < g_big_free[best].bytes))
+        best = i;
+    }
+    if (best >= 0) {
+      *out = g_big_free[best].p;
+      g_big_live.push_back(g_big_free[best]);
+      g_big_free.erase(g_big_free.begin() + best);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMallocAsync(out, bytes, s);
+  if (e == cudaSuccess && bytes >= kBigMin) {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    g_big_live.push_back({*out, bytes, dev});
+  }
+  return e;
+}
+
+void big_free(void* p, cudaStream_t s) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    for (size_t i = 0; i < g_big_live.size(); ++i) {
+      if (g_big_live[i].p != p) continue;
+      const BigBlock b = g_big_live[i];
+      g_big_live.erase(g_big_live.begin() + i);
+      size_t cached = 0;
+      for (const BigBlock& f : g_big_free) cached += f.bytes;
+      if (cached + b.bytes <= kBigCacheCap) {
+        g_big_free.push_back(b);
+        return;
+      }
+      break;
+    }
+  }
+  cudaFreeAsync(p, s);
+}
+
+// DK_TRACE=1: host-side phase timestamps of the set-up path on stderr (diagnostics)
+struct Trace {
+  bool on = getenv("DK_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[dk] %8.3f ms %s\n", ms, what);
+  }
+};
+
 // pinned State mirrors are recycled across operators: cudaFreeHost / cudaMallocHost are slow
 // and synchronising, and an operator is created per matrix
 std::mutex g_pinned_mu;
@@ -257,11 +333,11 @@ int ensure_part(dk_op* op, int q) {
 
 int ensure_work(dk_op* op, int m, int max_iters) {
   if (op->v_rows < m + 1) {
-    if (op->V_base) DK_TRY(cudaFreeAsync(op->V_base, op->stream));
+    if (op->V_base) big_free(op->V_base, op->stream);
     op->V_base = nullptr;
     op->vstride = op->n_pad + op->guard;
     const size_t total = (size_t)op->guard + (size_t)(m + 1) * op->vstride;
-    DK_TRY(cudaMallocAsync(&op->V_base, total * sizeof(double), op->stream));
+    DK_TRY(big_alloc((void**)&op->V_base, total * sizeof(double), op->stream));
     DK_TRY(cudaMemsetAsync(op->V_base, 0, total * sizeof(double), op->stream));
     op->v_rows = m + 1;
     op->g_m = -1;  // graph refers to the old basis
@@ -578,7 +654,19 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
     if (order[k].first == order[k - 1].first) return fail(DK_EINVAL, "duplicate diagonal offset");
   dk_op* op = new dk_op();
   DK_TRY(cudaGetDevice(&op->dev));
-  DK_TRY(cudaStreamCreateWithFlags(&op->own, cudaStreamNonBlocking));
+  {
+    // one library stream per device, shared by every operator: the stream-ordered pool then
+    // reuses freed GB-sized blocks (V, E, E^-1) across operators and contexts without
+    // cross-stream dependencies (per-operator streams occasionally made the pool map new
+    // memory, ~1 s for the E buffers)
+    static std::mutex mu;
+    static cudaStream_t dev_stream[64] = {nullptr};
+    std::lock_guard<std::mutex> lk(mu);
+    if (op->dev < 0 || op->dev >= 64) return fail(DK_EINVAL, "device ordinal out of range");
+    if (!dev_stream[op->dev])
+      DK_TRY(cudaStreamCreateWithFlags(&dev_stream[op->dev], cudaStreamNonBlocking));
+    op->own = dev_stream[op->dev];
+  }
   {
     // keep up to 16 GB of freed pool memory for the next context (E, E^-1, V are GB-sized)
     cudaMemPool_t pool;
@@ -724,14 +812,15 @@ int dk_op_destroy(dk_op* op) {
   if (op->gexec) cudaGraphExecDestroy(op->gexec);
   for (auto e : op->ev_pool) cudaEventDestroy(e);
   // all device buffers of an operator come from the stream-ordered pool
-  void* bufs[] = {op->V_base, op->dia,     op->inv_base, op->w_base, op->x_base, op->b_base,
+  big_free(op->V_base, op->stream);
+  void* bufs[] = {op->dia,     op->inv_base, op->w_base, op->x_base, op->b_base,
                   op->x0_base, op->t_base, op->part,     op->nrm,    op->tickets, op->one,
                   op->st,     op->scal,    op->hist,     op->rof,    op->gticket, op->gpart};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, op->stream);
   cudaStreamSynchronize(op->stream);
   if (op->st_host) pinned_state_release(op->st_host);
-  if (op->own) cudaStreamDestroy(op->own);
+  // op->own is the shared library stream of the device: not destroyed
   delete op;
   return DK_OK;
 }
@@ -820,6 +909,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     // A M^-1 with the identity preconditioner is A itself
     ap_choice = DK_AP_A;
   }
+  Trace tr;
   const long long n = op->n, n_pad = op->n_pad;
   // host copy of the labels (input may live on the device)
   std::vector<int> lab(n_pad, -1);
@@ -859,6 +949,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     for (long long r = 0; r < nruns; ++r)
       slot[r] = run_label[r] >= 0 ? fillp[run_label[r]]++ : spare++;
   }
+  tr.mark("labels + run map (host)");
   dk_defl* c = new dk_defl();
   c->op = op;
   c->serial = ++g_ctx_serial;
@@ -891,9 +982,11 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(cudaMallocAsync(&c->run_slot, slot.size() * sizeof(int), s));
   DKD(cudaMemcpyAsync(c->run_slot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
+  tr.mark("run map uploaded");
   // the O(d^2) buffers come from the stream-ordered pool (cached across contexts)
-  DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
-  DKD(cudaMallocAsync(&c->Einv, (size_t)d * c->ld * sizeof(double), s));
+  DKD(big_alloc((void**)&c->E, (size_t)d * c->ld * sizeof(double), s));
+  DKD(big_alloc((void**)&c->Einv, (size_t)d * c->ld * sizeof(double), s));
+  tr.mark("E, E^-1 allocated");
   DKD(cudaMallocAsync(&c->piv, (size_t)d * sizeof(int), s));
   DKD(cudaMallocAsync(&c->s, (size_t)c->ld * sizeof(double), s));
   DKD(cudaMallocAsync(&c->y, (size_t)c->ld * sizeof(double), s));
@@ -948,6 +1041,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
   const bool am = ap_choice == DK_AP_AM;
+  tr.mark("buffers + prolongation map");
   int err = build_coarse(make_dia(op, am), am, c->lab, n_pad, c->rm, c->E, c->ld,
                          c->qv_base + op->guard, s);
   cudaEventRecord(e1, s);
@@ -957,15 +1051,17 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   // keep a copy of E for inspection (the factorisations run in place on the copy)
   const size_t ebytes = (size_t)d * c->ld * sizeof(double);
   double* Ework = nullptr;
-  DKD(cudaMallocAsync(&Ework, ebytes, s));
+  DKD(big_alloc((void**)&Ework, ebytes, s));
   DKD(cudaMemcpyAsync(Ework, c->E, ebytes, cudaMemcpyDeviceToDevice, s));
   const bool symmetric = !am && coarse_is_symmetric(c->E, d, c->ld, s);
   bool inverted = false;
   if (symmetric) {  // SPD E: Cholesky-based inverse (half the work of LU + solves)
     double min_sq = 0.0;
+    tr.mark("E assembled");
     err = spd_inverse(Ework, d, c->ld, c->Einv, &min_sq, &c->ms[1], &c->ms[2], s);
+    tr.mark("E^-1 (Cholesky path)");
     if (err) {
-      cudaFreeAsync(Ework, s);
+      big_free(Ework, s);
       return cleanup_fail((cudaError_t)err, "spd_inverse");
     }
     if (min_sq >= 1e-280) {  // E^-1 is in Ework: it becomes Einv, the W scratch is released
@@ -979,21 +1075,21 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     double min_piv = 0.0;
     err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
     if (err) {
-      cudaFreeAsync(Ework, s);
+      big_free(Ework, s);
       return cleanup_fail((cudaError_t)err, "lu_and_inverse");
     }
     if (!(min_piv >= 1e-300)) {  // sparse.py:135-136 (NaN pivots are singular too)
-      cudaFreeAsync(Ework, s);
+      big_free(Ework, s);
       dk_defl_destroy(c);
       return fail(DK_ESINGULAR, "zero pivot in LU factorization");
     }
   }
-  cudaFreeAsync(Ework, s);
+  big_free(Ework, s);
   // symmetric E (symmetric A, A_p = A): stream only the upper tile triangle of E^-1
   if (d >= kSymvMinD && d <= kSymvMaxD && symmetric) {
     c->sym = 1;
     c->ntiles = symv_tiles(d);
-    DKD(cudaMallocAsync(&c->P, (size_t)c->ntiles * 1024 * sizeof(double), s));
+    DKD(big_alloc((void**)&c->P, (size_t)c->ntiles * 1024 * sizeof(double), s));
     DKD(cudaMallocAsync(&c->rowpart, (size_t)c->ntiles * 32 * sizeof(double), s));
     DKD(cudaMallocAsync(&c->colpart, (size_t)c->ntiles * 32 * sizeof(double), s));
     launch_symv_pack(c->Einv, d, c->ld, c->P, s);
@@ -1007,6 +1103,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
                         s));
     DKD(cudaStreamSynchronize(s));
   }
+  tr.mark("packed E^-1");
   // x* = Z E^-1 Z^T b  (deflation.py:88)
   cudaEventRecord(e0, s);
   if (b) {
@@ -1073,8 +1170,8 @@ static int defl_create_dense(dk_defl** out, dk_op* op, int32_t d, int32_t ap_cho
   DKD(cudaMemsetAsync(c->AZ_base, 0, rows_bytes, s));
   c->Z = c->Z_base + op->guard;
   c->AZ = c->AZ_base + op->guard;
-  DKD(cudaMallocAsync(&c->E, (size_t)d * c->ld * sizeof(double), s));
-  DKD(cudaMallocAsync(&c->Einv, (size_t)d * c->ld * sizeof(double), s));
+  DKD(big_alloc((void**)&c->E, (size_t)d * c->ld * sizeof(double), s));
+  DKD(big_alloc((void**)&c->Einv, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMemsetAsync(c->E, 0, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMallocAsync(&c->piv, (size_t)d * sizeof(int), s));
   DKD(cudaMallocAsync(&c->s, (size_t)c->ld * sizeof(double), s));
@@ -1112,12 +1209,12 @@ static int defl_create_dense(dk_defl** out, dk_op* op, int32_t d, int32_t ap_cho
   DKD(cudaEventSynchronize(e1));
   cudaEventElapsedTime(&c->ms[0], e0, e1);
   double* Ework = nullptr;
-  DKD(cudaMallocAsync(&Ework, (size_t)d * c->ld * sizeof(double), s));
+  DKD(big_alloc((void**)&Ework, (size_t)d * c->ld * sizeof(double), s));
   DKD(cudaMemcpyAsync(Ework, c->E, (size_t)d * c->ld * sizeof(double), cudaMemcpyDeviceToDevice,
                       s));
   double min_piv = 0.0;
   int err = lu_and_inverse(Ework, d, c->ld, c->Einv, c->piv, &min_piv, &c->ms[1], &c->ms[2], s);
-  cudaFreeAsync(Ework, s);
+  big_free(Ework, s);
   if (err) return cleanup_fail((cudaError_t)err, "lu_and_inverse");
   if (!(min_piv >= 1e-300)) {  // sparse.py:135-136
     dk_defl_destroy(c);
@@ -1182,7 +1279,10 @@ int dk_defl_destroy(dk_defl* c) {
   if (c->op) cudaStreamSynchronize(s);
   // every buffer of a context comes from the stream-ordered pool: no device-wide
   // synchronisation or OS-level free on destruction
-  void* bufs[] = {c->E,        c->Einv,         c->P,        c->Z_base,      c->AZ_base,
+  big_free(c->E, s);
+  big_free(c->Einv, s);
+  big_free(c->P, s);
+  void* bufs[] = {c->Z_base,   c->AZ_base,
                   c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
                   c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
                   c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->seg_ptr,

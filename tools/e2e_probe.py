@@ -11,7 +11,7 @@ A, b = c.problem()
 off, dg = A.dia()
 basis = dk.partition_to_basis(c.partition())
 M = dk.Preconditioner.jacobi(A)
-for it in range(4):
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     t0 = time.perf_counter()
     Ah = dk.SparseMatrix.from_dia(A.n, off, dg)
     op = Ah.device(); t1 = time.perf_counter()
