@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "dk_launch.h"
@@ -249,6 +250,18 @@ constexpr int DNW = 8;    // warps of the diagonal-block kernel
 constexpr int GB = 256;   // blocks are grouped for the trailing updates (rank GB)
 constexpr int kDiagSmem = (DB * (DB + 1) + 5 * DB + 2) * (int)sizeof(double);
 
+// 1/v from the hardware approximation refined by two Newton steps (error ~1 ulp); on the
+// critical path of every elimination step, where a correctly rounded division costs several
+// times more
+__device__ __forceinline__ double fast_rcp(double v) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  double e = fma(-v, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-v, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <int N>
 __device__ __forceinline__ double sel(const double (&v)[N], int k) {
   double r = v[0];
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(32 * DNW, 1) k_chol_diag(const double* __restr
   if (lane == 0)
 #pragma unroll
     for (int i = 0; i < RPW; ++i) buf[rb + i] = a[i][0];
-  if (tid == 0) ipb[0] = 1.0 / a[0][0];
+  if (tid == 0) ipb[0] = fast_rcp(a[0][0]);
   __syncthreads();
   for (int c = 0; c < nb; ++c) {
     const int n1 = c + 1;
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(32 * DNW, 1) k_chol_diag(const double* __restr
         for (int i = 0; i < RPW; ++i) {
           const double v = sel(a[i], q);
           nxt[rb + i] = v;
-          if (rb + i == n1) ipb[n1 & 1] = 1.0 / v;
+          if (rb + i == n1) ipb[n1 & 1] = fast_rcp(v);
         }
       }
     }
@@ -445,6 +458,21 @@ void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int l
   }
 }
 
+// high-priority stream of the device for the factorisation's look-ahead chain
+static cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t st[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!st[dev & 63]) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&st[dev & 63], cudaStreamNonBlocking, greatest);
+  }
+  return st[dev & 63];
+}
+
 int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
                 float* ms_inv, cudaStream_t s) {
   static bool attr = false;
@@ -481,37 +509,68 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
       reach[t] = std::max(t, mx + 1);
     }
   }
-  // 1. E = L L^T, right-looking by DB-wide blocks in groups of GB columns: the diagonal block
-  //    is factorised and inverted by one CTA (L11^-1 lands on W's diagonal), the block column
-  //    below becomes L21 = A21 L11^-T (in place: one tile column, each CTA owns its rows);
-  //    inside a group only the group's remaining columns are updated (rank DB), and the
-  //    trailing lower triangle receives the group's rank-GB update when the group completes
-  //    (few passes over the trailing matrix).
-  for (int q = 0; q < nblk; ++q) {
-    const int K0 = q * DB, nb = (d - K0 < DB) ? d - K0 : DB, Kend = K0 + nb, rest = d - Kend;
-    const int G0 = (K0 / GB) * GB, gend = (d - G0 < GB) ? d : G0 + GB;
-    k_chol_diag<<<1, 32 * DNW, kDiagSmem, s>>>(L, ld, K0, nb, W, dpmin, q);
-    if (rest <= 0) break;
-    const int rq = reach[Kend] - Kend;  // rows below the block inside the profile
-    if (rq > 0)
-      gemm_mma(false, true, at(L, Kend, K0), ld, at(W, K0, K0), ld, at(L, Kend, K0), ld, rq, nb,
-               nb, 1.0, 0.0, 0, INT_MIN, s);
-    if (Kend < gend) {
-      if (rq > 0)
-        gemm_mma(false, true, at(L, Kend, K0), ld, at(L, Kend, K0), ld, at(L, Kend, Kend), ld, rq,
-                 gend - Kend, nb, -1.0, 1.0, 0, INT_MIN, s);
-    } else {
-      const int rg = reach[Kend] - Kend;
-      if (rg > 0)
-        gemm_mma(false, true, at(L, Kend, G0), ld, at(L, Kend, G0), ld, at(L, Kend, Kend), ld, rg,
-                 rg, Kend - G0, -1.0, 1.0, 1, INT_MIN, s);
-    }
+  // 1. E = L L^T, right-looking by DB-wide blocks in groups of GB columns, with look-ahead.
+  //    The panel chain of a group runs on a high-priority side stream: per block, the
+  //    diagonal block is factorised and inverted by one CTA (L11^-1 lands on W's diagonal),
+  //    the block column below becomes L21 = A21 L11^-T (in place: one tile column, each CTA
+  //    owns its rows), and the group's remaining columns receive the block's rank-DB update.
+  //    When a group completes, the side stream applies its rank-GB update to the NEXT group's
+  //    columns only (a), so that group's chain can start at once, while the main stream
+  //    updates the rest of the trailing lower triangle (b).  Every product is limited to the
+  //    rows inside the profile (reach).
+  cudaStream_t side = side_stream();
+  const int ngroups = (d + GB - 1) / GB;
+  std::vector<cudaEvent_t> ev_chain(ngroups), ev_b(ngroups);
+  for (int g = 0; g < ngroups; ++g) {
+    cudaEventCreateWithFlags(&ev_chain[g], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_b[g], cudaEventDisableTiming);
   }
+  cudaEvent_t ev_start, ev_side_done;
+  cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_side_done, cudaEventDisableTiming);
+  cudaEventRecord(ev_start, s);
+  cudaStreamWaitEvent(side, ev_start, 0);
+  for (int g = 0; g < ngroups; ++g) {
+    const int G0 = g * GB, gend = (d - G0 < GB) ? d : G0 + GB;
+    for (int K0 = G0; K0 < gend; K0 += DB) {  // chain(g), side stream
+      const int nb = (d - K0 < DB) ? d - K0 : DB, Kend = K0 + nb;
+      k_chol_diag<<<1, 32 * DNW, kDiagSmem, side>>>(L, ld, K0, nb, W, dpmin, K0 / DB);
+      const int rq = reach[Kend] - Kend;  // rows below the block inside the profile
+      if (Kend >= d || rq <= 0) continue;
+      gemm_mma(false, true, at(L, Kend, K0), ld, at(W, K0, K0), ld, at(L, Kend, K0), ld, rq, nb,
+               nb, 1.0, 0.0, 0, INT_MIN, side);
+      if (Kend < gend)
+        gemm_mma(false, true, at(L, Kend, K0), ld, at(L, Kend, K0), ld, at(L, Kend, Kend), ld, rq,
+                 gend - Kend, nb, -1.0, 1.0, 0, INT_MIN, side);
+    }
+    cudaEventRecord(ev_chain[g], side);
+    if (gend >= d) break;
+    const int R = reach[gend], na = (d - gend < GB) ? d - gend : GB, rb0 = gend + na;
+    // (a) the next group's columns, after the previous trailing update (b) wrote them
+    if (g > 0) cudaStreamWaitEvent(side, ev_b[g - 1], 0);
+    if (R > gend)
+      gemm_mma(false, true, at(L, gend, G0), ld, at(L, gend, G0), ld, at(L, gend, gend), ld,
+               R - gend, std::min(na, R - gend), gend - G0, -1.0, 1.0, 0, INT_MIN, side);
+    // (b) the rest of the trailing lower triangle, main stream, once the group's panel is final
+    cudaStreamWaitEvent(s, ev_chain[g], 0);
+    if (R > rb0)
+      gemm_mma(false, true, at(L, rb0, G0), ld, at(L, rb0, G0), ld, at(L, rb0, rb0), ld, R - rb0,
+               R - rb0, gend - G0, -1.0, 1.0, 1, INT_MIN, s);
+    cudaEventRecord(ev_b[g], s);
+  }
+  cudaEventRecord(ev_side_done, side);
+  cudaStreamWaitEvent(s, ev_side_done, 0);
   std::vector<double> pm(nblk);
   cudaMemcpyAsync(pm.data(), dpmin, nblk * sizeof(double), cudaMemcpyDeviceToHost, s);
   cudaEventRecord(e1, s);
   cudaStreamSynchronize(s);
   cudaFreeAsync(dpmin, s);
+  for (int g = 0; g < ngroups; ++g) {
+    cudaEventDestroy(ev_chain[g]);
+    cudaEventDestroy(ev_b[g]);
+  }
+  cudaEventDestroy(ev_start);
+  cudaEventDestroy(ev_side_done);
   double mn = INFINITY;
   for (double v : pm) mn = (v != v || mn != mn) ? NAN : fmin(mn, v);
   *min_diag_sq = mn;
