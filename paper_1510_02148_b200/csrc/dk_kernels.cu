@@ -2,12 +2,13 @@
 //
 // Per inner iteration j (deflated), DESIGN.md §4:
 //   K1 k_stencil        w = A M^-1 v_j (DIA, Jacobi fused) + per-run sums of w  (Z^T w, part 1)
-//   K2 k_restrict_final s = Z^T w, one warp per column, fixed order              (part 2)
-//   K3 k_gemv           y = E^-1 s                                  (dk_coarse.cu)
-//   K4 k_project        w -= A Z y (<= 7-label gather), h = V^T w, ||w||  -> Hessenberg column
-//   K5 k_gs             u = w - V h, ||u||, corr = V^T u  -> selective re-orthogonalisation test,
-//                       Givens update, convergence test (last block)
-//   K6 k_gs<reorth>     u -= V corr, ||u||  (only when the test fired)
+//   K2 k_restrict_final s = Z^T w from the run partials, fixed order             (part 2)
+//   K3 k_symv / k_gemv  y = E^-1 s (packed symmetric / dense)           (dk_coarse.cu)
+//   K4 k_project        w -= A Z y (compact prolongation), h = V^T w, ||w||; last block: H
+//                       column, re-orthogonalisation test corr = h - G h
+//   K5 k_gs             u = w - V h, ||u||; last block: Givens update, convergence test
+//   K6 k_project<REDOTS> + k_gs<reorth>: corr = V^T u, u -= V corr (only when the test fired)
+//   dense bases (RDGMRES): k_zdots (s = Z^T w, y = E^-1 s) and k_project<DK_DENSE>
 // Reference semantics: _run_cycles, krylov.py:107-236.
 #include <cuda_runtime.h>
 
@@ -292,7 +293,8 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
 }
 
 // ======================================================================================
-// K2: per-column sum of run partials (one warp per deflation column, fixed order).
+// K2: per-column sum of run partials (label-major slots: one thread per column, a warp per
+// column with more than kShortRuns runs; fixed order).
 // ======================================================================================
 __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __restrict__ run_part,
                                                              const int* __restrict__ ptr, int d,
@@ -451,14 +453,14 @@ __device__ void finish_iteration_block(const Scal& sc, int j, double hj1, double
 }
 
 // ======================================================================================
-// K4: prolongation + subtraction, multi-dot, Gram column and norm.
+// K4: prolongation + subtraction, multi-dot and norm.
 //
-// h_i = V_i . w (classical Gram-Schmidt coefficients) and G_ij = V_i . V_j (the new column
-// of the basis Gram matrix) are formed in the same sweep — V_i is loaded once and used for
-// both.  With G the reference's re-orthogonalisation test (krylov.py:167-168: max |V^T w'|
+// h_i = V_i . w (classical Gram-Schmidt coefficients) in one sweep over V.  With the basis
+// Gram matrix G the reference's re-orthogonalisation test (krylov.py:167-168: max |V^T w'|
 // > 1e-8 ||w0|| after the projection) is evaluated without another pass over V:
-//     V^T (w - V h) = h - G h.
-// The test is evaluated up to O(eps ||w||), eight orders below its threshold.
+//     V^T (w - V h) = h - G h,
+// and the same identity gives G's next column (iter_finish): the test and G are exact up to
+// O(eps ||w||), several orders below the threshold.
 // ======================================================================================
 // Prolongation (A_p Z y)_i = sum over the row's coefficients of y[label of the column].
 // Precomputed per cell (k_prolong_setup): own = sum of the coefficients whose column carries

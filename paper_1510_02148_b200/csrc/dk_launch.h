@@ -54,7 +54,7 @@ void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad
                           unsigned char* mask, unsigned long long* nmasked, cudaStream_t s);
 
 enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
-// w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w and Gram column V^T V_j, ||w_out||^2
+// w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w, ||w_out||^2
 // -> H col j + re-orthogonalisation test; RESTART: ||w_out||^2 -> restart test;
 // REDOTS: corr = V^T u for the second Gram-Schmidt pass.  G = grid width (fixed per op).
 void launch_project(int mode, int defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
