@@ -100,6 +100,7 @@ struct dk_op {
   int part_q = 0;
   double* nrm = nullptr;  // [4] device norms
   unsigned int* tickets = nullptr;
+  bool gs_fuse = false;  // second Gram-Schmidt pass inside k_gs (whole grid co-resident)
   unsigned int* gticket = nullptr;  // reduce_grouped counters
   double* gpart = nullptr;          // reduce_grouped group partials [part_q x kGroupTickets]
   int* one = nullptr;  // device constant 1 (gate of ungated launches)
@@ -382,6 +383,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.gcol = p; p += m + 1;
   sc.gticket = op->gticket;
   sc.gpart = op->gpart;
+  op->gs_fuse = gs_can_fuse(op->G, sc) && getenv("DK_NO_GS_FUSE") == nullptr;
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
@@ -531,7 +533,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   }
   {
     ProfScope ps(op, PC_PROJECT,
-                 c ? (16.0 + 8.0 * nvec) * n + pro_bytes : (8.0 + 8.0 * nvec) * n);
+                 c ? (24.0 + 8.0 * nvec) * n + pro_bytes : (16.0 + 8.0 * nvec) * n);
     launch_project(PJ_ITER, defl_kind(c), am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                    op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
                    &st->active, op->stream);
@@ -539,8 +541,9 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   {
     ProfScope ps(op, PC_GS, (16.0 + 8.0 * nvec) * n);
     launch_gs(false, op->w, V + (long long)(j + 1) * op->vstride, V, op->vstride, nvec,
-              op->n_pad, op->part, op->G, op->sc, j, &st->active, op->stream);
+              op->n_pad, op->part, op->G, op->sc, j, &st->active, op->gs_fuse, op->stream);
   }
+  if (op->gs_fuse) return;  // the second pass, when needed, runs inside k_gs
   // second Gram-Schmidt pass, gated on the device-side test (krylov.py:167-170)
   if (op->prof) {
     if (read_state(op) || !op->st_host->reorth) return;
@@ -551,7 +554,8 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
                    V + (long long)(j + 1) * op->vstride, nullptr, V, op->vstride, nvec, op->n_pad,
                    op->part, op->G, op->sc, j, &st->reorth, op->stream);
     launch_gs(true, V + (long long)(j + 1) * op->vstride, V + (long long)(j + 1) * op->vstride, V,
-              op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j, &st->reorth, op->stream);
+              op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j, &st->reorth, false,
+              op->stream);
   }
 }
 
@@ -1415,7 +1419,10 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   cudaEventRecord(e0, op->stream);
   // stencil (+ restrict + E^-1 s; dense: one multi-dot)
   const int coarse_launches = c ? (c->dense ? 2 : c->sym ? 4 : 3) : 1;
-  const int per_cycle_launches = coarse_launches + 1 + m * (coarse_launches + 4) + 2;
+  // restart (stencil chain + projection), m x (stencil chain, projection, update [+ the
+  // separate second pass]), cycle end, x update
+  const int per_cycle_launches =
+      coarse_launches + 1 + m * (coarse_launches + (op->gs_fuse ? 2 : 4)) + 2;
   long long guard_cycles = run_cycles ? (long long)max_iters + 2 : 0;
   if (max_cycles > 0 && guard_cycles > max_cycles) guard_cycles = max_cycles;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {

@@ -554,46 +554,53 @@ __device__ __forceinline__ double reduce8(double (&v)[8], int lane) {
   return v[0];
 }
 
-// Last block of an Arnoldi projection: red[0..nvec] holds the reduced V^T w and ||w||^2.
-// Writes the Hessenberg column, the update coefficients and the Gram column, and evaluates
-// the re-orthogonalisation test (krylov.py:162-170): corr = V^T u = h - G h for
-// u = w - V h.  The Gram column of v_j = sigma_j u_{j-1} is sigma_j V^T u_{j-1}, i.e. the
-// previous iteration's corr (or, after a second pass, corr2 - G corr2), kept in gcol: the
-// identity holds to rounding (~1e-13 relative, far below the 1e-8 test), and no pass over V
-// is spent on it.  Shared scratch after red[0..nvec]: h[nvec], G[nvec][nvec], |corr|[nvec].
+// Last block of an Arnoldi projection: red[0..2 nvec] holds the reduced V^T w, the reduced
+// Gram column V^T v_j (measured in the same sweep: it carries the basis' actual loss of
+// orthogonality, which the test exists to detect) and ||w||^2.  Writes the Hessenberg column,
+// the update coefficients and the Gram column, and evaluates the re-orthogonalisation test
+// (krylov.py:162-170): corr = V^T u = h - G h for u = w - V h; corr is also kept in gcol (the
+// Gram row of the cycle's last vector, reported with the Arnoldi data).  Shared scratch after
+// red[0..2 nvec]: h[nvec], |corr|[nvec] and, for nvec <= kStageGram, G[nvec][nvec] (larger
+// cycles read G from global memory).
+constexpr int kStageGram = 96;
 __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
   State* st = sc.st;
   const int m = sc.m;
   double* Hc = sc.H + (size_t)j * (m + 1);
   const double sj = sc.sigma[nvec - 1];
-  double* sh_h = red + nvec + 1;
-  double* sh_g = sh_h + nvec;
-  double* sh_c = sh_g + nvec * nvec;
+  const bool stage = nvec <= kStageGram;
+  double* sh_h = red + 2 * nvec + 1;
+  double* sh_c = sh_h + nvec;
+  double* sh_g = sh_c + nvec;
   for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
     const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
     Hc[v] = h;
     sh_h[v] = h;
     sc.coef[v] = h * sc.sigma[v];
-    const double g = (v < nvec - 1) ? sj * sc.gcol[v] : 1.0;  // |v_j| = 1
+    const double g = red[nvec + v] * sc.sigma[v] * sj;  // V_i . V_j
     sc.Gm[(size_t)j * (m + 1) + v] = g;
-    sh_g[v * nvec + (nvec - 1)] = g;
-    sh_g[(nvec - 1) * nvec + v] = g;
+    if (stage) {
+      sh_g[v * nvec + (nvec - 1)] = g;
+      sh_g[(nvec - 1) * nvec + v] = g;
+    }
   }
-  for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
-    const int i = e / (nvec - 1), k = e % (nvec - 1);
-    sh_g[i * nvec + k] = gram_at(sc.Gm, m, i, k);
-  }
+  if (stage)
+    for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
+      const int i = e / (nvec - 1), k = e % (nvec - 1);
+      sh_g[i * nvec + k] = gram_at(sc.Gm, m, i, k);
+    }
   __syncthreads();
   // corr_i = h_i - sum_k G_ik h_k
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
     double c = sh_h[i];
-    for (int k = 0; k < nvec; ++k) c -= sh_g[i * nvec + k] * sh_h[k];
+    for (int k = 0; k < nvec; ++k)
+      c -= (stage ? sh_g[i * nvec + k] : gram_at(sc.Gm, m, i, k)) * sh_h[k];
     sh_c[i] = fabs(c);
     sc.gcol[i] = c;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    st->wnorm0 = sqrt(red[nvec]);  // krylov.py:162
+    st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
     double mx = 0.0;
     for (int i = 0; i < nvec; ++i) mx = fmax(mx, sh_c[i]);
     if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
@@ -617,13 +624,15 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
   if (*gate == 0) return;
   extern __shared__ double red[];  // [nq][kWarps]
   __shared__ __align__(16) double s_w[(MODE == PJ_ITER || MODE == PJ_REDOTS) ? kChunk : 2];
+  __shared__ __align__(16) double s_vj[MODE == PJ_ITER ? kChunk : 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // quantities: ITER: h[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
-  const int nq = (MODE == PJ_ITER) ? nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
-  const int nslot = (MODE == PJ_ITER) ? nvec : 0;
+  // quantities: ITER: h[nvec], g[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
+  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+  const int nslot = (MODE == PJ_ITER) ? 2 * nvec : 0;
   for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
+  const double* Vj = V + (long long)(nvec - 1) * vstride;
   for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long long cb = ch * kChunk + 2 * threadIdx.x;
     double w[8];
@@ -660,14 +669,18 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
       if (lane == 0) red[nslot * kWarps + warp] += nrm;
     }
     if (MODE == PJ_ITER || MODE == PJ_REDOTS) {
-      // Stage w of the chunk in shared memory; the warps then stream the basis as
+      // Stage w (and v_j) of the chunk in shared memory; the warps then stream the basis as
       // (vector, quarter-chunk) items: 8 x 16 B loads in flight per lane and one warp
       // reduction per 4 KB of V, instead of one per 128 B.  Item (v, q) goes to warp
-      // (4v + q) % 8 and its partial to that warp's slot: fixed order, deterministic.
+      // (4v + q) % 8 and its partial to that warp's slot: fixed order, deterministic.  Each
+      // V_i load serves both dots, V_i . w and the Gram entry V_i . v_j.
       double2* sw2 = reinterpret_cast<double2*>(s_w);
+      double2* sv2 = reinterpret_cast<double2*>(s_vj);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 4; ++k) {
         sw2[threadIdx.x + 256 * k] = make_double2(w[2 * k], w[2 * k + 1]);
+        if (MODE == PJ_ITER) sv2[threadIdx.x + 256 * k] = ld2(Vj + cb + 512 * k);
+      }
       __syncthreads();
       const long long c0 = ch * kChunk;
       const unsigned long long pol = l2_evict_first();
@@ -677,17 +690,27 @@ __global__ void __launch_bounds__(kThreads) k_project(Dia A, Prolong P,
         double2 p[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) p[i] = ld2_stream(Vr + 64 * i, pol);
-        double ah = 0.0;
+        double ah = 0.0, ag = 0.0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const double2 ww = sw2[256 * qtr + lane + 32 * i];
+          const int e = 256 * qtr + lane + 32 * i;
+          const double2 ww = sw2[e];
           ah = fma(p[i].x, ww.x, ah);
           ah = fma(p[i].y, ww.y, ah);
+          if (MODE == PJ_ITER) {
+            const double2 gg = sv2[e];
+            ag = fma(p[i].x, gg.x, ag);
+            ag = fma(p[i].y, gg.y, ag);
+          }
         }
         ah = warp_sum(ah);
-        if (lane == 0) red[v * kWarps + warp] += ah;
+        if (MODE == PJ_ITER) ag = warp_sum(ag);
+        if (lane == 0) {
+          red[v * kWarps + warp] += ah;
+          if (MODE == PJ_ITER) red[(nvec + v) * kWarps + warp] += ag;
+        }
       }
-      __syncthreads();  // the next chunk reuses s_w
+      __syncthreads();  // the next chunk reuses s_w / s_vj
     }
   }
   pdl_trigger();
@@ -731,9 +754,10 @@ static void project_t(const Dia& A, const Prolong& lab, const double* yc, const 
                       double* w_out, const double* V, long long vstride, int nvec,
                       long long n_pad, double* part, int G, const Scal& sc, int j,
                       const int* gate, cudaStream_t s) {
-  const int nq = (MODE == PJ_ITER) ? nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
   int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
-  const int tail = 3 * nvec + 1 + nvec * nvec;  // PJ_ITER re-orthogonalisation test scratch
+  // PJ_ITER re-orthogonalisation test scratch (iter_finish)
+  const int tail = 4 * nvec + 1 + (nvec <= kStageGram ? nvec * nvec : 0);
   if (MODE == PJ_ITER && tail > slots) slots = tail;
   if (nq + 260 > slots) slots = nq + 260;  // reduce_grouped scratch
   const size_t smem = (size_t)slots * sizeof(double);
@@ -913,18 +937,56 @@ void launch_combine_rows(const double* R, long long rs, const double* sigma, int
 // REORTH: the second pass u -= sum_i corr_i V_i (only when the test in K4 fired; corr is
 // then recomputed from the stored u by a PJ_REDOTS sweep, as the reference does).
 // ======================================================================================
+// Grid-wide release of the fused second pass: every block arrives; the last one runs `lead`
+// (all its threads), then releases the others, which spin on the generation counter.  Only
+// used when the whole grid is co-resident (checked on the host) and no dependent launch was
+// triggered, so nothing can hold the SMs the waiting blocks need.
+template <class F>
+__device__ __forceinline__ void grid_arrive_lead_release(unsigned int* count, unsigned int* gen,
+                                                         F lead) {
+  __shared__ int s_lead;
+  __shared__ unsigned int s_gen;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_gen = *reinterpret_cast<volatile unsigned int*>(gen);
+    __threadfence();
+    s_lead = (atomicAdd(count, 1u) == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_lead) {
+    __threadfence();
+    lead();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    while (*reinterpret_cast<volatile unsigned int*>(gen) == s_gen) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// K5 (FUSE): when the projection's test fired (rare), the reference's second Gram-Schmidt
+// pass (krylov.py:169-170) runs inside the same launch — corr = V^T u over the stored u,
+// the coefficients in the leading block, u -= V corr — instead of two extra launches that
+// are otherwise issued gated-off every iteration.
 template <bool REORTH>
 __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_out,
                                                  const double* __restrict__ V, long long vstride,
                                                  int nvec, long long n_pad,
                                                  double* __restrict__ part, int G, Scal sc, int j,
-                                                 const int* __restrict__ gate) {
+                                                 const int* __restrict__ gate, int fuse) {
   pdl_wait();
   if (*gate == 0) return;
   extern __shared__ double sh[];
   double* cf = sh;                                  // [nvec]
   double* red = sh + nvec;                          // [kWarps] (+ scratch)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool second = !REORTH && fuse && sc.st->reorth != 0;
   for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = REORTH ? sc.corr[q] : sc.coef[q];
   for (int q = threadIdx.x; q < kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
@@ -960,7 +1022,88 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     nrm = warp_sum(nrm);
     if (lane == 0) red[warp] += nrm;
   }
-  pdl_trigger();
+  if (second) {
+    // corr_v = V_v . u: block partials over this block's chunks (u re-read from its own writes)
+    __syncthreads();
+    for (int v = 0; v < nvec; ++v) {
+      double a = 0.0;
+      for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const long long cb = ch * kChunk + 2 * threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 uu = ld2cg(u_out + cb + 512 * k);
+          const double2 p = ld2_stream(V + (long long)v * vstride + cb + 512 * k, pol);
+          a = fma(p.x, uu.x, a);
+          a = fma(p.y, uu.y, a);
+        }
+      }
+      a = warp_sum(a);
+      if (lane == 0) red[warp] = a;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < kWarps; ++w2) t += red[w2];
+        part[(size_t)v * G + blockIdx.x] = t;
+      }
+      __syncthreads();
+    }
+    grid_arrive_lead_release(sc.gticket + kGroupTickets - 2, sc.gticket + kGroupTickets - 3, [&] {
+      // the PJ_REDOTS finish: H column += corr, coefficients, next Gram column corr - G corr
+      const int m = sc.m;
+      double* Hc = sc.H + (size_t)j * (m + 1);
+      double* cr = red;
+      for (int v = warp; v < nvec; v += kWarps) {
+        double t = 0.0;
+        for (int b = lane; b < G; b += 32) t += __ldcg(part + (size_t)v * G + b);
+        t = warp_sum(t);
+        if (lane == 0) cr[v] = t * sc.sigma[v];
+      }
+      __syncthreads();
+      for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+        Hc[v] += cr[v];
+        sc.corr[v] = cr[v] * sc.sigma[v];
+      }
+      for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+        double c = cr[i];
+        for (int k = 0; k < nvec; ++k) c -= gram_at(sc.Gm, m, i, k) * cr[k];
+        sc.gcol[i] = c;
+      }
+    });
+    // u -= V corr, new norm
+    for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = __ldcg(sc.corr + q);
+    for (int q = threadIdx.x; q < kWarps; q += blockDim.x) red[q] = 0.0;
+    __syncthreads();
+    for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+      const long long cb = ch * kChunk + 2 * threadIdx.x;
+      double u[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 x = ld2cg(u_out + cb + 512 * k);
+        u[2 * k] = x.x;
+        u[2 * k + 1] = x.y;
+      }
+      for (int v = 0; v < nvec; ++v) {
+        const double c = cf[v];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 p = ld2_stream(V + (long long)v * vstride + cb + 512 * k, pol);
+          u[2 * k] = __dsub_rn(u[2 * k], __dmul_rn(c, p.x));
+          u[2 * k + 1] = __dsub_rn(u[2 * k + 1], __dmul_rn(c, p.y));
+        }
+      }
+      double nrm = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        st2(u_out + cb + 512 * k, make_double2(u[2 * k], u[2 * k + 1]));
+        nrm = fma(u[2 * k], u[2 * k], nrm);
+        nrm = fma(u[2 * k + 1], u[2 * k + 1], nrm);
+      }
+      nrm = warp_sum(nrm);
+      if (lane == 0) red[warp] += nrm;
+    }
+  } else {
+    pdl_trigger();
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
@@ -970,22 +1113,35 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   if (!reduce_grouped(part, 1, G, sc.gticket, sc.gpart, red)) return;
   const double hj1 = sqrt(red[0]);
   __syncthreads();
-  if (!REORTH && sc.st->reorth) return;  // the second pass finishes the iteration
+  if (!REORTH && !second && sc.st->reorth) return;  // the separate second pass finishes it
   finish_iteration_block(sc, j, hj1, red);
+}
+
+static size_t gs_smem(const Scal& sc, int nvec) {
+  int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
+  if (slots < 261) slots = 261;  // reduce_grouped scratch
+  return ((size_t)nvec + (size_t)slots) * sizeof(double);
+}
+
+bool gs_can_fuse(int G, const Scal& sc) {
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs<false>, kThreads,
+                                                gs_smem(sc, sc.m + 1));
+  return (long long)per_sm * nsm >= G;
 }
 
 void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
                int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
-               const int* gate, cudaStream_t s) {
-  int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
-  if (slots < 261) slots = 261;  // reduce_grouped scratch
-  const size_t smem = ((size_t)nvec + (size_t)slots) * sizeof(double);
+               const int* gate, bool fuse, cudaStream_t s) {
+  const size_t smem = gs_smem(sc, nvec);
   if (reorth)
     launch_pdl(k_gs<true>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
-               n_pad, part, G, sc, j, gate);
+               n_pad, part, G, sc, j, gate, 0);
   else
     launch_pdl(k_gs<false>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
-               n_pad, part, G, sc, j, gate);
+               n_pad, part, G, sc, j, gate, fuse ? 1 : 0);
 }
 
 // ======================================================================================
@@ -1017,17 +1173,16 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
   }
   const double r00 = fabs(sc.R[0]);
   while (cols > 1 && fabs(sc.R[(size_t)(cols - 1) * (m + 1) + (cols - 1)]) < 1e-14 * r00) --cols;
-  double* Rs = sm;                 // cols x cols, column-major
-  double* y = sm + cols * cols;    // cols
-  for (int e = lane; e < cols * cols; e += 32)
-    Rs[e] = sc.R[(size_t)(e / cols) * (m + 1) + (e % cols)];
+  const double* R = sc.R;          // column k holds rows 0..k (ld m + 1)
+  double* y = sm;                  // cols
   for (int i = lane; i < cols; i += 32) y[i] = sc.g[i];
   __syncwarp();
   for (int k = cols - 1; k >= 0; --k) {
-    if (lane == 0) y[k] = y[k] / Rs[k * cols + k];
+    const double* Rk = R + (size_t)k * (m + 1);
+    if (lane == 0) y[k] = y[k] / Rk[k];
     __syncwarp();
     const double yk = y[k];
-    for (int i = lane; i < k; i += 32) y[i] = __dsub_rn(y[i], __dmul_rn(yk, Rs[k * cols + i]));
+    for (int i = lane; i < k; i += 32) y[i] = __dsub_rn(y[i], __dmul_rn(yk, Rk[i]));
     __syncwarp();
   }
   for (int i = lane; i < cols; i += 32) {
@@ -1044,7 +1199,7 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
 }
 
 void launch_cycle_end(const Scal& sc, cudaStream_t s) {
-  const size_t smem = ((size_t)sc.m * sc.m + sc.m + 1) * sizeof(double);
+  const size_t smem = ((size_t)sc.m + 1) * sizeof(double);
   launch_pdl(k_cycle_end, dim3(1), dim3(32), smem, s, sc);
 }
 // x += M^-1 (sum_{i<cols} y_i V_i)   (krylov.py:206)

@@ -78,7 +78,9 @@ void launch_combine_rows(const double* R, long long rs, const double* sigma, int
 // u = w - sum coef_i u_i (+ corr dots, norm) or the re-orthogonalisation pass.
 void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
                int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
-               const int* gate, cudaStream_t s);
+               const int* gate, bool fuse, cudaStream_t s);
+// the whole k_gs grid is co-resident: the second Gram-Schmidt pass may run inside it
+bool gs_can_fuse(int G, const Scal& sc);
 void launch_cycle_end(const Scal& sc, cudaStream_t s);
 void launch_xupdate(const Dia& A, double* x, const double* V, long long vstride, long long n_pad,
                     const Scal& sc, cudaStream_t s);

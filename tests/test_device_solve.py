@@ -6,6 +6,7 @@ Parity bar (BASELINE north_star): identical labels / column map / d; |x - x_ref|
 from __future__ import annotations
 
 import numpy as np
+import scipy.sparse
 import pytest
 
 import paper_1510_02148_b200 as dk
@@ -256,3 +257,33 @@ def test_jacobi_rejects_zero_diagonal(gpu):
     A = dk.SparseMatrix.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
     with pytest.raises(ValueError):
         dk.Preconditioner.jacobi(A)
+
+
+@pytest.mark.gpu
+def test_second_gram_schmidt_pass_and_long_cycles(gpu, monkeypatch):
+    """A diagonal operator with condition 1e10 and GMRES(250): the basis loses orthogonality,
+    the re-orthogonalisation test fires (krylov.py:167-170) and the second pass runs — inside
+    k_gs (whole grid co-resident) and as separate launches (DK_NO_GS_FUSE); cycles longer than
+    the shared-memory Gram staging (m > 96) read G from global memory."""
+    n, m = 300, 250
+    d = np.logspace(0, 10, n)
+    A = dk.SparseMatrix.from_dia(n, [0], d[None, :])
+    b = np.ones(n)
+    ref = O.run_cycles(scipy.sparse.diags([d], [0]).tocsr(), b, m=m, tol=1e-12, max_iters=2 * m)
+    assert ref["reorths"] > 0
+    reps = []
+    for fuse in (True, False):
+        if fuse:
+            monkeypatch.delenv("DK_NO_GS_FUSE", raising=False)
+        else:
+            monkeypatch.setenv("DK_NO_GS_FUSE", "1")
+        rep = dk.gmres(A, b, m=m, tol=1e-12, max_iters=2 * m)
+        assert rep.reorthogonalisations > 0
+        assert rep.iterations == ref["iterations"]
+        assert 0.2 < rep.final_relres / ref["final_relres"] < 5.0
+        reps.append(rep)
+    # the two paths sum the second-pass dots in different orders; at condition 1e10 the runs
+    # agree to the first plateau and in their final residuals, not digit for digit
+    np.testing.assert_allclose(reps[0].residual_history[:60], reps[1].residual_history[:60],
+                               rtol=1e-6)
+    assert 0.5 < reps[0].final_relres / reps[1].final_relres < 2.0
