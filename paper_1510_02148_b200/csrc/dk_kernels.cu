@@ -1173,12 +1173,22 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
   }
   const double r00 = fabs(sc.R[0]);
   while (cols > 1 && fabs(sc.R[(size_t)(cols - 1) * (m + 1) + (cols - 1)]) < 1e-14 * r00) --cols;
-  const double* R = sc.R;          // column k holds rows 0..k (ld m + 1)
+  // R (column k holds rows 0..k, ld m + 1) staged in shared memory for cycles up to
+  // kStageGram columns, read from global memory beyond
+  const bool stage = m <= kStageGram;
+  const int ldr = stage ? cols : m + 1;
   double* y = sm;                  // cols
+  const double* R = sc.R;
+  if (stage) {
+    double* Rs = sm + cols;
+    for (int e = lane; e < cols * cols; e += 32)
+      Rs[e] = sc.R[(size_t)(e / cols) * (m + 1) + (e % cols)];
+    R = Rs;
+  }
   for (int i = lane; i < cols; i += 32) y[i] = sc.g[i];
   __syncwarp();
   for (int k = cols - 1; k >= 0; --k) {
-    const double* Rk = R + (size_t)k * (m + 1);
+    const double* Rk = R + (size_t)k * ldr;
     if (lane == 0) y[k] = y[k] / Rk[k];
     __syncwarp();
     const double yk = y[k];
@@ -1199,7 +1209,13 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
 }
 
 void launch_cycle_end(const Scal& sc, cudaStream_t s) {
-  const size_t smem = ((size_t)sc.m + 1) * sizeof(double);
+  const size_t m = (size_t)sc.m;
+  const size_t smem = (m + 1 + (sc.m <= kStageGram ? m * m : 0)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_cycle_end, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
   launch_pdl(k_cycle_end, dim3(1), dim3(32), smem, s, sc);
 }
 // x += M^-1 (sum_{i<cols} y_i V_i)   (krylov.py:206)
