@@ -472,15 +472,24 @@ __device__ __forceinline__ double prolong_cell(const Dia& A, const Prolong& P,
                                                int L, double own, unsigned msk) {
   double t = (L >= 0) ? __dmul_rn(own, __ldg(yc + L)) : 0.0;
   if (msk) {
+    // all masked coefficients and neighbour labels first (independent loads in flight), then
+    // the y gathers, then the sum in diagonal order
+    double a[kMaxDiag];
+    int nl[kMaxDiag];
 #pragma unroll
     for (int q = 0; q < kMaxDiag; ++q) {
-      if ((msk >> q) & 1u) {
-        const long long o = A.off[q];
-        double a = dia_coef(A, q, c);
-        if (AM) a = __dmul_rn(a, __ldg(A.inv + c + o));
-        t = __dadd_rn(t, __dmul_rn(a, __ldg(yc + __ldg(P.lab + c + o))));
-      }
+      const bool on = (msk >> q) & 1u;
+      const long long o = A.off[q];
+      a[q] = on ? dia_coef(A, q, c) : 0.0;
+      if (AM) a[q] = on ? __dmul_rn(a[q], __ldg(A.inv + c + o)) : 0.0;
+      nl[q] = on ? __ldg(P.lab + c + o) : 0;
     }
+    double yv[kMaxDiag];
+#pragma unroll
+    for (int q = 0; q < kMaxDiag; ++q) yv[q] = ((msk >> q) & 1u) ? __ldg(yc + nl[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxDiag; ++q)
+      if ((msk >> q) & 1u) t = __dadd_rn(t, __dmul_rn(a[q], yv[q]));
   }
   return t;
 }
