@@ -278,6 +278,9 @@ def test_second_gram_schmidt_pass_and_long_cycles(gpu, monkeypatch):
         else:
             monkeypatch.setenv("DK_NO_GS_FUSE", "1")
         rep = dk.gmres(A, b, m=m, tol=1e-12, max_iters=2 * m)
+        again = dk.gmres(A, b, m=m, tol=1e-12, max_iters=2 * m)  # replayed as a CUDA graph
+        np.testing.assert_array_equal(again.x, rep.x)
+        np.testing.assert_array_equal(again.residual_history, rep.residual_history)
         assert rep.reorthogonalisations > 0
         assert rep.iterations == ref["iterations"]
         assert 0.2 < rep.final_relres / ref["final_relres"] < 5.0
