@@ -236,6 +236,8 @@ cudaError_t big_alloc(void** out, size_t bytes, cudaStream_t s) {
 
 void big_free(void* p, cudaStream_t s) {
   if (!p) return;
+  // the block may be handed to another stream next: let this stream's work on it finish
+  cudaStreamSynchronize(s);
   {
     std::lock_guard<std::mutex> lk(g_big_mu);
     for (size_t i = 0; i < g_big_live.size(); ++i) {
