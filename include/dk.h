@@ -128,6 +128,10 @@ int dk_defl_coarse(dk_defl* ctx, double* E, double* Einv);
 /* Setup timings in ms: [assemble E, factorisation (Cholesky if E is SPD, else pivoted LU),
    forming E^-1, x*]. */
 int dk_defl_setup_ms(dk_defl* ctx, double* ms4);
+/* How y = E^-1 s is applied: *kind = 0 dense GEMV of E^-1, 1 packed symmetric tiles of E^-1,
+   2 two passes over the nonzero tiles of W = L^-1 in nested-dissection order (SPD E),
+   3 dense-basis multi-dot; *tiles = 32 x 32 tiles streamed per application. */
+int dk_defl_coarse_kind(dk_defl* ctx, int32_t* kind, int64_t* tiles);
 
 /* ---- solver ----------------------------------------------------------------------- */
 /* Restarted right-preconditioned GMRES(m) on P1 A M^-1 (ctx != NULL) or A M^-1 (ctx NULL),

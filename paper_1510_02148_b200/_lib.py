@@ -28,7 +28,7 @@ EXPORTS = (
     "dk_defl_reconstruct", "dk_defl_x_star", "dk_defl_coarse", "dk_defl_setup_ms",
     "dk_gmres", "dk_gmres_ex", "dk_last_basis_vector", "dk_levelset_labels",
     "dk_levelset_labels_device", "dk_assemble_tpfa", "dk_defl_create_dense",
-    "dk_defl_create_ritz",
+    "dk_defl_create_ritz", "dk_defl_coarse_kind",
 )
 
 
@@ -89,6 +89,7 @@ def _declare(lib):
         "dk_defl_x_star": (C.c_int, [_P, _P]),
         "dk_defl_coarse": (C.c_int, [_P, _P, _P]),
         "dk_defl_setup_ms": (C.c_int, [_P, _D]),
+        "dk_defl_coarse_kind": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
         "dk_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int32, C.c_int32,
                                _P, _P, _P, _P, C.POINTER(SolveInfo)]),
         "dk_gmres_ex": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_double, C.c_int32, C.c_int32,

@@ -55,12 +55,13 @@ enum ProfClass {
   PC_XUPDATE,
   PC_RESTART,
   PC_COARSE_REDUCE,
+  PC_GEMV_T,
   PC_COUNT
 };
 const char* kProfNames[PC_COUNT] = {"stencil_restrict", "restrict_final", "coarse_gemv",
                                     "prolong_dots",     "gs_update",      "gs_reorth",
                                     "cycle_end",        "x_update",       "restart",
-                                    "coarse_reduce"};
+                                    "coarse_reduce",    "coarse_gemv_t"};
 
 unsigned long long g_ctx_serial = 0;
 
@@ -163,6 +164,15 @@ struct dk_defl {
   double* colpart = nullptr;
   int* seg_ptr = nullptr;   // row-part segment slots per tile row
   int* seg_slot = nullptr;
+  // SPD E in nested-dissection order (dk_profile.cu): y = P^T W^T W P s through two tile
+  // streams of W = L^-1; Einv then holds W (permuted) and E^-1 is formed only on request
+  int prof = 0;
+  int* perm = nullptr;   // perm[i] = label at position i
+  int* iperm = nullptr;  // position of label L
+  double* tv = nullptr;  // t = W s~
+  double* T1 = nullptr;  // stream of W's tiles by block row
+  double* T2 = nullptr;  // stream of W^T's tiles
+  TileGemv tg1{}, tg2{};
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
   double nmasked = 0;  // foreign-label coefficients of the prolongation (byte accounting)
@@ -469,6 +479,16 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
   {
     ProfScope ps(op, PC_RESTRICT, 12.0 * (double)c->nlabelled + 8.0 * c->d);
     launch_restrict_final(c->rm, c->s, gate, op->stream);
+  }
+  if (c->prof) {
+    // tiles + x segments (+ the pieces of blocks split across warps)
+    {
+      ProfScope ps(op, PC_GEMV, (8.0 * 1024.0 + 256.0) * (double)c->tg1.nt);
+      launch_tgemv(c->tg1, c->s, c->tv, nullptr, c->d, gate, op->stream);
+    }
+    ProfScope ps(op, PC_GEMV_T, (8.0 * 1024.0 + 256.0) * (double)c->tg2.nt);
+    launch_tgemv(c->tg2, c->tv, c->y, c->perm, c->d, gate, op->stream);
+    return;
   }
   {
     if (c->sym) {
@@ -994,10 +1014,13 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(big_alloc((void**)&c->Einv, (size_t)d * c->ld * sizeof(double), s));
   tr.mark("E, E^-1 allocated");
   DKD(cudaMallocAsync(&c->piv, (size_t)d * sizeof(int), s));
-  DKD(cudaMallocAsync(&c->s, (size_t)c->ld * sizeof(double), s));
-  DKD(cudaMallocAsync(&c->y, (size_t)c->ld * sizeof(double), s));
-  DKD(cudaMemsetAsync(c->s, 0, (size_t)c->ld * sizeof(double), s));
-  DKD(cudaMemsetAsync(c->y, 0, (size_t)c->ld * sizeof(double), s));
+  const size_t dvec = (size_t)round_up(d, 32) * sizeof(double);  // k_tgemv reads 32-blocks
+  DKD(cudaMallocAsync(&c->s, dvec, s));
+  DKD(cudaMallocAsync(&c->y, dvec, s));
+  DKD(cudaMallocAsync(&c->tv, dvec, s));
+  DKD(cudaMemsetAsync(c->s, 0, dvec, s));
+  DKD(cudaMemsetAsync(c->y, 0, dvec, s));
+  DKD(cudaMemsetAsync(c->tv, 0, dvec, s));
   DKD(cudaMallocAsync(&c->xs_base, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMemsetAsync(c->xs_base, 0, (size_t)op->vlen * sizeof(double), s));
   c->xs = c->xs_base + op->guard;
@@ -1060,8 +1083,81 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(big_alloc((void**)&Ework, ebytes, s));
   DKD(cudaMemcpyAsync(Ework, c->E, ebytes, cudaMemcpyDeviceToDevice, s));
   const bool symmetric = !am && coarse_is_symmetric(c->E, d, c->ld, s);
-  bool inverted = false;
-  if (symmetric) {  // SPD E: Cholesky-based inverse (half the work of LU + solves)
+  bool inverted = false, spd_failed = false;
+  if (symmetric && d >= kSymvMinD && !getenv("DK_NO_ND")) {
+    // nested dissection of the label graph: keep it when W's tiles stream in fewer bytes
+    // (two passes) than the packed triangle of E^-1
+    std::vector<int> gptr, gcol, perm;
+    err = coarse_pattern(c->E, d, c->ld, gptr, gcol, s);
+    if (err) {
+      big_free(Ework, s);
+      return cleanup_fail((cudaError_t)err, "coarse_pattern");
+    }
+    nd_order(d, gptr, gcol, perm);
+    tr.mark("nested dissection");
+    if (2 * nd_profile_tiles(d, gptr, gcol, perm) < symv_tiles(d) || getenv("DK_FORCE_ND")) {
+      std::vector<int> iperm(d);
+      for (int i = 0; i < d; ++i) iperm[perm[i]] = i;
+      DKD(cudaMallocAsync(&c->perm, (size_t)d * sizeof(int), s));
+      DKD(cudaMallocAsync(&c->iperm, (size_t)d * sizeof(int), s));
+      DKD(cudaMemcpyAsync(c->perm, perm.data(), (size_t)d * sizeof(int), cudaMemcpyHostToDevice,
+                          s));
+      DKD(cudaMemcpyAsync(c->iperm, iperm.data(), (size_t)d * sizeof(int),
+                          cudaMemcpyHostToDevice, s));
+      launch_permute_sym(c->E, d, c->ld, c->perm, Ework, s);
+      double min_sq = 0.0;
+      err = spd_inverse(Ework, d, c->ld, c->Einv, &min_sq, &c->ms[1], &c->ms[2], s, false);
+      tr.mark("L, W = L^-1 (nested dissection)");
+      if (err) {
+        big_free(Ework, s);
+        return cleanup_fail((cudaError_t)err, "spd_inverse");
+      }
+      if (min_sq >= 1e-280) {
+        cudaEvent_t p0, p1;
+        cudaEventCreate(&p0);
+        cudaEventCreate(&p1);
+        cudaEventRecord(p0, s);
+        std::vector<int> fW(d);
+        int* df = nullptr;
+        DKD(cudaMallocAsync(&df, (size_t)d * sizeof(int), s));
+        launch_row_first_nz(c->Einv, d, c->ld, df, s);
+        DKD(cudaMemcpyAsync(fW.data(), df, (size_t)d * sizeof(int), cudaMemcpyDeviceToHost, s));
+        DKD(cudaFreeAsync(df, s));
+        DKD(cudaStreamSynchronize(s));
+        TileGemvHost h1, h2;
+        err = profile_streams(c->Einv, d, c->ld, fW, h1, h2, s);
+        if (err) {
+          big_free(Ework, s);
+          return cleanup_fail(err > 0 ? (cudaError_t)err : cudaErrorUnknown, "profile_streams");
+        }
+        DKD(big_alloc((void**)&c->T1, (size_t)h1.nt * 1024 * sizeof(double), s));
+        DKD(big_alloc((void**)&c->T2, (size_t)h2.nt * 1024 * sizeof(double), s));
+        c->tg1.T = c->T1;
+        c->tg2.T = c->T2;
+        err = upload_stream(c->Einv, d, c->ld, false, h1, c->tg1, s);
+        if (!err) err = upload_stream(c->Einv, d, c->ld, true, h2, c->tg2, s);
+        if (err) {
+          big_free(Ework, s);
+          return cleanup_fail((cudaError_t)err, "upload_stream");
+        }
+        cudaEventRecord(p1, s);
+        DKD(cudaStreamSynchronize(s));
+        float pm = 0.f;
+        cudaEventElapsedTime(&pm, p0, p1);
+        c->ms[2] += pm;  // the tile streams belong to the inverse's set-up share
+        cudaEventDestroy(p0);
+        cudaEventDestroy(p1);
+        c->prof = 1;
+        c->rm.s_pos = c->iperm;
+        inverted = true;
+        tr.mark("W tile streams");
+      } else {
+        spd_failed = true;
+        DKD(cudaMemcpyAsync(Ework, c->E, ebytes, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  if (symmetric && !inverted && !spd_failed) {  // SPD E: Cholesky-based inverse
     double min_sq = 0.0;
     tr.mark("E assembled");
     err = spd_inverse(Ework, d, c->ld, c->Einv, &min_sq, &c->ms[1], &c->ms[2], s);
@@ -1092,7 +1188,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   }
   big_free(Ework, s);
   // symmetric E (symmetric A, A_p = A): stream only the upper tile triangle of E^-1
-  if (d >= kSymvMinD && d <= kSymvMaxD && symmetric) {
+  if (d >= kSymvMinD && d <= kSymvMaxD && symmetric && !c->prof) {
     c->sym = 1;
     c->ntiles = symv_tiles(d);
     DKD(big_alloc((void**)&c->P, (size_t)c->ntiles * 1024 * sizeof(double), s));
@@ -1288,7 +1384,12 @@ int dk_defl_destroy(dk_defl* c) {
   big_free(c->E, s);
   big_free(c->Einv, s);
   big_free(c->P, s);
-  void* bufs[] = {c->Z_base,   c->AZ_base,
+  big_free(c->T1, s);
+  big_free(c->T2, s);
+  free_stream(c->tg1, s);
+  free_stream(c->tg2, s);
+  void* bufs[] = {c->perm,     c->iperm,        c->tv,
+                  c->Z_base,   c->AZ_base,
                   c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
                   c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
                   c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->seg_ptr,
@@ -1358,11 +1459,32 @@ int dk_defl_coarse(dk_defl* c, double* E, double* Einv) {
   if (E)
     DK_TRY(cudaMemcpy2DAsync(E, (size_t)c->d * sizeof(double), c->E, (size_t)c->ld * sizeof(double),
                              (size_t)c->d * sizeof(double), c->d, cudaMemcpyDefault, s));
-  if (Einv)
+  if (Einv && c->prof) {  // E^-1 = P^T (W^T W) P, formed on request
+    const size_t eb = (size_t)c->d * c->ld * sizeof(double);
+    double *X = nullptr, *Y = nullptr;
+    DK_TRY(big_alloc((void**)&X, eb, s));
+    DK_TRY(big_alloc((void**)&Y, eb, s));
+    lauum_into(c->Einv, c->d, c->ld, X, s);
+    launch_unpermute_sym(X, c->d, c->ld, c->perm, Y, c->ld, s);
+    DK_TRY(cudaMemcpy2DAsync(Einv, (size_t)c->d * sizeof(double), Y,
+                             (size_t)c->ld * sizeof(double), (size_t)c->d * sizeof(double), c->d,
+                             cudaMemcpyDefault, s));
+    big_free(X, s);
+    big_free(Y, s);
+  } else if (Einv) {
     DK_TRY(cudaMemcpy2DAsync(Einv, (size_t)c->d * sizeof(double), c->Einv,
                              (size_t)c->ld * sizeof(double), (size_t)c->d * sizeof(double), c->d,
                              cudaMemcpyDefault, s));
+  }
   DK_TRY(cudaStreamSynchronize(s));
+  return DK_OK;
+}
+
+int dk_defl_coarse_kind(dk_defl* c, int32_t* kind, int64_t* tiles) {
+  if (!c || !kind || !tiles) return fail(DK_EINVAL, "null argument");
+  const long long nb = (c->d + 31) / 32;
+  *kind = c->dense ? 3 : c->prof ? 2 : c->sym ? 1 : 0;
+  *tiles = c->dense ? 0 : c->prof ? c->tg1.nt + c->tg2.nt : c->sym ? c->ntiles : nb * nb;
   return DK_OK;
 }
 
@@ -1420,7 +1542,7 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   cudaEventCreate(&e1);
   cudaEventRecord(e0, op->stream);
   // stencil (+ restrict + E^-1 s; dense: one multi-dot)
-  const int coarse_launches = c ? (c->dense ? 2 : c->sym ? 4 : 3) : 1;
+  const int coarse_launches = c ? (c->dense ? 2 : (c->sym || c->prof) ? 4 : 3) : 1;
   // restart (stencil chain + projection), m x (stencil chain, projection, update [+ the
   // separate second pass]), cycle end, x update
   const int per_cycle_launches =

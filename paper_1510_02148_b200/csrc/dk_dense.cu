@@ -441,6 +441,17 @@ __global__ void __launch_bounds__(256) k_mirror_upper(double* __restrict__ X, in
 
 }  // namespace
 
+void launch_row_first_nz(const double* X, int d, int ld, int* f, cudaStream_t s) {
+  k_row_first_nz<<<148 * 4, 256, 0, s>>>(X, d, ld, f);
+}
+
+// X = W^T W (full) for lower-triangular W
+void lauum_into(const double* W, int d, int ld, double* X, cudaStream_t s) {
+  gemm_mma(true, false, W, ld, W, ld, X, ld, d, d, d, 1.0, 0.0, 2, 0, s);
+  const int nt = (d + 31) / 32;
+  k_mirror_upper<<<dim3(nt, nt), 256, 0, s>>>(X, d, ld);
+}
+
 int g_gemm_nt = 2;  // n8 tiles per warp of the set-up GEMM (2: 128 x 64 CTA tiles, 2 per SM)
 
 void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int ldb, double* C,
@@ -474,7 +485,7 @@ static cudaStream_t side_stream() {
 }
 
 int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
-                float* ms_inv, cudaStream_t s) {
+                float* ms_inv, cudaStream_t s, bool form_inverse) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
@@ -605,11 +616,7 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
   }
   // 3. E^-1 = W^T W: upper tiles into L's storage (A = W^T, B = W lower: K from the tile
   //    column), then the lower triangle mirrored
-  gemm_mma(true, false, W, ld, W, ld, L, ld, d, d, d, 1.0, 0.0, 2, 0, s);
-  {
-    const int nt = (d + 31) / 32;
-    k_mirror_upper<<<dim3(nt, nt), 256, 0, s>>>(L, d, ld);
-  }
+  if (form_inverse) lauum_into(W, d, ld, L, s);
   cudaEventRecord(e2, s);
   cudaStreamSynchronize(s);
   cudaEventElapsedTime(ms_fac, e0, e1);

@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
                                                              const int* __restrict__ long_ids,
                                                              int nlong, int short_blocks,
                                                              double* __restrict__ s,
+                                                             const int* __restrict__ s_pos,
                                                              const int* __restrict__ gate) {
   pdl_wait();
   if (gate != nullptr && *gate == 0) return;
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
     double acc = 0.0;
 #pragma unroll 4
     for (int k = lo; k < hi; ++k) acc += __ldcg(run_part + k);
-    s[L] = acc;
+    s[s_pos ? s_pos[L] : L] = acc;
     return;
   }
   // one warp per long column (lane-strided, fixed xor tree)
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
   const int lo = ptr[L], hi = ptr[L + 1];
   for (int k = lo + lane; k < hi; k += 32) acc += __ldcg(run_part + k);
   acc = warp_sum(acc);
-  if (lane == 0) s[L] = acc;
+  if (lane == 0) s[s_pos ? s_pos[L] : L] = acc;
 }
 
 void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s) {
@@ -334,7 +335,7 @@ void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cud
   const unsigned grid =
       (unsigned)(short_blocks + ((long long)rm.nlong * 32 + kThreads - 1) / kThreads);
   launch_pdl(k_restrict_final, dim3(grid), dim3(kThreads), 0, s, rm.run_part, rm.lab_run_ptr,
-             rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, gate);
+             rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, rm.s_pos, gate);
 }
 
 // ======================================================================================

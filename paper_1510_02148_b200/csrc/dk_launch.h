@@ -25,6 +25,7 @@ struct RunMap {            // label-segmented restriction metadata (see DESIGN.m
   int d;
   const int* long_ids;     // columns with more than kShortRuns runs (summed by a warp)
   int nlong;
+  const int* s_pos;        // nullptr, or the position of label L in s (coarse ordering)
 };
 constexpr int kShortRuns = 16;
 
@@ -33,7 +34,7 @@ constexpr int kShortRuns = 16;
 void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
                     const double* scale, const double* b, double* out, const RunMap* rm,
                     const int* gate, cudaStream_t s);
-// s[L] = sum of run partials of label L, fixed order.
+// s[s_pos[L]] (s[L] without s_pos) = sum of run partials of label L, fixed order.
 void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s);
 // y = M x, M d x d row-major with leading dimension ld.
 void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
@@ -136,7 +137,58 @@ void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int l
 // Symmetric positive definite E (in L, overwritten): Cholesky, W = L^-1 (into W), then
 // E^-1 = W^T W written back into L (full).  *min_diag_sq = min L_kk^2 (NaN if not SPD); when
 // it is below 1e-280 the inverse is not formed and the caller falls back to LU.
+// form_inverse = false stops after W = L^-1 (W holds it, L the factor).
 int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
-                float* ms_inv, cudaStream_t s);
+                float* ms_inv, cudaStream_t s, bool form_inverse = true);
+// X = W^T W (full, d x d) for lower-triangular W
+void lauum_into(const double* W, int d, int ld, double* X, cudaStream_t s);
+
+// ---- coarse solve through W = L^-1 in nested-dissection order (dk_profile.cu) ----
+constexpr int kTgGrid = 148, kTgWarps = 12;
+// a tile stream of k_tgemv: nt 32 x 32 tiles grouped by output block (trow ascending)
+struct TileGemv {
+  const double* T = nullptr;   // [nt][16][32][2]
+  const int* trow = nullptr;   // output block per tile
+  const int* tcol = nullptr;   // input block per tile
+  const int* rfirst = nullptr; // first warp of each output block
+  const int* rslot = nullptr;  // partial-slot base of a block split across warps
+  const int* rnp = nullptr;    // warps holding pieces of the block
+  double* part = nullptr;      // [slots][32]
+  unsigned* cnt = nullptr;     // arrival tickets per output block (reset by the last)
+  long long nt = 0;
+  int nw = 0;                  // warps holding tiles (min(kTgGrid * kTgWarps, nt))
+  int nrows = 0;
+};
+struct TileGemvHost {
+  long long nt = 0;
+  int nw = 0;
+  std::vector<int> trow, tcol, rfirst, rslot, rnp;
+  int nslots = 1;
+};
+// E's off-diagonal pattern (CSR, host)
+int coarse_pattern(const double* E, int d, int ld, std::vector<int>& ptr, std::vector<int>& col,
+                   cudaStream_t s);
+// level-structure nested dissection of the pattern graph: perm[new] = old
+void nd_order(int d, const std::vector<int>& ptr, const std::vector<int>& col,
+              std::vector<int>& perm);
+// 32 x 32 tiles of W's structural row profile under perm (upper bound of the stream)
+long long nd_profile_tiles(int d, const std::vector<int>& ptr, const std::vector<int>& col,
+                           const std::vector<int>& perm);
+void launch_permute_sym(const double* E, int d, int ld, const int* perm, double* out,
+                        cudaStream_t s);
+void launch_unpermute_sym(const double* X, int d, int ld, const int* perm, double* out, int ldo,
+                          cudaStream_t s);
+// nonzero tiles of W (row profile fW) as the two streams t = W s~ and y~ = W^T t
+int profile_streams(const double* W, int d, int ld, const std::vector<int>& fW,
+                    TileGemvHost& p1, TileGemvHost& p2, cudaStream_t s);
+// metadata to the device and the tiles packed into g.T (allocated by the caller, nt x 8 KB)
+int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost& h, TileGemv& g,
+                  cudaStream_t s);
+void free_stream(TileGemv& g, cudaStream_t s);
+// y[scatter ? scatter[i] : i] = (sum over the stream's tiles) for rows i < d
+void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
+                  const int* gate, cudaStream_t s);
+// f[r] = first nonzero column of row r (<= r) of a d x d matrix (device)
+void launch_row_first_nz(const double* X, int d, int ld, int* f, cudaStream_t s);
 
 }  // namespace dk

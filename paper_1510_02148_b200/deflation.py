@@ -147,6 +147,14 @@ class DeflationContext:
         _lib.check(self._lib.dk_defl_setup_ms(self.h, ms))
         return {"assemble_E": ms[0], "factor": ms[1], "inverse": ms[2], "x_star": ms[3]}
 
+    _COARSE_KINDS = ("dense_gemv", "packed_symmetric", "nested_dissection_W", "dense_basis")
+
+    def coarse_kind(self) -> tuple:
+        """(how E^-1 is applied, 32 x 32 tiles streamed per application) — see include/dk.h."""
+        k, t = C.c_int32(), C.c_int64()
+        _lib.check(self._lib.dk_defl_coarse_kind(self.h, C.byref(k), C.byref(t)))
+        return self._COARSE_KINDS[k.value], int(t.value)
+
     @property
     def AZ(self) -> np.ndarray:
         """Dense A_p Z (small problems only; the device never forms it)."""

@@ -192,3 +192,42 @@ def test_symmetric_indefinite_coarse_system_falls_back_to_lu(gpu):
     np.testing.assert_array_equal(E, E.T)
     assert np.linalg.eigvalsh(E).min() < 0 < np.linalg.eigvalsh(E).max()
     assert rel(Einv, np.linalg.inv(E)) < 1e-10
+
+
+@pytest.mark.parametrize("boxes,force", [((12, 10, 6), True), ((24, 20, 12), True)])
+def test_nested_dissection_coarse_solve(gpu, boxes, force, monkeypatch):
+    """SPD E with hundreds of labels: y = E^-1 s runs as P^T W^T W P s over the nonzero tiles
+    of W = L^-1 in nested-dissection order (dk_profile.cu); projectors, x* and the formed
+    E^-1 agree with the label oracle's dense solve."""
+    grid = dk.Grid(48, 40, 24)
+    rng = np.random.default_rng(sum(boxes))
+    k = 10.0 ** rng.uniform(-2, 2, grid.n_cells)
+    field = dk.PermeabilityField(grid, k, k.copy(), 0.1 * k)
+    q = np.zeros(grid.n_cells)
+    q[0], q[-1] = 1.0, -1.0
+    prob = dk.assemble_pressure(field, dk.BoundarySpec(), q)
+    A, b = prob.A, prob.b
+    part = dk.subdomain_partition(grid, *boxes)
+    basis = dk.partition_to_basis(part)
+    M = dk.Preconditioner.jacobi(A)
+    if force:  # below the size where it pays: forced (DK_FORCE_ND)
+        monkeypatch.setenv("DK_FORCE_ND", "1")
+    ctx = dk.build_context(A, M, basis, b)
+    kind, tiles = ctx.coarse_kind()
+    assert kind == "nested_dissection_W"
+    nb = (basis.d + 31) // 32
+    assert force or tiles < nb * (nb + 1) // 2
+    Ac = sp.csr_matrix((A.values, A.col_indices, A.row_offsets), shape=(A.n, A.n))
+    o = O.LabelDeflation(Ac, basis.labels, basis.d, b, M.inv_diag)
+    E, Einv = ctx.coarse_matrix()
+    np.testing.assert_allclose(Einv @ E, np.eye(basis.d), atol=1e-9)
+    v = rng.standard_normal(A.n)
+    assert rel(ctx.apply_p1(v), o.apply_p1(v)) < 1e-11
+    assert rel(ctx.apply_p2(v), o.apply_p2(v)) < 1e-11
+    assert rel(ctx.x_star, o.x_star) < 1e-11
+    # deterministic: the same application twice is bit-identical
+    np.testing.assert_array_equal(ctx.apply_p1(v), ctx.apply_p1(v))
+    rep = dk.gmres(A, b, M=M, m=30, tol=1e-10, max_iters=3000, deflation=ctx)
+    ref = O.run_cycles(Ac, b, None, M.inv_diag, 30, 1e-10, 3000, 0, o)
+    assert abs(rep.iterations - ref["iterations"]) <= 2
+    assert rel(rep.x, ref["x"]) <= 1e-8
