@@ -55,13 +55,12 @@ enum ProfClass {
   PC_XUPDATE,
   PC_RESTART,
   PC_COARSE_REDUCE,
-  PC_GEMV_T,
   PC_COUNT
 };
 const char* kProfNames[PC_COUNT] = {"stencil_restrict", "restrict_final", "coarse_gemv",
                                     "prolong_dots",     "gs_update",      "gs_reorth",
                                     "cycle_end",        "x_update",       "restart",
-                                    "coarse_reduce",    "coarse_gemv_t"};
+                                    "coarse_reduce"};
 
 unsigned long long g_ctx_serial = 0;
 
@@ -476,19 +475,19 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
     ProfScope ps(op, PC_STENCIL, by * n);
     launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream);
   }
+  if (c->prof) {  // s~ = P Z^T w, then the two tile streams (t = W s~, y = P^T W^T t)
+    {
+      ProfScope ps(op, PC_RESTRICT, 12.0 * (double)c->nlabelled + 8.0 * c->d);
+      launch_restrict_final(c->rm, c->s, gate, op->stream);
+    }
+    ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)(c->tg1.nt + c->tg2.nt));
+    launch_tgemv(c->tg1, c->s, c->tv, nullptr, c->d, gate, op->stream);
+    launch_tgemv(c->tg2, c->tv, c->y, c->perm, c->d, gate, op->stream);
+    return;
+  }
   {
     ProfScope ps(op, PC_RESTRICT, 12.0 * (double)c->nlabelled + 8.0 * c->d);
     launch_restrict_final(c->rm, c->s, gate, op->stream);
-  }
-  if (c->prof) {
-    // tiles + x segments (+ the pieces of blocks split across warps)
-    {
-      ProfScope ps(op, PC_GEMV, (8.0 * 1024.0 + 256.0) * (double)c->tg1.nt);
-      launch_tgemv(c->tg1, c->s, c->tv, nullptr, c->d, gate, op->stream);
-    }
-    ProfScope ps(op, PC_GEMV_T, (8.0 * 1024.0 + 256.0) * (double)c->tg2.nt);
-    launch_tgemv(c->tg2, c->tv, c->y, c->perm, c->d, gate, op->stream);
-    return;
   }
   {
     if (c->sym) {
@@ -1082,18 +1081,22 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   double* Ework = nullptr;
   DKD(big_alloc((void**)&Ework, ebytes, s));
   DKD(cudaMemcpyAsync(Ework, c->E, ebytes, cudaMemcpyDeviceToDevice, s));
+  tr.mark("E assembled + copied");
   const bool symmetric = !am && coarse_is_symmetric(c->E, d, c->ld, s);
+  tr.mark("symmetry check");
   bool inverted = false, spd_failed = false;
   if (symmetric && d >= kSymvMinD && !getenv("DK_NO_ND")) {
     // nested dissection of the label graph: keep it when W's tiles stream in fewer bytes
     // (two passes) than the packed triangle of E^-1
     std::vector<int> gptr, gcol, perm;
+    std::vector<NDTreeNode> tree;
     err = coarse_pattern(c->E, d, c->ld, gptr, gcol, s);
     if (err) {
       big_free(Ework, s);
       return cleanup_fail((cudaError_t)err, "coarse_pattern");
     }
-    nd_order(d, gptr, gcol, perm);
+    tr.mark("pattern of E");
+    nd_order(d, gptr, gcol, perm, &tree);
     tr.mark("nested dissection");
     if (2 * nd_profile_tiles(d, gptr, gcol, perm) < symv_tiles(d) || getenv("DK_FORCE_ND")) {
       std::vector<int> iperm(d);
@@ -1106,8 +1109,19 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
                           cudaMemcpyHostToDevice, s));
       launch_permute_sym(c->E, d, c->ld, c->perm, Ework, s);
       double min_sq = 0.0;
-      err = spd_inverse(Ework, d, c->ld, c->Einv, &min_sq, &c->ms[1], &c->ms[2], s, false);
-      tr.mark("L, W = L^-1 (nested dissection)");
+      cudaEvent_t f0, f1;
+      cudaEventCreate(&f0);
+      cudaEventCreate(&f1);
+      cudaEventRecord(f0, s);
+      DKD(cudaMemsetAsync(c->Einv, 0, ebytes, s));
+      err = nd_tree_inverse(Ework, d, c->ld, tree, c->Einv, &min_sq, s);
+      cudaEventRecord(f1, s);
+      cudaEventSynchronize(f1);
+      cudaEventElapsedTime(&c->ms[1], f0, f1);
+      c->ms[2] = 0.f;
+      cudaEventDestroy(f0);
+      cudaEventDestroy(f1);
+      tr.mark("W = L^-1 along the dissection tree");
       if (err) {
         big_free(Ework, s);
         return cleanup_fail((cudaError_t)err, "spd_inverse");

@@ -16,7 +16,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -50,6 +54,12 @@ __device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) 
                "r"(bytes));
 }
 
+// 8-byte variant for operands that are not 16-byte aligned (odd column offsets / strides)
+__device__ __forceinline__ void cp8(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sm32(dst)), "l"(src),
+               "r"(bytes));
+}
+
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
 template <int N>
@@ -68,7 +78,7 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
 // Stage one GK-deep slice of an operand tile of extent EXT.  KCONT: the global operand is
 // stored with K contiguous (rows = the M or N index), else with M/N contiguous (rows = K).
 // `mn_lim` bounds the M/N index, `k_lim` the K index; invalid halves are zero-filled.
-template <bool KCONT, int EXT>
+template <bool KCONT, int EXT, bool A8>
 __device__ __forceinline__ void stage_operand(double* s, const double* g, int ldg, int mn0,
                                               int mn_lim, int k0, int k_lim) {
   constexpr int LDM = EXT + 4;
@@ -95,7 +105,12 @@ __device__ __forceinline__ void stage_operand(double* s, const double* g, int ld
       valid = (gk < k_lim) ? min(2, max(0, mn_lim - gmn)) : 0;
       src = g + (long long)gk * ldg + gmn;
     }
-    cp16(s + so, valid ? src : g, valid * 8);
+    if (A8) {  // the pair's second element sits at +1 (K) or +1 (M/N) in both layouts
+      cp8(s + so, valid >= 1 ? src : g, valid >= 1 ? 8 : 0);
+      cp8(s + so + 1, valid >= 2 ? src + 1 : g, valid >= 2 ? 8 : 0);
+    } else {
+      cp16(s + so, valid ? src : g, valid * 8);
+    }
   }
 }
 
@@ -107,10 +122,10 @@ __device__ __forceinline__ void stage_operand(double* s, const double* g, int ld
 // completes before the epilogue.  kshift != INT_MIN: B is lower triangular in the sense
 // B[k][j] == 0 for k < j + kshift, so tile column c0 starts its K loop at c0 + kshift
 // (rounded down to GK).
-template <bool TA, bool TB, int NT>
+template <bool TA, bool TB, int NT, bool A8>
 __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
     k_dgemm_mma(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
-                int N, int K, double alpha, double beta, int tri, int kshift) {
+                int N, int K, double alpha, double beta, int tri, int kshift, int kstop) {
   constexpr int BN = 32 * NT, LDMA = GM + 4, LDMB = BN + 4;
   constexpr int OPA = op_doubles<GM>(), OPB = op_doubles<BN>();
   extern __shared__ __align__(128) double smem[];
@@ -122,7 +137,9 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
     kbeg = c0 + kshift;
     kbeg = kbeg < 0 ? 0 : (kbeg / GK) * GK;
   }
-  const int nk = (K > kbeg) ? (K - kbeg + GK - 1) / GK : 0;
+  int kend = K;
+  if (kstop != INT_MIN) kend = min(K, c0 + BN + kstop);  // op(B)[k][j] == 0 for k >= j + kstop
+  const int nk = (kend > kbeg) ? (kend - kbeg + GK - 1) / GK : 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 2) * 64, wn = (warp & 3) * (8 * NT);
@@ -145,7 +162,10 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           const int col = c0 + wn + j * 8 + 2 * t;
-          if (col + 1 < N) {
+          if (A8) {
+            if (col < N) acc[i][j][2 * h] = sc * crow[col];
+            if (col + 1 < N) acc[i][j][2 * h + 1] = sc * crow[col + 1];
+          } else if (col + 1 < N) {
             const double2 cv = *reinterpret_cast<const double2*>(crow + col);
             acc[i][j][2 * h] = sc * cv.x;
             acc[i][j][2 * h + 1] = sc * cv.y;
@@ -160,8 +180,8 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
     double* sa = smem + (it % GSTAGES) * (OPA + OPB);
     double* sb = sa + OPA;
     const int k0 = kbeg + it * GK;
-    stage_operand<!TA, GM>(sa, A, lda, r0, M, k0, K);
-    stage_operand<TB, BN>(sb, B, ldb, c0, N, k0, K);
+    stage_operand<!TA, GM, A8>(sa, A, lda, r0, M, k0, K);
+    stage_operand<TB, BN, A8>(sb, B, ldb, c0, N, k0, K);
   };
 #pragma unroll
   for (int it = 0; it < GSTAGES - 1; ++it) {
@@ -212,36 +232,59 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         const int col = c0 + wn + j * 8 + 2 * t;
-        if (col + 1 < N)
+        if (A8) {
+          if (col < N) crow[col] = alpha * acc[i][j][2 * h];
+          if (col + 1 < N) crow[col + 1] = alpha * acc[i][j][2 * h + 1];
+        } else if (col + 1 < N) {
           *reinterpret_cast<double2*>(crow + col) =
               make_double2(alpha * acc[i][j][2 * h], alpha * acc[i][j][2 * h + 1]);
-        else if (col < N)
+        } else if (col < N) {
           crow[col] = alpha * acc[i][j][2 * h];
+        }
       }
     }
   }
 }
 
-template <bool TA, bool TB, int NT>
-void launch_mma(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
-                int N, int K, double alpha, double beta, int tri, int kshift, cudaStream_t s) {
+template <bool TA, bool TB, int NT, bool A8>
+void launch_mma_a(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
+                  int N, int K, double alpha, double beta, int tri, int kshift, int kstop,
+                  cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dgemm_mma<TA, TB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         gemm_smem<NT>());
+    cudaFuncSetAttribute(k_dgemm_mma<TA, TB, NT, A8>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem<NT>());
     attr = true;
   }
   dim3 grid((N + 32 * NT - 1) / (32 * NT), (M + GM - 1) / GM);
-  k_dgemm_mma<TA, TB, NT><<<grid, 256, gemm_smem<NT>(), s>>>(A, lda, B, ldb, C, ldc, M, N, K,
-                                                            alpha, beta, tri, kshift);
+  k_dgemm_mma<TA, TB, NT, A8><<<grid, 256, gemm_smem<NT>(), s>>>(A, lda, B, ldb, C, ldc, M, N,
+                                                                K, alpha, beta, tri, kshift,
+                                                                kstop);
+}
+
+// operands at odd column offsets or with odd strides take the 8-byte copy path
+template <bool TA, bool TB, int NT>
+void launch_mma(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
+                int N, int K, double alpha, double beta, int tri, int kshift, int kstop,
+                cudaStream_t s) {
+  const bool a8 = (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15) != 0 ||
+                  ((lda | ldb | ldc) & 1) != 0;
+  if (a8)
+    launch_mma_a<TA, TB, NT, true>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift,
+                                   kstop, s);
+  else
+    launch_mma_a<TA, TB, NT, false>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift,
+                                    kstop, s);
 }
 
 template <bool TA, bool TB>
 void launch_mma_nt(int nt, const double* A, int lda, const double* B, int ldb, double* C,
                    int ldc, int M, int N, int K, double alpha, double beta, int tri, int kshift,
-                   cudaStream_t s) {
-  if (nt == 2) launch_mma<TA, TB, 2>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
-  else launch_mma<TA, TB, 4>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+                   int kstop, cudaStream_t s) {
+  if (nt == 2)
+    launch_mma<TA, TB, 2>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, kstop, s);
+  else
+    launch_mma<TA, TB, 4>(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, kstop, s);
 }
 
 // ---- Cholesky pieces ---------------------------------------------------------------------
@@ -280,10 +323,18 @@ __device__ __forceinline__ double sel(const double (&v)[N], int k) {
 // step c has updated them; warps whose rows are all done sit out), then X = L~^-1 by a
 // right-looking sweep over rows, and L11^-1 = D^-1/2 X.  pmin[blk] = min pivot D_cc
 // (= L_cc^2); NaN if a pivot is not positive.
+// jobs != nullptr: a batch of independent blocks, CTA b takes (k0, nb) = jobs[b] and
+// writes pmin[blk + b].
 __global__ void __launch_bounds__(32 * DNW, 1) k_chol_diag(const double* __restrict__ A, int ld,
                                                           int k0, int nb, double* __restrict__ W,
-                                                          double* __restrict__ pmin, int blk) {
+                                                          double* __restrict__ pmin, int blk,
+                                                          const int2* __restrict__ jobs) {
   constexpr int RPW = DB / DNW, CPL = DB / 32;
+  if (jobs != nullptr) {
+    k0 = jobs[blockIdx.x].x;
+    nb = jobs[blockIdx.x].y;
+    blk += blockIdx.x;
+  }
   extern __shared__ __align__(16) double dsm[];
   double(*lt)[DB + 1] = reinterpret_cast<double(*)[DB + 1]>(dsm);  // L~ (unit lower)
   double* buf = dsm + DB * (DB + 1);                                // 2 x DB columns
@@ -456,16 +507,16 @@ int g_gemm_nt = 2;  // n8 tiles per warp of the set-up GEMM (2: 128 x 64 CTA til
 
 void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int ldb, double* C,
               int ldc, int M, int N, int K, double alpha, double beta, int tri, int kshift,
-              cudaStream_t s) {
+              cudaStream_t s, int kstop) {
   if (M <= 0 || N <= 0) return;
   // N <= tile width: one tile column (the in-place TRSM relies on it)
   const int nt = (N <= 64) ? 2 : (N <= 128) ? 4 : g_gemm_nt;
   if (ta) {
-    if (tb) launch_mma_nt<true, true>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
-    else launch_mma_nt<true, false>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+    if (tb) launch_mma_nt<true, true>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, kstop, s);
+    else launch_mma_nt<true, false>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, kstop, s);
   } else {
-    if (tb) launch_mma_nt<false, true>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
-    else launch_mma_nt<false, false>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, s);
+    if (tb) launch_mma_nt<false, true>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, kstop, s);
+    else launch_mma_nt<false, false>(nt, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, tri, kshift, kstop, s);
   }
 }
 
@@ -485,7 +536,7 @@ static cudaStream_t side_stream() {
 }
 
 int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
-                float* ms_inv, cudaStream_t s, bool form_inverse) {
+                float* ms_inv, cudaStream_t s, bool form_inverse, bool clear_w) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
@@ -500,7 +551,7 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
   auto at = [&](double* X, int r, int c) { return X + (long long)r * ld + c; };
   double* dpmin = nullptr;
   cudaMallocAsync(&dpmin, nblk * sizeof(double), s);
-  cudaMemsetAsync(W, 0, (size_t)d * ld * sizeof(double), s);
+  if (clear_w) cudaMemsetAsync(W, 0, (size_t)d * ld * sizeof(double), s);
   // row profile -> reach(t) = 1 + the last row whose profile starts left of column t: the rows
   // of L that can be nonzero in columns < t lie in [t, reach(t))
   std::vector<int> reach(d + 1, 0);
@@ -545,7 +596,7 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
     const int G0 = g * GB, gend = (d - G0 < GB) ? d : G0 + GB;
     for (int K0 = G0; K0 < gend; K0 += DB) {  // chain(g), side stream
       const int nb = (d - K0 < DB) ? d - K0 : DB, Kend = K0 + nb;
-      k_chol_diag<<<1, 32 * DNW, kDiagSmem, side>>>(L, ld, K0, nb, W, dpmin, K0 / DB);
+      k_chol_diag<<<1, 32 * DNW, kDiagSmem, side>>>(L, ld, K0, nb, W, dpmin, K0 / DB, nullptr);
       const int rq = reach[Kend] - Kend;  // rows below the block inside the profile
       if (Kend >= d || rq <= 0) continue;
       gemm_mma(false, true, at(L, Kend, K0), ld, at(W, K0, K0), ld, at(L, Kend, K0), ld, rq, nb,
@@ -625,6 +676,133 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
   return (int)cudaGetLastError();
+}
+
+
+// ---- SPD inverse factor along a nested-dissection tree ------------------------------------
+// E~ (nested-dissection order) has, for every tree node N with separator S and descendants D
+// (the children's subtrees, which E~ does not couple), the block structure
+//     E~_T = [[E_D, E_SD^T], [E_SD, E_S]],  E_D = blockdiag(E_C),
+// so with W_C = L_C^-1 of every child already formed (post-order):
+//     L_SD = E_SD W_D^T,  S = E_S - L_SD L_SD^T = L_S L_S^T,  W_S = L_S^-1,
+//     W_SD = -W_S L_SD W_D,
+// i.e. W = L^-1 is built node by node with GEMMs over the node's own rows only: O(sum |S|
+// |D|^2) instead of the O(d^3) of the dense factorisation.  Leaves (no descendants) are
+// factorised and inverted in one batched launch.  E~ is overwritten by the Schur complements
+// on the separator diagonal blocks; W must be zero on entry.
+int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tree, double* W,
+                    double* min_diag_sq, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
+    attr = true;
+  }
+  auto at = [&](double* X, int r, int c) { return X + (long long)r * ld + c; };
+  // leaves: batched diagonal factorisation + inversion
+  std::vector<int2> jobs;
+  long long xmax = 0;
+  int nbig = 0;
+  for (const auto& n : tree) {
+    const int ns = n.s1 - n.s0, nd = n.s0 - n.t0;
+    if (ns <= 0) continue;
+    if (nd == 0 && ns <= DB) jobs.push_back(make_int2(n.s0, ns));
+    else if (ns > DB) ++nbig;
+    if (nd > 0) xmax = std::max(xmax, (long long)ns * nd);
+  }
+  const int nslots = (int)jobs.size() + (int)tree.size() + 1;
+  double* dpmin = nullptr;
+  int2* djobs = nullptr;
+  double *X = nullptr, *T = nullptr;
+  cudaMallocAsync(&dpmin, (size_t)nslots * sizeof(double), s);
+  cudaMemsetAsync(dpmin, 0x7f, (size_t)nslots * sizeof(double), s);  // large positive
+  if (!jobs.empty()) {
+    cudaMallocAsync(&djobs, jobs.size() * sizeof(int2), s);
+    cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
+    k_chol_diag<<<(unsigned)jobs.size(), 32 * DNW, kDiagSmem, s>>>(E, ld, 0, 0, W, dpmin, 0,
+                                                                     djobs);
+  }
+  if (xmax > 0) {
+    cudaMallocAsync(&X, (size_t)xmax * sizeof(double), s);
+    cudaMallocAsync(&T, (size_t)xmax * sizeof(double), s);
+  }
+  double host_min = INFINITY;
+  int slot = (int)jobs.size();
+  const bool trace = getenv("DK_TRACE_TREE") != nullptr;
+  cudaEvent_t tev[3];
+  if (trace) {
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], s);
+    cudaEventSynchronize(tev[0]);
+  }
+  auto t_start = std::chrono::steady_clock::now();
+  for (const auto& n : tree) {
+    const int ns = n.s1 - n.s0, nd = n.s0 - n.t0;
+    if (ns <= 0 || (nd == 0 && ns <= DB)) continue;
+    if (trace) cudaEventRecord(tev[1], s);
+    if (nd > 0) {
+      const int ldx = nd;
+      // L_SD = E_SD W_D^T, child by child (W_C lower: op(B)[k][j] = 0 for k > j)
+      for (int k : n.kids) {
+        const int a = tree[k].t0, nc = tree[k].s1 - tree[k].t0;
+        gemm_mma(false, true, at(E, n.s0, a), ld, at(W, a, a), ld, X + (a - n.t0), ldx, ns, nc,
+                 nc, 1.0, 0.0, 0, INT_MIN, s, 0);
+      }
+      // S = E_S - L_SD L_SD^T (lower tiles)
+      gemm_mma(false, true, X, ldx, X, ldx, at(E, n.s0, n.s0), ld, ns, ns, nd, -1.0, 1.0, 1,
+               INT_MIN, s);
+      // T = L_SD W_D, child by child (W_C lower: B[k][j] = 0 for k < j)
+      for (int k : n.kids) {
+        const int a = tree[k].t0, nc = tree[k].s1 - tree[k].t0;
+        gemm_mma(false, false, X + (a - n.t0), ldx, at(W, a, a), ld, T + (a - n.t0), ldx, ns,
+                 nc, nc, 1.0, 0.0, 0, 0, s);
+      }
+    }
+    // W_S = chol(S)^-1
+    if (ns <= DB) {
+      k_chol_diag<<<1, 32 * DNW, kDiagSmem, s>>>(E, ld, n.s0, ns, W, dpmin, slot++, nullptr);
+    } else {
+      double mn = 0.0;
+      float f0 = 0.f, f1 = 0.f;
+      const int err = spd_inverse(at(E, n.s0, n.s0), ns, ld, at(W, n.s0, n.s0), &mn, &f0, &f1,
+                                  s, false, false);
+      if (err) return err;
+      host_min = (mn != mn || host_min != host_min) ? NAN : fmin(host_min, mn);
+      if (!(mn >= 1e-280)) break;  // not SPD: the caller falls back
+    }
+    // W_SD = -W_S T
+    if (nd > 0)
+      gemm_mma(false, false, at(W, n.s0, n.s0), ld, T, nd, at(W, n.s0, n.t0), ld, ns, nd, ns,
+               -1.0, 0.0, 0, INT_MIN, s);
+    if (trace) {
+      cudaEventRecord(tev[2], s);
+      cudaEventSynchronize(tev[2]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[1], tev[2]);
+      fprintf(stderr, "[tree] node sep %d desc %d kids %zu: %.3f ms\n", ns, nd, n.kids.size(),
+              ms);
+    }
+  }
+  if (trace) {
+    cudaEventRecord(tev[2], s);
+    cudaEventSynchronize(tev[2]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, tev[0], tev[2]);
+    fprintf(stderr, "[tree] leaves %zu; nodes total %.3f ms device, %.3f ms host\n", jobs.size(),
+            ms, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                          t_start).count());
+  }
+  std::vector<double> pm(slot > 0 ? slot : 1, INFINITY);
+  if (slot > 0)
+    cudaMemcpyAsync(pm.data(), dpmin, (size_t)slot * sizeof(double), cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cudaFreeAsync(dpmin, s);
+  if (djobs) cudaFreeAsync(djobs, s);
+  if (X) cudaFreeAsync(X, s);
+  if (T) cudaFreeAsync(T, s);
+  double mn = host_min;
+  for (int i = 0; i < slot; ++i) mn = (pm[i] != pm[i] || mn != mn) ? NAN : fmin(mn, pm[i]);
+  *min_diag_sq = mn;
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
 }
 
 }  // namespace dk

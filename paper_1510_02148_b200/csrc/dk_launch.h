@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <string>
 #include <vector>
 
@@ -130,21 +131,26 @@ int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min
                    float* ms_lu, float* ms_inv, cudaStream_t s);
 // C = beta C + alpha op(A) op(B) on the fp64 tensor cores (dk_dense.cu).  ta: A stored K x M;
 // tb: B stored N x K; tri 0/1/2 = all / lower / upper tiles; kshift (INT_MIN = off): B[k][j]
-// is structurally zero for k < j + kshift.
+// is structurally zero for k < j + kshift; kstop (INT_MIN = off): zero for k >= j + kstop
+// (rounded up to the CTA tile: tile column c0 stops its K loop at c0 + BN + kstop).
 void gemm_mma(bool ta, bool tb, const double* A, int lda, const double* B, int ldb, double* C,
               int ldc, int M, int N, int K, double alpha, double beta, int tri, int kshift,
-              cudaStream_t s);
+              cudaStream_t s, int kstop = INT_MIN);
 // Symmetric positive definite E (in L, overwritten): Cholesky, W = L^-1 (into W), then
 // E^-1 = W^T W written back into L (full).  *min_diag_sq = min L_kk^2 (NaN if not SPD); when
 // it is below 1e-280 the inverse is not formed and the caller falls back to LU.
 // form_inverse = false stops after W = L^-1 (W holds it, L the factor).
 int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
-                float* ms_inv, cudaStream_t s, bool form_inverse = true);
+                float* ms_inv, cudaStream_t s, bool form_inverse = true, bool clear_w = true);
+struct NDTreeNode;
+// W = L^-1 of an SPD E~ in nested-dissection order, node by node along the tree (W zeroed
+// on entry; E~'s separator blocks are overwritten).  *min_diag_sq as for spd_inverse.
+int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tree, double* W,
+                    double* min_diag_sq, cudaStream_t s);
 // X = W^T W (full, d x d) for lower-triangular W
 void lauum_into(const double* W, int d, int ld, double* X, cudaStream_t s);
 
 // ---- coarse solve through W = L^-1 in nested-dissection order (dk_profile.cu) ----
-constexpr int kTgGrid = 148, kTgWarps = 12;
 // a tile stream of k_tgemv: nt 32 x 32 tiles grouped by output block (trow ascending)
 struct TileGemv {
   const double* T = nullptr;   // [nt][16][32][2]
@@ -156,7 +162,7 @@ struct TileGemv {
   double* part = nullptr;      // [slots][32]
   unsigned* cnt = nullptr;     // arrival tickets per output block (reset by the last)
   long long nt = 0;
-  int nw = 0;                  // warps holding tiles (min(kTgGrid * kTgWarps, nt))
+  int nw = 0;                  // warps holding tiles (min(kTgGrid * warps per CTA, nt))
   int nrows = 0;
 };
 struct TileGemvHost {
@@ -168,9 +174,16 @@ struct TileGemvHost {
 // E's off-diagonal pattern (CSR, host)
 int coarse_pattern(const double* E, int d, int ld, std::vector<int>& ptr, std::vector<int>& col,
                    cudaStream_t s);
-// level-structure nested dissection of the pattern graph: perm[new] = old
+// a node of the dissection tree in the new order: subtree [t0, s1), separator [s0, s1)
+// (descendants [t0, s0) are the children's subtrees, which E does not couple)
+struct NDTreeNode {
+  int t0, s0, s1;
+  std::vector<int> kids;  // indices of the children (post-order: children come first)
+};
+// level-structure nested dissection of the pattern graph: perm[new] = old; the tree in
+// post-order (root last) when tree != nullptr
 void nd_order(int d, const std::vector<int>& ptr, const std::vector<int>& col,
-              std::vector<int>& perm);
+              std::vector<int>& perm, std::vector<NDTreeNode>* tree = nullptr);
 // 32 x 32 tiles of W's structural row profile under perm (upper bound of the stream)
 long long nd_profile_tiles(int d, const std::vector<int>& ptr, const std::vector<int>& col,
                            const std::vector<int>& perm);

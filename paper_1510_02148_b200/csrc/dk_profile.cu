@@ -17,6 +17,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <atomic>
+#include <future>
+#include <cstdlib>
 #include <vector>
 
 #include "dk_launch.h"
@@ -121,114 +125,95 @@ __global__ void k_tile_pack(const double* __restrict__ X, int d, int ld, const i
 
 // ---- the tile-sparse GEMV ------------------------------------------------------------
 // y_R = sum over the tiles t of output block R (in stream order) of T_t x_{col(t)}.
-// Each warp streams a contiguous, balanced range of tiles: one-lane TMA copies of the 8 KB
-// tile and its 256 B x segment complete on the stage's mbarrier; lane r owns row r, so the
-// row sum accumulates in a register across the warp's tiles of one output block.  A block
-// whose tiles span several warps is finished by the last of them to arrive (row ticket),
-// summing the pieces in warp order: deterministic.  With scatter, output row i goes to
-// y[scatter[i]] (back to the label order).
-constexpr int kTgStages = 2;
-constexpr int kTgStageBytes = kPTileBytes + kPSegBytes;
+// Each warp streams a contiguous, balanced range of tiles through KS shared-memory stages
+// filled by one-lane TMA bulk copies (8 KB, completion on the stage's mbarrier); lane r owns
+// row r, so the row sum accumulates in a register across the warp's tiles of one output
+// block.  Lane c holds x_{col(t)}[c] (read after the dependency wait, the first kXPre tiles'
+// segments prefetched at once) and broadcasts it by shuffle.  A block whose tiles span
+// several warps is finished by the last of them to arrive (row ticket), summing the pieces
+// in warp order: deterministic.  With scatter, output row i goes to y[scatter[i]].
+constexpr int kXPre = 8;
 
-// bulk copy on an mbarrier whose expect_tx the caller already posted; the tile streams are
-// read once per pass (evict-first), the x segments are reused (default policy)
-__device__ __forceinline__ void tma_copy_nx(void* dst, const void* src, unsigned bytes,
-                                            unsigned long long* bar, unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void tma_copy_x(void* dst, const void* src, unsigned bytes,
-                                           unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-// post the stage's byte count, then its tile and x segment
-__device__ __forceinline__ void tg_issue(unsigned char* b, const double* T, const double* xseg,
+// bulk copy of one tile on an mbarrier (evict-first: each tile is read once per pass)
+__device__ __forceinline__ void tg_issue(unsigned char* b, const double* T,
                                          unsigned long long* bar, unsigned long long pol) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"((unsigned)kTgStageBytes)
+               "r"((unsigned)kPTileBytes)
                : "memory");
-  tma_copy_nx(b, T, kPTileBytes, bar, pol);
-  tma_copy_x(b + kPTileBytes, xseg, kPSegBytes, bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(b)),
+      "l"(T), "r"((unsigned)kPTileBytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
 }
 
-__global__ void __launch_bounds__(kTgWarps * 32, 1) k_tgemv(TileGemv g, const double* __restrict__ x,
-                                                            double* __restrict__ y,
-                                                            const int* __restrict__ scatter, int d,
-                                                            const int* __restrict__ gate) {
+template <int KW, int KS>
+__global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* __restrict__ x,
+                                                      double* __restrict__ y,
+                                                      const int* __restrict__ scatter, int d,
+                                                      const int* __restrict__ gate) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) unsigned long long bars[kTgWarps][kTgStages];
+  __shared__ __align__(8) unsigned long long bars[KW][KS];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  unsigned char* wbuf = smem_raw + (size_t)wl * kTgStages * kTgStageBytes;
+  unsigned char* wbuf = smem_raw + (size_t)wl * KS * kPTileBytes;
   // g.nw <= nt warps hold the tiles, every one of them at least one
   const long long Wn = g.nw;
-  const long long w = (long long)blockIdx.x * kTgWarps + wl;
+  const long long w = (long long)blockIdx.x * KW + wl;
   const long long t0 = w < Wn ? w * g.nt / Wn : g.nt, t1 = w < Wn ? (w + 1) * g.nt / Wn : g.nt;
   const unsigned long long pol = l2_evict_first();
   if (lane == 0)
-    for (int s = 0; s < kTgStages; ++s) mbar_init1(&bars[wl][s]);
+    for (int s = 0; s < KS; ++s) mbar_init1(&bars[wl][s]);
   mbar_init_fence();
   __syncwarp();
   // The tiles and their metadata are set-up constants: fetched before the dependency wait,
   // so they stream in while the producer of x drains.  Lane k holds tile t0 + k's blocks.
-  const int nfirst = t1 - t0 < kTgStages ? (int)(t1 - t0) : kTgStages;
+  const int nfirst = t1 - t0 < KS ? (int)(t1 - t0) : KS;
   const int my_row = (t0 + lane < t1) ? g.trow[t0 + lane] : -1;
   const int my_col = (t0 + lane < t1) ? g.tcol[t0 + lane] : 0;
   if (lane == 0)
-    for (int s = 0; s < nfirst; ++s) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_addr(&bars[wl][s])),
-                   "r"((unsigned)kTgStageBytes)
-                   : "memory");
-      tma_copy_nx(wbuf + s * kTgStageBytes, g.T + (t0 + s) * (kPT * kPT), kPTileBytes,
-                  &bars[wl][s], pol);
-    }
+    for (int s = 0; s < nfirst; ++s)
+      tg_issue(wbuf + s * kPTileBytes, g.T + (t0 + s) * (kPT * kPT), &bars[wl][s], pol);
   pdl_wait();
   const bool off = gate != nullptr && *gate == 0;
-  for (int s = 0; s < nfirst; ++s) {
-    const int c = __shfl_sync(0xffffffffu, my_col, s);
-    if (lane == 0)
-      tma_copy_x(wbuf + s * kTgStageBytes + kPTileBytes, x + (long long)c * kPT, kPSegBytes,
-                 &bars[wl][s]);
-  }
-  if (off) {  // drain the copies already in flight, then leave
+  if (off || t0 >= t1) {  // drain the copies already in flight, then leave
     for (int s = 0; s < nfirst; ++s) mbar_wait_parity(&bars[wl][s], 0);
     return;
   }
-  if (t0 >= t1) return;
+  double xr[kXPre];
+#pragma unroll
+  for (int k = 0; k < kXPre; ++k) {
+    const int c = __shfl_sync(0xffffffffu, my_col, k);
+    xr[k] = (t0 + k < t1) ? __ldcg(x + (long long)c * kPT + lane) : 0.0;
+  }
   int R = __shfl_sync(0xffffffffu, my_row, 0);
   double racc = 0.0;
   for (long long t = t0; t < t1; ++t) {
     const int k = (int)(t - t0);
-    const int s = k % kTgStages;
-    const unsigned parity = (unsigned)((k / kTgStages) & 1);
-    // metadata of tile t + kTgStages (refill) and t + 1 (block change)
-    const int kr = k + kTgStages, kn = k + 1;
-    const int col_r = kr < 32 ? __shfl_sync(0xffffffffu, my_col, kr & 31)
-                              : (t + kTgStages < t1 ? g.tcol[t + kTgStages] : 0);
+    const int s = k % KS;
+    const unsigned parity = (unsigned)((k / KS) & 1);
+    const int kn = k + 1;
     const int row_n = kn < 32 ? __shfl_sync(0xffffffffu, my_row, kn & 31)
                               : (t + 1 < t1 ? g.trow[t + 1] : -1);
+    double xv = 0.0;
+#pragma unroll
+    for (int q = 0; q < kXPre; ++q)
+      if (q == k) xv = xr[q];
+    if (k >= kXPre) {
+      const int c = k < 32 ? __shfl_sync(0xffffffffu, my_col, k & 31) : g.tcol[t];
+      xv = __ldcg(x + (long long)c * kPT + lane);
+    }
     mbar_wait_parity(&bars[wl][s], parity);
-    const unsigned char* b = wbuf + s * kTgStageBytes;
-    const double2* T = reinterpret_cast<const double2*>(b);
-    const double2* xs = reinterpret_cast<const double2*>(b + kPTileBytes);
+    const double2* T = reinterpret_cast<const double2*>(wbuf + s * kPTileBytes);
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
-      const double2 a = T[p * kPT + lane], xx = xs[p];
-      racc = fma(a.x, xx.x, racc);
-      racc = fma(a.y, xx.y, racc);
+      const double2 a = T[p * kPT + lane];
+      racc = fma(a.x, __shfl_sync(0xffffffffu, xv, 2 * p), racc);
+      racc = fma(a.y, __shfl_sync(0xffffffffu, xv, 2 * p + 1), racc);
     }
     __syncwarp();
-    if (lane == 0 && t + kTgStages < t1)  // refill this stage
-      tg_issue(wbuf + s * kTgStageBytes, g.T + (t + kTgStages) * (kPT * kPT),
-               x + (long long)col_r * kPT, &bars[wl][s], pol);
+    if (lane == 0 && t + KS < t1)  // refill this stage
+      tg_issue(wbuf + s * kPTileBytes, g.T + (t + KS) * (kPT * kPT), &bars[wl][s], pol);
     const int Rn = (t + 1 < t1) ? row_n : -1;
     if (Rn == R) continue;
     // output block R ends in this warp's range
@@ -261,23 +246,39 @@ __global__ void __launch_bounds__(kTgWarps * 32, 1) k_tgemv(TileGemv g, const do
   }
 }
 
+}  // namespace
+
 // ---- host: level-structure nested dissection -----------------------------------------
+// George's automatic nested dissection: a BFS level structure from a pseudo-peripheral node
+// (two sweeps), the separator = the vertices of the smallest level with 25-75 % of the nodes
+// on either side that touch the next level, recursion on both sides (independent halves in
+// parallel near the root), separator last.  Emits the order and the dissection tree.
+namespace {
+
+struct NDNode {
+  int t0, s0, s1;       // subtree [t0, s1): descendants [t0, s0), separator [s0, s1)
+  std::vector<int> kids;
+};
+
+struct NDPart {
+  std::vector<int> order;
+  std::vector<NDNode> nodes;  // post-order; the last is this part's root
+};
+
 struct NestedDissection {
   const std::vector<int>& ptr;
   const std::vector<int>& col;
-  std::vector<int> part, level, order, seen;
-  int next_id = 2;
+  std::vector<int> part, level;
+  std::atomic<int> next_id{2};
   int leaf;
 
   NestedDissection(int d, const std::vector<int>& p, const std::vector<int>& c, int lf)
-      : ptr(p), col(c), part(d, 1), level(d, -1), leaf(lf) {
-    order.reserve(d);
-  }
+      : ptr(p), col(c), part(d, 1), level(d, -1), leaf(lf) {}
 
   int deg(int v) const { return ptr[v + 1] - ptr[v]; }
 
-  // BFS from src inside part pid; levels set, visit order in `seen`
-  void bfs(int src, int pid) {
+  // BFS from src inside part pid (levels must be -1 on the part's nodes)
+  void bfs(int src, int pid, std::vector<int>& seen) {
     seen.clear();
     level[src] = 0;
     seen.push_back(src);
@@ -293,63 +294,81 @@ struct NestedDissection {
     }
   }
 
-  void emit_sorted(std::vector<int>& nodes) {
+  // a leaf: every node in the separator, natural order
+  static void leaf_node(std::vector<int>& nodes, int base, NDPart& out) {
     std::sort(nodes.begin(), nodes.end());
-    for (int v : nodes) {
-      part[v] = 0;
-      order.push_back(v);
-    }
+    out.order.insert(out.order.end(), nodes.begin(), nodes.end());
+    out.nodes.push_back({base, base, base + (int)nodes.size(), {}});
   }
 
-  void rec(std::vector<int> nodes, int pid) {
-    if ((int)nodes.size() <= leaf) {
-      emit_sorted(nodes);
-      return;
+  // splice a child's nodes (renumbered) into out and register its root under `parent`
+  static void append(NDPart& out, NDPart& sub, NDNode& parent) {
+    const int off = (int)out.nodes.size();
+    out.order.insert(out.order.end(), sub.order.begin(), sub.order.end());
+    for (auto& nd : sub.nodes) {
+      for (int& k : nd.kids) k += off;
+      out.nodes.push_back(std::move(nd));
     }
-    std::sort(nodes.begin(), nodes.end());
+    parent.kids.push_back((int)out.nodes.size() - 1);
+  }
+
+  // order `nodes` (all in part pid) into positions [base, base + n)
+  NDPart rec(std::vector<int> nodes, int pid, int base, int depth) {
+    NDPart out;
+    const int n = (int)nodes.size();
+    if (n <= leaf) {
+      for (int v : nodes) part[v] = 0;
+      leaf_node(nodes, base, out);
+      return out;
+    }
     for (int v : nodes) level[v] = -1;
-    std::vector<std::vector<int>> comps;
+    int src = nodes[0];
     for (int v : nodes)
-      if (level[v] < 0) {
-        bfs(v, pid);
-        comps.push_back(seen);
-      }
-    if (comps.size() > 1) {
+      if (deg(v) < deg(src)) src = v;
+    std::vector<int> seen;
+    bfs(src, pid, seen);
+    if ((int)seen.size() < n) {
+      // several components: each is a child, no separator
+      std::vector<std::vector<int>> comps;
+      comps.push_back(seen);
+      for (int v : nodes)
+        if (level[v] < 0) {
+          bfs(v, pid, seen);
+          comps.push_back(seen);
+        }
       std::vector<int> ids;
       for (auto& c : comps) {
         const int id = next_id++;
         ids.push_back(id);
         for (int v : c) part[v] = id;
       }
-      for (size_t i = 0; i < comps.size(); ++i) rec(std::move(comps[i]), ids[i]);
-      return;
+      NDNode root{base, base + n, base + n, {}};
+      int b = base;
+      for (size_t i = 0; i < comps.size(); ++i) {
+        const int sz = (int)comps[i].size();
+        NDPart sub = rec(std::move(comps[i]), ids[i], b, depth + 1);
+        append(out, sub, root);
+        b += sz;
+      }
+      out.nodes.push_back(std::move(root));
+      return out;
     }
-    std::vector<int>& comp = comps[0];
-    // pseudo-peripheral start: repeated BFS from a minimum-degree node of the last level
-    int src = comp[0];
-    for (int v : comp)
-      if (deg(v) < deg(src)) src = v;
-    int ecc = -1;
-    for (;;) {
-      for (int v : comp) level[v] = -1;
-      bfs(src, pid);
+    // second sweep from a minimum-degree node of the last level
+    {
       const int e = level[seen.back()];
-      if (e <= ecc) break;
-      ecc = e;
       int best = -1;
       for (int i = (int)seen.size() - 1; i >= 0 && level[seen[i]] == e; --i)
         if (best < 0 || deg(seen[i]) < deg(best)) best = seen[i];
-      src = best;
+      for (int v : seen) level[v] = -1;
+      bfs(best, pid, seen);
     }
     const int nl = level[seen.back()] + 1;
-    const long long n = (long long)seen.size();
     std::vector<long long> cnt(nl, 0), cum(nl, 0);
     for (int v : seen) ++cnt[level[v]];
     for (int l = 0; l < nl; ++l) cum[l] = cnt[l] + (l ? cum[l - 1] : 0);
-    // the separator level: smallest level with 25-75 % of the nodes on either side
     int L = -1;
     for (int l = 1; l + 1 < nl; ++l)
-      if (4 * cum[l - 1] >= n && 4 * cum[l] <= 3 * n && (L < 0 || cnt[l] < cnt[L])) L = l;
+      if (4 * cum[l - 1] >= n && 4 * cum[l] <= 3LL * n && (L < 0 || cnt[l] < cnt[L])) L = l;
     if (L < 0) {
       L = 0;
       while (L < nl - 1 && 2 * cum[L] < n) ++L;
@@ -367,51 +386,79 @@ struct NestedDissection {
         A.push_back(v);
       }
     }
-    if (A.empty() || B.empty()) {
-      emit_sorted(comp);
-      return;
+    if (A.empty() || B.empty()) {  // no useful split: one dense node
+      for (int v : nodes) part[v] = 0;
+      leaf_node(nodes, base, out);
+      return out;
     }
     const int ida = next_id++, idb = next_id++;
     for (int v : A) part[v] = ida;
     for (int v : B) part[v] = idb;
     for (int v : sep) part[v] = 0;
-    rec(std::move(A), ida);
-    rec(std::move(B), idb);
-    for (int v : sep) order.push_back(v);
+    const int na = (int)A.size(), nb = (int)B.size();
+    NDPart pa, pb;
+    if (depth < 4 && n > 2048) {  // independent halves, disjoint nodes: in parallel
+      auto fa = std::async(std::launch::async,
+                           [&] { return rec(std::move(A), ida, base, depth + 1); });
+      pb = rec(std::move(B), idb, base + na, depth + 1);
+      pa = fa.get();
+    } else {
+      pa = rec(std::move(A), ida, base, depth + 1);
+      pb = rec(std::move(B), idb, base + na, depth + 1);
+    }
+    NDNode root{base, base + na + nb, base + n, {}};
+    append(out, pa, root);
+    append(out, pb, root);
+    out.order.insert(out.order.end(), sep.begin(), sep.end());
+    out.nodes.push_back(std::move(root));
+    return out;
   }
 };
 
 }  // namespace
 
 void nd_order(int d, const std::vector<int>& ptr, const std::vector<int>& col,
-              std::vector<int>& perm) {
+              std::vector<int>& perm, std::vector<NDTreeNode>* tree) {
   NestedDissection nd(d, ptr, col, 64);
   std::vector<int> all(d);
   for (int i = 0; i < d; ++i) all[i] = i;
-  nd.rec(std::move(all), 1);
-  perm.swap(nd.order);
+  NDPart p = nd.rec(std::move(all), 1, 0, 0);
+  perm.swap(p.order);
+  if (tree) {
+    tree->clear();
+    for (auto& n : p.nodes) tree->push_back({n.t0, n.s0, n.s1, n.kids});
+  }
 }
 
 long long nd_profile_tiles(int d, const std::vector<int>& ptr, const std::vector<int>& col,
                            const std::vector<int>& perm) {
-  // the row profile f of E~, closed under W = L^-1: g(i) = min(f(i), min_{f(i)<=k<i} g(k)),
-  // evaluated with a sparse-table-free sweep (g is checked over the range once per row)
-  std::vector<int> inv(d), f(d), g(d);
+  // the row profile f of E~ closed under W = L^-1: g(i) = min(f(i), min_{f(i)<=k<i} g(k))
+  // (range minimum by a segment tree), counted in 32 x 32 tiles
+  std::vector<int> inv(d), f(d);
   for (int i = 0; i < d; ++i) inv[perm[i]] = i;
   for (int i = 0; i < d; ++i) f[i] = i;
   for (int v = 0; v < d; ++v)
     for (int k = ptr[v]; k < ptr[v + 1]; ++k) f[inv[v]] = std::min(f[inv[v]], inv[col[k]]);
-  // block-level closure is enough for a tile count: gb(I) = min over I's rows
+  int sz = 1;
+  while (sz < d) sz <<= 1;
+  std::vector<int> seg(2 * sz, 1 << 30);
+  auto query = [&](int lo, int hi) {  // min over [lo, hi)
+    int m = 1 << 30;
+    for (lo += sz, hi += sz; lo < hi; lo >>= 1, hi >>= 1) {
+      if (lo & 1) m = std::min(m, seg[lo++]);
+      if (hi & 1) m = std::min(m, seg[--hi]);
+    }
+    return m;
+  };
   const int nb = (d + kPT - 1) / kPT;
-  std::vector<int> fb(nb, 1 << 30), gb(nb);
-  for (int i = 0; i < d; ++i) fb[i / kPT] = std::min(fb[i / kPT], f[i] / kPT);
-  long long tiles = 0;
-  for (int I = 0; I < nb; ++I) {
-    int m = fb[I];
-    for (int K = fb[I]; K < I; ++K) m = std::min(m, gb[K]);
-    gb[I] = m;
-    tiles += I - m + 1;
+  std::vector<int> gb(nb, 1 << 30);
+  for (int i = 0; i < d; ++i) {
+    const int g = f[i] < i ? std::min(f[i], query(f[i], i)) : f[i];
+    for (int p = i + sz; p >= 1; p >>= 1) seg[p] = std::min(seg[p], g);
+    gb[i / kPT] = std::min(gb[i / kPT], g / kPT);
   }
+  long long tiles = 0;
+  for (int I = 0; I < nb; ++I) tiles += I - gb[I] + 1;
   return tiles;
 }
 
@@ -452,6 +499,9 @@ void launch_unpermute_sym(const double* X, int d, int ld, const int* perm, doubl
   k_unpermute_sym<<<148 * 8, 256, 0, s>>>(X, d, ld, perm, out, ldo);
 }
 
+int tgemv_warps_per_cta();
+int tg_grid();
+
 // Nonzero tiles of W (lower triangle, row profile fW from k_row_first_nz) as two streams:
 // pass 1 by block rows of W (t = W s~), pass 2 by block columns of W, tiles transposed
 // (y~ = W^T t).  Host metadata for the row tickets of k_tgemv.
@@ -467,7 +517,7 @@ static int build_stream(const std::vector<int>& ti, const std::vector<int>& tj, 
   std::vector<long long> rs(nrows + 1, 0);
   for (long long t = 0; t < nt; ++t) ++rs[ti[t] + 1];
   for (int R = 0; R < nrows; ++R) rs[R + 1] += rs[R];
-  const long long Wn = std::min<long long>((long long)kTgGrid * kTgWarps, nt);
+  const long long Wn = std::min<long long>((long long)tg_grid() * tgemv_warps_per_cta(), nt);
   h.nw = (int)Wn;
   auto warp_of = [&](long long t) {  // the warp whose range [w nt / Wn, (w+1) nt / Wn) holds t
     long long w = (t * Wn) / nt;
@@ -577,16 +627,51 @@ void free_stream(TileGemv& g, cudaStream_t s) {
   g.cnt = nullptr;
 }
 
-void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
-                  const int* gate, cudaStream_t s) {
-  const size_t smem = (size_t)kTgWarps * kTgStages * kTgStageBytes;
+// (warps per CTA, stages per warp) of k_tgemv; DK_TG_CFG picks one (set-up and launch agree)
+static const int kTgCfg[][2] = {{12, 2}, {16, 1}, {8, 3}, {4, 6}, {16, 2}, {8, 6}};
+int tgemv_cfg() {
+  static int c = -1;
+  if (c < 0) {
+    const char* e = getenv("DK_TG_CFG");
+    c = e ? atoi(e) : 0;
+    if (c < 0 || c > 5) c = 0;
+  }
+  return c;
+}
+int tgemv_warps_per_cta() { return kTgCfg[tgemv_cfg()][0]; }
+
+// SMs of the current device (the tile streams are split over tg_grid() CTAs)
+int tg_grid() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!n[dev & 63]) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev & 63];
+}
+
+template <int KW, int KS>
+static void launch_tg(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
+                      const int* gate, cudaStream_t s) {
+  const size_t smem = (size_t)KW * KS * kPTileBytes;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_tgemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_tgemv<KW, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const unsigned grid = (unsigned)((g.nw + kTgWarps - 1) / kTgWarps);
-  launch_pdl(k_tgemv, dim3(grid), dim3(kTgWarps * 32), smem, s, g, x, y, scatter, d, gate);
+  const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
+  launch_pdl(k_tgemv<KW, KS>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d, gate);
+}
+
+void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
+                  const int* gate, cudaStream_t s) {
+  switch (tgemv_cfg()) {
+    case 1: launch_tg<16, 1>(g, x, y, scatter, d, gate, s); break;
+    case 2: launch_tg<8, 3>(g, x, y, scatter, d, gate, s); break;
+    case 3: launch_tg<4, 6>(g, x, y, scatter, d, gate, s); break;
+    case 4: launch_tg<16, 2>(g, x, y, scatter, d, gate, s); break;
+    case 5: launch_tg<8, 6>(g, x, y, scatter, d, gate, s); break;
+    default: launch_tg<12, 2>(g, x, y, scatter, d, gate, s); break;
+  }
 }
 
 }  // namespace dk

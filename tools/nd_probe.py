@@ -231,3 +231,41 @@ def main2():
 if __name__ == "__main__":
     main()
     main2()
+
+
+def flops(ptr, col, perm):
+    d = len(perm)
+    inv = np.empty(d, np.int64)
+    inv[perm] = np.arange(d)
+    f = np.arange(d)
+    for v in range(d):
+        nb = col[ptr[v]:ptr[v + 1]]
+        if len(nb):
+            f[inv[v]] = min(f[inv[v]], inv[nb].min())
+    g = f.copy()
+    for i in range(d):
+        if f[i] < i:
+            g[i] = min(f[i], g[f[i]:i].min())
+    out = []
+    for prof in (f, g):
+        # column counts: rows i >= j with prof(i) <= j
+        cnt = np.zeros(d + 1, np.int64)
+        np.add.at(cnt, prof, 1)
+        np.add.at(cnt, np.arange(1, d + 1), -1)
+        cc = np.cumsum(cnt)[:d]
+        out.append(float((cc.astype(float) ** 2).sum()))
+    return out
+
+
+if __name__ == "__main__" and len(sys.argv) > 2:
+    c = configs.make_case(int(sys.argv[1]))
+    px, py, pz = c.boxes
+    part = dk.subdomain_levelset_partition(c.band_field, px, py, pz, c.jump_threshold,
+                                           backend="host")
+    lab = np.asarray(part.labels)
+    ptr, col = adjacency(c.grid, lab, part.d)
+    perm = graph_nd(ptr, col, 64)
+    fl, fw = flops(ptr, col, perm)
+    d = part.d
+    print(f"d={d} chol flops (envelope) {fl/1e9:.1f} GF, W flops ~{fw/1e9:.1f} GF; dense d^3/3 "
+          f"{d**3/3/1e9:.0f} GF")
