@@ -14,7 +14,8 @@ import numpy as np
 
 from .errors import SingularCoarseMatrix
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdk.so"
+LIB_PATH = Path(os.environ.get("DK_LIB_PATH") or
+                Path(__file__).resolve().parent / "_lib" / "libdk.so")  # override: experiments
 
 DK_OK, DK_EINVAL, DK_ESINGULAR, DK_ECUDA, DK_EUNSUPPORTED = 0, 1, 2, 3, 4
 DK_AP_A, DK_AP_AM = 0, 1

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include "dk_launch.h"
 
@@ -106,6 +107,48 @@ __device__ void tile_restrict(const double* sw, const int* sl, double* out,
     const bool is_tail = (e < 7) ? ((heads >> (e + 1)) & 1u) != 0
                                  : (c0 + 8 >= kTile || next != lb[7]);
     if (is_tail) out[__ldg(slot + ridx)] = run;
+  }
+}
+
+// Run sums of a stencil tile's outputs rr (8 per thread: cells 2t + 512k, +1) with labels lb.
+__device__ __forceinline__ void stencil_restrict_tail(const double (&rr)[8], const int2 (&lb)[4],
+                                                      double* sw, int* sl, double* wsum,
+                                                      const int* __restrict__ tile_run_off,
+                                                      const int* __restrict__ run_slot,
+                                                      double* __restrict__ run_part) {
+  constexpr bool RESTRICT = true;  // (the body is shared by both stencil kernels)
+  // a tile inside one region is a single run: plain block sum instead of the segmented scan
+  const bool one_run =
+      RESTRICT && (tile_run_off[blockIdx.x + 1] - tile_run_off[blockIdx.x] == 1);
+  double tsum = 0.0;
+  if (RESTRICT) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (one_run) {
+        tsum = __dadd_rn(tsum, __dadd_rn(rr[2 * k], rr[2 * k + 1]));
+      } else {
+        const int p = pidx(2 * threadIdx.x + 512 * k);
+        sw[p] = rr[2 * k];
+        sw[p + 1] = rr[2 * k + 1];
+        sl[p] = lb[k].x;
+        sl[p + 1] = lb[k].y;
+      }
+    }
+  }
+  if (RESTRICT) {
+    if (one_run) {
+      tsum = warp_sum(tsum);
+      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tsum;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
+        run_part[run_slot[tile_run_off[blockIdx.x]]] = s;
+      }
+    } else {
+      __syncthreads();
+      tile_restrict(sw, sl, run_part, run_slot + tile_run_off[blockIdx.x]);
+    }
   }
 }
 
@@ -221,39 +264,162 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
     rr[2 * k + 1] = r1;
     if (RESTRICT) lb[k] = *reinterpret_cast<const int2*>(lab + i);
   }
-  // a tile inside one region is a single run: plain block sum instead of the segmented scan
-  const bool one_run =
-      RESTRICT && (tile_run_off[blockIdx.x + 1] - tile_run_off[blockIdx.x] == 1);
-  double tsum = 0.0;
-  if (RESTRICT) {
+  if (RESTRICT) stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+}
+
+// K1 for the symmetric 7-point operator (TPFA; DIA offsets -nxny, -nx, -1, 0, 1, nx, nxny,
+// arrays c0, u1, ux, uz for the centre and the positive diagonals, nx and nxny even): the
+// same arithmetic as k_stencil<ST_APPLY> (same products, same ascending-offset order), with
+// every global load of a pair of cells known up front.  The coefficient and z-neighbour loads
+// of the thread's first two pairs are issued before the tile's input p = (sigma v) M^-1 is
+// staged in shared memory (halo H >= nx + 2), the next two while the first are computed.
+struct Sym7Pair {
+  double2 c, u1, u1m, ux, uxm, uz, uzm, vm, vp, im, ip;
+};
+
+template <bool PRE>
+__device__ __forceinline__ void sym7_load(Sym7Pair& q, const Dia& A, const double* __restrict__ v,
+                                          long long i, long long nx, long long nz) {
+  q.c = ld2(A.co[3] + i);
+  q.u1 = ld2(A.co[4] + i);
+  q.u1m = ld2(A.co[4] + i - 2);
+  q.ux = ld2(A.co[5] + i);
+  q.uxm = ld2(A.co[5] + i - nx);
+  q.uz = ld2(A.co[6] + i);
+  q.uzm = ld2(A.co[6] + i - nz);
+  q.vm = ld2(v + i - nz);
+  q.vp = ld2(v + i + nz);
+  if (PRE) {
+    q.im = ld2(A.inv + i - nz);
+    q.ip = ld2(A.inv + i + nz);
+  }
+}
+
+__device__ __forceinline__ double sym7_x(double x, double sc, bool has_scale, bool pre, double m) {
+  if (has_scale) x = __dmul_rn(x, sc);
+  if (pre) x = __dmul_rn(x, m);
+  return x;
+}
+
+template <bool PRE>
+__device__ __forceinline__ double2 sym7_apply(const Sym7Pair& q, const double* pp, long long nx,
+                                              double sc, bool has_scale) {
+  // pp = staged p at cell i;  cell i: coefficients uzm.x uxm.x u1m.y c.x u1.x ux.x uz.x,
+  // cell i+1: uzm.y uxm.y u1.x c.y u1.y ux.y uz.y
+  const double zm0 = sym7_x(q.vm.x, sc, has_scale, PRE, PRE ? q.im.x : 1.0);
+  const double zm1 = sym7_x(q.vm.y, sc, has_scale, PRE, PRE ? q.im.y : 1.0);
+  const double zp0 = sym7_x(q.vp.x, sc, has_scale, PRE, PRE ? q.ip.x : 1.0);
+  const double zp1 = sym7_x(q.vp.y, sc, has_scale, PRE, PRE ? q.ip.y : 1.0);
+  double r0 = __dmul_rn(q.uzm.x, zm0);
+  r0 = __dadd_rn(r0, __dmul_rn(q.uxm.x, pp[-nx]));
+  r0 = __dadd_rn(r0, __dmul_rn(q.u1m.y, pp[-1]));
+  r0 = __dadd_rn(r0, __dmul_rn(q.c.x, pp[0]));
+  r0 = __dadd_rn(r0, __dmul_rn(q.u1.x, pp[1]));
+  r0 = __dadd_rn(r0, __dmul_rn(q.ux.x, pp[nx]));
+  r0 = __dadd_rn(r0, __dmul_rn(q.uz.x, zp0));
+  double r1 = __dmul_rn(q.uzm.y, zm1);
+  r1 = __dadd_rn(r1, __dmul_rn(q.uxm.y, pp[1 - nx]));
+  r1 = __dadd_rn(r1, __dmul_rn(q.u1.x, pp[0]));
+  r1 = __dadd_rn(r1, __dmul_rn(q.c.y, pp[1]));
+  r1 = __dadd_rn(r1, __dmul_rn(q.u1.y, pp[2]));
+  r1 = __dadd_rn(r1, __dmul_rn(q.ux.y, pp[1 + nx]));
+  r1 = __dadd_rn(r1, __dmul_rn(q.uz.y, zp1));
+  return make_double2(r0, r1);
+}
+
+template <bool PRE, bool RESTRICT, bool WRITE>
+__global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const double* __restrict__ v,
+                                                           const double* __restrict__ scale,
+                                                           double* __restrict__ out,
+                                                           const int* __restrict__ lab,
+                                                           const int* __restrict__ tile_run_off,
+                                                           const int* __restrict__ run_slot,
+                                                           double* __restrict__ run_part,
+                                                           const int* __restrict__ gate, int H) {
+  pdl_wait();
+  if (gate != nullptr && *gate == 0) return;
+  extern __shared__ __align__(16) double sp[];  // [H | kTile | H]
+  __shared__ double sw[RESTRICT ? kTilePad : 2];
+  __shared__ int sl[RESTRICT ? kTilePad : 2];
+  __shared__ double wsum[kWarps];
+  const long long base = (long long)blockIdx.x * kTile;
+  const long long nx = A.off[5], nz = A.off[6];
+  const bool has_scale = scale != nullptr;
+  const double sc = has_scale ? *scale : 1.0;
+  Sym7Pair q0, q1;
+  sym7_load<PRE>(q0, A, v, base + 2 * threadIdx.x, nx, nz);
+  sym7_load<PRE>(q1, A, v, base + 2 * threadIdx.x + 512, nx, nz);
+  for (int e = threadIdx.x; e < (kTile + 2 * H) / 2; e += kThreads) {
+    const long long i = base - H + 2 * e;
+    double2 x = ld2(v + i);
+    if (has_scale) {
+      x.x = __dmul_rn(x.x, sc);
+      x.y = __dmul_rn(x.y, sc);
+    }
+    if (PRE) {
+      const double2 m = ld2(A.inv + i);
+      x.x = __dmul_rn(x.x, m.x);
+      x.y = __dmul_rn(x.y, m.y);
+    }
+    reinterpret_cast<double2*>(sp)[e] = x;
+  }
+  int2 lb[4];
+  if (RESTRICT)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (one_run) {
-        tsum = __dadd_rn(tsum, __dadd_rn(rr[2 * k], rr[2 * k + 1]));
-      } else {
-        const int p = pidx(2 * threadIdx.x + 512 * k);
-        sw[p] = rr[2 * k];
-        sw[p + 1] = rr[2 * k + 1];
-        sl[p] = lb[k].x;
-        sl[p + 1] = lb[k].y;
-      }
-    }
+    for (int k = 0; k < 4; ++k)
+      lb[k] = *reinterpret_cast<const int2*>(lab + base + 2 * threadIdx.x + 512 * k);
+  __syncthreads();
+  double rr[8];
+  const double* pp = sp + H + 2 * threadIdx.x;
+  double2 r = sym7_apply<PRE>(q0, pp, nx, sc, has_scale);
+  rr[0] = r.x;
+  rr[1] = r.y;
+  sym7_load<PRE>(q0, A, v, base + 2 * threadIdx.x + 1024, nx, nz);
+  r = sym7_apply<PRE>(q1, pp + 512, nx, sc, has_scale);
+  rr[2] = r.x;
+  rr[3] = r.y;
+  sym7_load<PRE>(q1, A, v, base + 2 * threadIdx.x + 1536, nx, nz);
+  r = sym7_apply<PRE>(q0, pp + 1024, nx, sc, has_scale);
+  rr[4] = r.x;
+  rr[5] = r.y;
+  r = sym7_apply<PRE>(q1, pp + 1536, nx, sc, has_scale);
+  rr[6] = r.x;
+  rr[7] = r.y;
+  if (WRITE)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      st2(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
+  if (RESTRICT)
+    stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+}
+
+// halo of k_stencil_sym7, or 0 when the operator is not the symmetric even 7-point stencil
+static int sym7_halo(const Dia& A) {
+  if (A.ndiag != 7 || A.center != 3 || A.off[3] != 0 || A.off[4] != 1) return 0;
+  const long long nx = A.off[5], nz = A.off[6];
+  if (A.off[2] != -1 || A.off[1] != -nx || A.off[0] != -nz) return 0;
+  if ((nx & 1) || (nz & 1) || nx + 2 > 4096) return 0;
+  if (A.co[0] != A.co[6] || A.co[1] != A.co[5] || A.co[2] != A.co[4]) return 0;
+  if (A.csh[0] != -nz || A.csh[1] != -nx || A.csh[2] != -1) return 0;
+  for (int q = 3; q < 7; ++q)
+    if (A.csh[q] != 0) return 0;
+  return (int)((nx + 2 + 31) / 32 * 32);
+}
+
+template <bool PRE, bool R, bool W>
+static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, const double* scale,
+                       double* out, const RunMap* rm, const int* gate, cudaStream_t s) {
+  const unsigned grid = (unsigned)(n_pad / kTile);
+  const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(k_stencil_sym7<PRE, R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = smem;
   }
-  if (RESTRICT) {
-    if (one_run) {
-      tsum = warp_sum(tsum);
-      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tsum;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
-        run_part[run_slot[tile_run_off[blockIdx.x]]] = s;
-      }
-    } else {
-      __syncthreads();
-      tile_restrict(sw, sl, run_part, run_slot + tile_run_off[blockIdx.x]);
-    }
-  }
+  launch_pdl(k_stencil_sym7<PRE, R, W>, dim3(grid), dim3(kThreads), smem, s, A, v, scale, out,
+             rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H);
 }
 
 template <int MODE, bool PRE, bool R, bool W>
@@ -281,6 +447,16 @@ static void stencil_rw(bool write, const Dia& A, long long n_pad, const double* 
 void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
                     const double* scale, const double* b, double* out, const RunMap* rm,
                     const int* gate, cudaStream_t s) {
+  const int H = (mode == ST_APPLY && !getenv("DK_GENERIC_STENCIL")) ? sym7_halo(A) : 0;
+  if (H > 0) {
+    if (pre && rm && write) stencil7_t<true, true, true>(A, H, n_pad, v, scale, out, rm, gate, s);
+    else if (pre && rm) stencil7_t<true, true, false>(A, H, n_pad, v, scale, out, rm, gate, s);
+    else if (pre) stencil7_t<true, false, true>(A, H, n_pad, v, scale, out, rm, gate, s);
+    else if (rm && write) stencil7_t<false, true, true>(A, H, n_pad, v, scale, out, rm, gate, s);
+    else if (rm) stencil7_t<false, true, false>(A, H, n_pad, v, scale, out, rm, gate, s);
+    else stencil7_t<false, false, true>(A, H, n_pad, v, scale, out, rm, gate, s);
+    return;
+  }
   if (mode == ST_IDENT) {
     stencil_rw<ST_IDENT, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
   } else if (mode == ST_RESID) {
@@ -309,22 +485,33 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
     // one thread per column with at most kShortRuns runs, serial in run order
     const int L = blockIdx.x * blockDim.x + threadIdx.x;
     if (L >= d) return;
-    const int lo = ptr[L], hi = ptr[L + 1];
-    if (hi - lo > kShortRuns) return;
+    const int lo = ptr[L], len = ptr[L + 1] - lo;
+    if (len > kShortRuns) return;
+    double v[kShortRuns];  // every load in flight, then the in-order sum
+#pragma unroll
+    for (int k = 0; k < kShortRuns; ++k) v[k] = k < len ? __ldcg(run_part + lo + k) : 0.0;
     double acc = 0.0;
-#pragma unroll 4
-    for (int k = lo; k < hi; ++k) acc += __ldcg(run_part + k);
+#pragma unroll
+    for (int k = 0; k < kShortRuns; ++k)
+      if (k < len) acc += v[k];
     s[s_pos ? s_pos[L] : L] = acc;
     return;
   }
-  // one warp per long column (lane-strided, fixed xor tree)
+  // one warp per long column (lane-strided, eight loads per lane in flight, fixed xor tree)
   const int wl = ((blockIdx.x - short_blocks) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wl >= nlong) return;
   const int L = long_ids[wl];
   double acc = 0.0;
   const int lo = ptr[L], hi = ptr[L + 1];
-  for (int k = lo + lane; k < hi; k += 32) acc += __ldcg(run_part + k);
+  for (int k0 = lo + lane; k0 < hi; k0 += 32 * 8) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = k0 + 32 * i < hi ? __ldcg(run_part + k0 + 32 * i) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (k0 + 32 * i < hi) acc += v[i];
+  }
   acc = warp_sum(acc);
   if (lane == 0) s[s_pos ? s_pos[L] : L] = acc;
 }
