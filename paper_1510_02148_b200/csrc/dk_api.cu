@@ -154,6 +154,8 @@ struct dk_defl {
   double* qv_base = nullptr;
   double* own_base = nullptr;           // compact prolongation (k_prolong_setup)
   unsigned char* mask_base = nullptr;
+  int2* flab_base = nullptr;            // first two foreign labels per cell
+  double2* fco_base = nullptr;          // and their summed coefficients
   Prolong pro{};
   // symmetric coarse solve (E symmetric): packed upper tile triangle of E^-1 + partials
   int sym = 0;
@@ -174,7 +176,7 @@ struct dk_defl {
   TileGemv tg1{}, tg2{};
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
-  double nmasked = 0;  // foreign-label coefficients of the prolongation (byte accounting)
+  double nmasked = 0;  // masked (third+ foreign label) coefficients (byte accounting)
   // dense basis (non-indicator Z, d <= kDenseMaxD): rows Z_k and A_p Z_k, guarded like V
   int dense = 0;
   double* Z_base = nullptr;
@@ -524,7 +526,7 @@ void issue_restart(dk_op* op, dk_defl* c) {
   // w in/out; with deflation the compact prolongation: labels 4, own 8, mask 1 per cell and
   // one coefficient + label (+ M^-1 for A_p = AM) per foreign-label entry; dense: A_p Z rows
   const double pro_bytes = !c ? 0.0 : c->dense ? 8.0 * c->d * n
-                                               : 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
+                                               : 37.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
   ProfScope ps(op, PC_RESTART, 16.0 * n + pro_bytes);
   launch_project(PJ_RESTART, defl_kind(c), am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
                  op->w, op->V_base + op->guard, nullptr, op->vstride, 0, op->n_pad, op->part,
@@ -543,7 +545,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   double* V = op->V_base + op->guard;
   const int nvec = j + 1;
   const double pro_bytes = !c ? 0.0 : c->dense ? 8.0 * c->d * n
-                                               : 13.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
+                                               : 37.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
   if (c) {
     coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
                  nullptr, op->w, &st->active);
@@ -1029,8 +1031,14 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(cudaMemsetAsync(c->own_base, 0, (size_t)op->vlen * sizeof(double), s));
   DKD(cudaMallocAsync(&c->mask_base, (size_t)op->vlen, s));
   DKD(cudaMemsetAsync(c->mask_base, 0, (size_t)op->vlen, s));
+  DKD(cudaMallocAsync(&c->flab_base, (size_t)op->vlen * sizeof(int2), s));
+  DKD(cudaMemsetAsync(c->flab_base, 0xff, (size_t)op->vlen * sizeof(int2), s));
+  DKD(cudaMallocAsync(&c->fco_base, (size_t)op->vlen * sizeof(double2), s));
+  DKD(cudaMemsetAsync(c->fco_base, 0, (size_t)op->vlen * sizeof(double2), s));
   c->pro.lab = c->lab;
   c->pro.own = c->own_base + op->guard;
+  c->pro.flab = c->flab_base + op->guard;
+  c->pro.fco = c->fco_base + op->guard;
   c->pro.mask = c->mask_base + op->guard;
   {
     unsigned long long* dcnt = nullptr;
@@ -1038,7 +1046,8 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
     DKD(cudaMallocAsync(&dcnt, sizeof(unsigned long long), s));
     DKD(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), s));
     launch_prolong_setup(ap_choice == DK_AP_AM, make_dia(op, ap_choice == DK_AP_AM), c->lab, n_pad,
-                         c->own_base + op->guard, c->mask_base + op->guard, dcnt, s);
+                         c->own_base + op->guard, c->flab_base + op->guard,
+                         c->fco_base + op->guard, c->mask_base + op->guard, dcnt, s);
     DKD(cudaMemcpyAsync(&hcnt, dcnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
     DKD(cudaFreeAsync(dcnt, s));
     DKD(cudaStreamSynchronize(s));
@@ -1406,7 +1415,7 @@ int dk_defl_destroy(dk_defl* c) {
                   c->Z_base,   c->AZ_base,
                   c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
                   c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
-                  c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->seg_ptr,
+                  c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->flab_base, c->fco_base, c->seg_ptr,
                   c->seg_slot, c->long_ids};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);

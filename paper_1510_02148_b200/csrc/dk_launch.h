@@ -45,7 +45,9 @@ void launch_gemv(const double* M, int d, int ld, const double* x, double* y, con
 struct Prolong {
   const int* lab;             // guarded labels
   const double* own;          // guarded: sum of a cell's coefficients into its own column
-  const unsigned char* mask;  // guarded: diagonals whose column carries another label
+  const int2* flab;           // guarded: the first two foreign labels of a cell's row (-1: none)
+  const double2* fco;         // guarded: their summed coefficients
+  const unsigned char* mask;  // guarded: diagonals whose label is a third (or later) foreign one
   const double* az;           // dense basis: rows A_p Z_k (stride azs), k < dz
   long long azs;
   int dz;
@@ -53,7 +55,8 @@ struct Prolong {
 // deflation kind of a projection: none, indicator (labels), dense basis rows
 enum DeflKind { DK_NONE = 0, DK_LABELS = 1, DK_DENSE = 2 };
 void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad, double* own,
-                          unsigned char* mask, unsigned long long* nmasked, cudaStream_t s);
+                          int2* flab, double2* fco, unsigned char* mask,
+                          unsigned long long* nmasked, cudaStream_t s);
 
 enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
 // w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w, ||w_out||^2
