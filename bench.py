@@ -350,8 +350,9 @@ def run_ours(args, world, rank, local, pg):
             "config": {"workload": case.name, "config_index": args.config, "n_cells": n,
                        "d": basis.d, "m": case.m, "tol": case.tol, "seed": args.seed,
                        "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (per-iteration stream ~1.6 GB: V 458 MB, "
-                             "E^-1 953 MB)"},
+                       "l2": f"inputs larger than L2 (per-iteration stream "
+                             f"{bytes_per_iter / 1e6:.0f} MB on average; the basis V alone "
+                             f"{(case.m + 1) * 8.0 * n / 1e6:.0f} MB; no flush needed)"},
             "iterations_per_solve": iters_per_solve, "converged": converged,
             "final_relres": relres, "time_to_solve_s": ms_max * 1e-3 / args.steps,
             "setup_s": setup_s, "setup_ms": setup_ms,
