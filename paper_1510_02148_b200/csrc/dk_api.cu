@@ -363,7 +363,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   }
   if (op->scal_m < m) {
     if (op->scal) DK_TRY(cudaFreeAsync(op->scal, op->stream));
-    const size_t cnt = 6 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
+    const size_t cnt = 7 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
                        (size_t)(m + 1) * (m + 1);
     DK_TRY(cudaMallocAsync(&op->scal, cnt * sizeof(double), op->stream));
     DK_TRY(cudaMemsetAsync(op->scal, 0, cnt * sizeof(double), op->stream));
@@ -397,6 +397,11 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.gticket = op->gticket;
   sc.gpart = op->gpart;
   op->gs_fuse = gs_can_fuse(op->G, sc) && getenv("DK_NO_GS_FUSE") == nullptr;
+  // early start of each iteration's stencil on k_gs's published sigma (needs the fused second
+  // Gram-Schmidt pass: k_gs then always finishes the iteration itself)
+  sc.post = (op->gs_fuse && getenv("DK_NO_EARLY") == nullptr) ? reinterpret_cast<unsigned*>(p)
+                                                               : nullptr;
+  p += m + 1;
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
@@ -452,7 +457,8 @@ void prof_collect(dk_op* op) {
 // ---- the deflation building blocks ------------------------------------------------------
 // s = Z^T (mode-applied v) ; y = E^-1 s
 void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const double* v,
-                  const double* scale, const double* b, double* out, const int* gate) {
+                  const double* scale, const double* b, double* out, const int* gate,
+                  const unsigned* wait = nullptr) {
   const Dia A = make_dia(op, pre);
   const double n = (double)op->n;
   if (c->dense) {  // stencil (stored), then s = Z^T w and y = E^-1 s in one multi-dot kernel
@@ -462,7 +468,8 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
       ProfScope ps(op, PC_STENCIL,
                    (16.0 + 8.0 * op->nstore + (pre ? 8.0 : 0.0) + (mode == ST_RESID ? 8.0 : 0.0)) *
                        n);
-      launch_stencil(mode, pre, true, A, op->n_pad, v, scale, b, dst, nullptr, gate, op->stream);
+      launch_stencil(mode, pre, true, A, op->n_pad, v, scale, b, dst, nullptr, gate, op->stream,
+                     wait);
       src = dst;
     }
     ProfScope ps(op, PC_RESTRICT, 8.0 * (c->d + 1) * n);
@@ -475,7 +482,8 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
     const double by = 12.0 + (write ? 8.0 : 0.0) +
                       (mode == ST_IDENT ? 0.0 : 8.0 * op->nstore + (pre ? 8.0 : 0.0));
     ProfScope ps(op, PC_STENCIL, by * n);
-    launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream);
+    launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream,
+                   wait);
   }
   if (c->prof) {  // s~ = P Z^T w, then the two tile streams (t = W s~, y = P^T W^T t)
     {
@@ -546,13 +554,15 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   const int nvec = j + 1;
   const double pro_bytes = !c ? 0.0 : c->dense ? 8.0 * c->d * n
                                                : 37.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
+  // from the second iteration of a cycle on, the stencil starts on k_gs's published sigma
+  const unsigned* wait = (op->sc.post != nullptr && j >= 1) ? op->sc.post + (j - 1) : nullptr;
   if (c) {
     coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
-                 nullptr, op->w, &st->active);
+                 nullptr, op->w, &st->active, wait);
   } else {
     ProfScope ps(op, PC_STENCIL, (8.0 * op->nstore + (pre ? 24.0 : 16.0)) * n);
     launch_stencil(ST_APPLY, pre, true, A, op->n_pad, V + (long long)j * op->vstride,
-                   op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream);
+                   op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream, wait);
   }
   {
     ProfScope ps(op, PC_PROJECT,

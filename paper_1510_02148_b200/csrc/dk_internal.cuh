@@ -81,8 +81,15 @@ struct Scal {
   double* gpart;          // [quantities x kGroupTickets] group partials of reduce_grouped
   double* hist;    // [max_iters+1]
   int* restart_of; // [max_iters+1]
+  unsigned* post;  // [m+1] early-start flags (nullptr: off): post[j] = 1 once k_gs(j) has
+                   // published sigma_{j+1}; the next stencil starts on it
   int m;
 };
+
+// volatile (L2) load of a flag or scalar another grid still running may write
+__device__ __forceinline__ unsigned ld_flag(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
 
 // ---- programmatic dependent launch ----------------------------------------------------
 // Every kernel of the solve sequence is launched with programmatic stream serialisation:

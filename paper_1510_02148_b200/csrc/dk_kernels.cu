@@ -152,6 +152,27 @@ __device__ __forceinline__ void stencil_restrict_tail(const double (&rr)[8], con
   }
 }
 
+// Early start of an iteration's stencil (wait != nullptr): the grid is launched while k_gs of
+// the previous iteration finishes its reduction and Givens update.  It starts once k_gs has
+// published sigma (post flag) instead of on the whole grid's completion, and waits for that
+// completion (griddepcontrol.wait) only before it exits, so every later kernel still sees
+// k_gs's control state.  A gate already closed means the previous k_gs did not run (it
+// would have posted otherwise): skip.  Returns false when the block skips.
+__device__ __forceinline__ bool early_start(const unsigned* wait, const int* gate) {
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    int go = gate == nullptr || *reinterpret_cast<const volatile int*>(gate) != 0;
+    if (go) {
+      while (ld_flag(wait) == 0u) __nanosleep(64);
+      __threadfence();
+    }
+    s_go = go;
+  }
+  __syncthreads();
+  if (!s_go) pdl_wait();
+  return s_go != 0;
+}
+
 // ======================================================================================
 // K1: DIA stencil with fused scale / Jacobi / residual, optional run restriction.
 // Row sums are accumulated in ascending-offset (= CSR column) order with separately
@@ -166,9 +187,14 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
                                                       const int* __restrict__ tile_run_off,
                                                       const int* __restrict__ run_slot,
                                                       double* __restrict__ run_part,
-                                                      const int* __restrict__ gate) {
-  pdl_wait();
-  if (gate != nullptr && *gate == 0) return;
+                                                      const int* __restrict__ gate,
+                                                      const unsigned* wait) {
+  if (wait != nullptr) {
+    if (!early_start(wait, gate)) return;
+  } else {
+    pdl_wait();
+    if (gate != nullptr && *gate == 0) return;
+  }
   __shared__ double sw[RESTRICT ? kTilePad : 2];
   __shared__ int sl[RESTRICT ? kTilePad : 2];
   __shared__ double wsum[kWarps];
@@ -180,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
   __shared__ __align__(16) double sp[STAGE ? kTile + 2 * kHalo : 2];
   const long long base = (long long)blockIdx.x * kTile;
   const bool has_scale = (MODE == ST_APPLY) && scale != nullptr;
-  const double sc = has_scale ? *scale : 1.0;
+  const double sc = has_scale ? __ldcg(scale) : 1.0;
   if (STAGE) {
     for (int e = threadIdx.x; e < (kTile + 2 * kHalo) / 2; e += kThreads) {
       const long long i = base - kHalo + 2 * e;
@@ -265,6 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
     if (RESTRICT) lb[k] = *reinterpret_cast<const int2*>(lab + i);
   }
   if (RESTRICT) stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  if (wait != nullptr) pdl_wait();
 }
 
 // K1 for the symmetric 7-point operator (TPFA; DIA offsets -nxny, -nx, -1, 0, 1, nx, nxny,
@@ -335,9 +362,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
                                                            const int* __restrict__ tile_run_off,
                                                            const int* __restrict__ run_slot,
                                                            double* __restrict__ run_part,
-                                                           const int* __restrict__ gate, int H) {
-  pdl_wait();
-  if (gate != nullptr && *gate == 0) return;
+                                                           const int* __restrict__ gate, int H,
+                                                           const unsigned* wait) {
+  if (wait != nullptr) {
+    if (!early_start(wait, gate)) return;
+  } else {
+    pdl_wait();
+    if (gate != nullptr && *gate == 0) return;
+  }
   extern __shared__ __align__(16) double sp[];  // [H | kTile | H]
   __shared__ double sw[RESTRICT ? kTilePad : 2];
   __shared__ int sl[RESTRICT ? kTilePad : 2];
@@ -345,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
   const long long base = (long long)blockIdx.x * kTile;
   const long long nx = A.off[5], nz = A.off[6];
   const bool has_scale = scale != nullptr;
-  const double sc = has_scale ? *scale : 1.0;
+  const double sc = has_scale ? __ldcg(scale) : 1.0;
   Sym7Pair q0, q1;
   sym7_load<PRE>(q0, A, v, base + 2 * threadIdx.x, nx, nz);
   sym7_load<PRE>(q1, A, v, base + 2 * threadIdx.x + 512, nx, nz);
@@ -391,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
       st2(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
   if (RESTRICT)
     stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  if (wait != nullptr) pdl_wait();
 }
 
 // halo of k_stencil_sym7, or 0 when the operator is not the symmetric even 7-point stencil
@@ -408,7 +441,8 @@ static int sym7_halo(const Dia& A) {
 
 template <bool PRE, bool R, bool W>
 static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, const double* scale,
-                       double* out, const RunMap* rm, const int* gate, cudaStream_t s) {
+                       double* out, const RunMap* rm, const int* gate, cudaStream_t s,
+                       const unsigned* wait) {
   const unsigned grid = (unsigned)(n_pad / kTile);
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
   static size_t attr = 0;
@@ -419,42 +453,45 @@ static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, co
   }
   launch_pdl(k_stencil_sym7<PRE, R, W>, dim3(grid), dim3(kThreads), smem, s, A, v, scale, out,
              rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
-             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H);
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H, wait);
 }
 
 template <int MODE, bool PRE, bool R, bool W>
 static void stencil_t(const Dia& A, long long n_pad, const double* v, const double* scale,
                       const double* b, double* out, const RunMap* rm, const int* gate,
-                      cudaStream_t s) {
+                      cudaStream_t s, const unsigned* wait = nullptr) {
   const unsigned grid = (unsigned)(n_pad / kTile);
   launch_pdl(k_stencil<MODE, PRE, R, W>, dim3(grid), dim3(kThreads), 0, s, A, v, scale, b, out,
              rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
-             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate);
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, wait);
 }
 
 template <int MODE, bool PRE>
 static void stencil_rw(bool write, const Dia& A, long long n_pad, const double* v,
                        const double* scale, const double* b, double* out, const RunMap* rm,
-                       const int* gate, cudaStream_t s) {
+                       const int* gate, cudaStream_t s, const unsigned* wait = nullptr) {
   if (rm) {
-    if (write) stencil_t<MODE, PRE, true, true>(A, n_pad, v, scale, b, out, rm, gate, s);
-    else stencil_t<MODE, PRE, true, false>(A, n_pad, v, scale, b, out, rm, gate, s);
+    if (write) stencil_t<MODE, PRE, true, true>(A, n_pad, v, scale, b, out, rm, gate, s, wait);
+    else stencil_t<MODE, PRE, true, false>(A, n_pad, v, scale, b, out, rm, gate, s, wait);
   } else {
-    stencil_t<MODE, PRE, false, true>(A, n_pad, v, scale, b, out, rm, gate, s);
+    stencil_t<MODE, PRE, false, true>(A, n_pad, v, scale, b, out, rm, gate, s, wait);
   }
 }
 
 void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
                     const double* scale, const double* b, double* out, const RunMap* rm,
-                    const int* gate, cudaStream_t s) {
+                    const int* gate, cudaStream_t s, const unsigned* wait) {
+  if (mode != ST_APPLY) wait = nullptr;
   const int H = (mode == ST_APPLY && !getenv("DK_GENERIC_STENCIL")) ? sym7_halo(A) : 0;
   if (H > 0) {
-    if (pre && rm && write) stencil7_t<true, true, true>(A, H, n_pad, v, scale, out, rm, gate, s);
-    else if (pre && rm) stencil7_t<true, true, false>(A, H, n_pad, v, scale, out, rm, gate, s);
-    else if (pre) stencil7_t<true, false, true>(A, H, n_pad, v, scale, out, rm, gate, s);
-    else if (rm && write) stencil7_t<false, true, true>(A, H, n_pad, v, scale, out, rm, gate, s);
-    else if (rm) stencil7_t<false, true, false>(A, H, n_pad, v, scale, out, rm, gate, s);
-    else stencil7_t<false, false, true>(A, H, n_pad, v, scale, out, rm, gate, s);
+    if (pre && rm && write)
+      stencil7_t<true, true, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+    else if (pre && rm) stencil7_t<true, true, false>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+    else if (pre) stencil7_t<true, false, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+    else if (rm && write)
+      stencil7_t<false, true, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+    else if (rm) stencil7_t<false, true, false>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+    else stencil7_t<false, false, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
     return;
   }
   if (mode == ST_IDENT) {
@@ -462,9 +499,9 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
   } else if (mode == ST_RESID) {
     stencil_rw<ST_RESID, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
   } else if (pre) {
-    stencil_rw<ST_APPLY, true>(write, A, n_pad, v, scale, b, out, rm, gate, s);
+    stencil_rw<ST_APPLY, true>(write, A, n_pad, v, scale, b, out, rm, gate, s, wait);
   } else {
-    stencil_rw<ST_APPLY, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
+    stencil_rw<ST_APPLY, false>(write, A, n_pad, v, scale, b, out, rm, gate, s, wait);
   }
 }
 
@@ -805,6 +842,13 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
       sh_g[(nvec - 1) * nvec + v] = g;
     }
   }
+  if (sc.post != nullptr) {  // early start of k_gs: the coefficients are final here
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicExch(sc.post + (m + 1) + j, 1u);
+    }
+  }
   if (stage)
     for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
       const int i = e / (nvec - 1), k = e % (nvec - 1);
@@ -842,6 +886,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
                                                       double* __restrict__ part, int G, Scal sc,
                                                       int j, const int* __restrict__ gate) {
   pdl_wait();
+  // the stencil of this iteration has completed: re-arm its early-start flag
+  if (MODE == PJ_ITER && sc.post != nullptr && j >= 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    sc.post[j - 1] = 0u;            // consumed by this iteration's stencil
+    sc.post[sc.m + 1 + j - 1] = 0u;  // consumed by the previous k_gs (done: the stencil waited)
+  }
   if (*gate == 0) return;
   extern __shared__ double red[];  // [nq][kWarps]
   __shared__ __align__(16) double s_w[(MODE == PJ_ITER || MODE == PJ_REDOTS) ? kChunk : 2];
@@ -1218,15 +1267,22 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
                                                  const double* __restrict__ V, long long vstride,
                                                  int nvec, long long n_pad,
                                                  double* __restrict__ part, int G, Scal sc, int j,
-                                                 const int* __restrict__ gate, int fuse) {
-  pdl_wait();
-  if (*gate == 0) return;
+                                                 const int* __restrict__ gate, int fuse,
+                                                 const unsigned* wait) {
+  // early start (wait != nullptr): on the projection's published coefficients; its
+  // re-orthogonalisation verdict is read after its completion (griddepcontrol.wait below)
+  if (wait != nullptr) {
+    if (!early_start(wait, gate)) return;
+  } else {
+    pdl_wait();
+    if (*gate == 0) return;
+  }
   extern __shared__ double sh[];
   double* cf = sh;                                  // [nvec]
   double* red = sh + nvec;                          // [kWarps] (+ scratch)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool second = !REORTH && fuse && sc.st->reorth != 0;
-  for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = REORTH ? sc.corr[q] : sc.coef[q];
+  for (int q = threadIdx.x; q < nvec; q += blockDim.x)
+    cf[q] = REORTH ? sc.corr[q] : __ldcg(sc.coef + q);
   for (int q = threadIdx.x; q < kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
@@ -1261,6 +1317,9 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     nrm = warp_sum(nrm);
     if (lane == 0) red[warp] += nrm;
   }
+  if (wait != nullptr) pdl_wait();
+  const bool second =
+      !REORTH && fuse && *reinterpret_cast<const volatile int*>(&sc.st->reorth) != 0;
   if (second) {
     // corr_v = V_v . u: block partials over this block's chunks (u re-read from its own writes)
     __syncthreads();
@@ -1351,6 +1410,11 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   }
   if (!reduce_grouped(part, 1, G, sc.gticket, sc.gpart, red)) return;
   const double hj1 = sqrt(red[0]);
+  if (!REORTH && sc.post != nullptr && threadIdx.x == 0) {  // early start of the next stencil
+    sc.sigma[j + 1] = 1.0 / hj1;
+    __threadfence();
+    atomicExch(sc.post + j, 1u);
+  }
   __syncthreads();
   if (!REORTH && !second && sc.st->reorth) return;  // the separate second pass finishes it
   finish_iteration_block(sc, j, hj1, red);
@@ -1377,10 +1441,12 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
   const size_t smem = gs_smem(sc, nvec);
   if (reorth)
     launch_pdl(k_gs<true>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
-               n_pad, part, G, sc, j, gate, 0);
+               n_pad, part, G, sc, j, gate, 0, (const unsigned*)nullptr);
   else
     launch_pdl(k_gs<false>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
-               n_pad, part, G, sc, j, gate, fuse ? 1 : 0);
+               n_pad, part, G, sc, j, gate, fuse ? 1 : 0,
+               (const unsigned*)(fuse && sc.post != nullptr ? sc.post + (sc.m + 1) + j
+                                                            : nullptr));
 }
 
 // ======================================================================================
@@ -1391,6 +1457,8 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
 __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
   pdl_wait();
   State* st = sc.st;
+  if (sc.post != nullptr)  // re-arm the early-start flags (the last iteration's is still set)
+    for (int i = threadIdx.x; i < 2 * (sc.m + 1); i += 32) sc.post[i] = 0u;
   if (!st->cycle_open) return;
   extern __shared__ double sm[];
   const int m = sc.m;

@@ -32,9 +32,11 @@ constexpr int kShortRuns = 16;
 
 // w = (mode) ; if rm != nullptr also run sums of w.  pre: apply the Jacobi inverse.
 // scale (device scalar or nullptr) multiplies v first.  gate (device int or nullptr).
+// wait (ST_APPLY only; nullptr: off): start on *wait != 0 instead of the predecessor grid's
+// completion (the scale is read after it), wait for the predecessor only before exiting.
 void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
                     const double* scale, const double* b, double* out, const RunMap* rm,
-                    const int* gate, cudaStream_t s);
+                    const int* gate, cudaStream_t s, const unsigned* wait = nullptr);
 // s[s_pos[L]] (s[L] without s_pos) = sum of run partials of label L, fixed order.
 void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s);
 // y = M x, M d x d row-major with leading dimension ld.

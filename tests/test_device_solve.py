@@ -310,3 +310,23 @@ def test_sym7_stencil_matches_generic(gpu, monkeypatch):
     assert runs[0].iterations == runs[1].iterations
     np.testing.assert_array_equal(runs[0].x, runs[1].x)
     np.testing.assert_array_equal(runs[0].residual_history, runs[1].residual_history)
+
+
+def test_early_start_matches_serialised(gpu, monkeypatch):
+    """Early start of the stencil / Gram-Schmidt kernels on published scalars (post flags)
+    changes only the schedule: identical solves, bit for bit, with and without it."""
+    case = configs.config1()
+    A, b = case.problem()
+    basis = dk.partition_to_basis(case.partition())
+    M = dk.Preconditioner.jacobi(A)
+    runs = []
+    for early in (True, False):
+        if not early:
+            monkeypatch.setenv("DK_NO_EARLY", "1")
+        A.release_device()
+        runs.append([dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol,
+                                max_iters=case.max_iters) for _ in range(2)])  # eager + graph
+    for a, c in zip(runs[0], runs[1]):
+        assert a.iterations == c.iterations
+        np.testing.assert_array_equal(a.x, c.x)
+        np.testing.assert_array_equal(a.residual_history, c.residual_history)
