@@ -161,6 +161,11 @@ __device__ __forceinline__ double2 ld2_stream(const double* ptr, unsigned long l
                : "l"(ptr), "l"(pol));
   return v;
 }
+// Bulk prefetch of [p, p + bytes) into L2 (16 B aligned, bytes a multiple of 16): issued by
+// early-started grids for data that is already final while they wait for their start flag.
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 // ---- 1D TMA bulk copies completing on an mbarrier (cp.async.bulk, UBLKCP in SASS) --------
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -365,6 +365,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
                                                            const int* __restrict__ gate, int H,
                                                            const unsigned* wait) {
   if (wait != nullptr) {
+    // the tile's operator diagonals, M^-1 and labels are final: into L2 while waiting
+    const long long b0 = (long long)blockIdx.x * kTile;
+    const int t = threadIdx.x;
+    if (t < 4) l2_prefetch(A.co[3 + t] + b0, kTile * 8);
+    if (PRE && t == 4) l2_prefetch(A.inv + b0, kTile * 8);
+    if (RESTRICT && t == 5) l2_prefetch(lab + b0, kTile * 4);
     if (!early_start(wait, gate)) return;
   } else {
     pdl_wait();
@@ -1262,6 +1268,11 @@ __device__ __forceinline__ void grid_arrive_lead_release(unsigned int* count, un
 // pass (krylov.py:169-170) runs inside the same launch — corr = V^T u over the stored u,
 // the coefficients in the leading block, u -= V corr — instead of two extra launches that
 // are otherwise issued gated-off every iteration.
+#ifndef DK_EARLY_ROWS
+#define DK_EARLY_ROWS 4
+#endif
+constexpr int kEarlyRows = DK_EARLY_ROWS;  // basis rows k_gs prefetches while it waits
+
 template <bool REORTH>
 __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_out,
                                                  const double* __restrict__ V, long long vstride,
@@ -1272,6 +1283,11 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   // early start (wait != nullptr): on the projection's published coefficients; its
   // re-orthogonalisation verdict is read after its completion (griddepcontrol.wait below)
   if (wait != nullptr) {
+    // the basis rows are final: the first ones of this block's chunk into L2 while waiting
+    if (gridDim.x * (long long)kChunk >= n_pad && threadIdx.x < kEarlyRows &&
+        (int)threadIdx.x < nvec)
+      l2_prefetch(V + (long long)threadIdx.x * vstride + (long long)blockIdx.x * kChunk,
+                  kChunk * 8);
     if (!early_start(wait, gate)) return;
   } else {
     pdl_wait();
