@@ -628,7 +628,7 @@ void free_stream(TileGemv& g, cudaStream_t s) {
 }
 
 // (warps per CTA, stages per warp) of k_tgemv; DK_TG_CFG picks one (set-up and launch agree)
-static const int kTgCfg[][2] = {{12, 2}, {16, 1}, {8, 3}, {4, 6}, {16, 2}, {8, 6}};
+static const int kTgCfg[][2] = {{12, 2}, {16, 1}, {8, 3}, {4, 6}, {8, 2}, {6, 2}};
 int tgemv_cfg() {
   static int c = -1;
   if (c < 0) {
@@ -668,8 +668,8 @@ void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scat
     case 1: launch_tg<16, 1>(g, x, y, scatter, d, gate, s); break;
     case 2: launch_tg<8, 3>(g, x, y, scatter, d, gate, s); break;
     case 3: launch_tg<4, 6>(g, x, y, scatter, d, gate, s); break;
-    case 4: launch_tg<16, 2>(g, x, y, scatter, d, gate, s); break;
-    case 5: launch_tg<8, 6>(g, x, y, scatter, d, gate, s); break;
+    case 4: launch_tg<8, 2>(g, x, y, scatter, d, gate, s); break;
+    case 5: launch_tg<6, 2>(g, x, y, scatter, d, gate, s); break;
     default: launch_tg<12, 2>(g, x, y, scatter, d, gate, s); break;
   }
 }
