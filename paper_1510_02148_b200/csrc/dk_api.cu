@@ -402,6 +402,8 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.post = (op->gs_fuse && getenv("DK_NO_EARLY") == nullptr) ? reinterpret_cast<unsigned*>(p)
                                                                : nullptr;
   p += m + 1;
+  sc.ng = (op->G + kGroup - 1) / kGroup;
+  sc.gpart_gs = op->gpart + (size_t)(op->part_q - 1) * kGroupTickets;  // past the dots' rows
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
@@ -469,7 +471,7 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
                    (16.0 + 8.0 * op->nstore + (pre ? 8.0 : 0.0) + (mode == ST_RESID ? 8.0 : 0.0)) *
                        n);
       launch_stencil(mode, pre, true, A, op->n_pad, v, scale, b, dst, nullptr, gate, op->stream,
-                     wait);
+                     wait, op->sc.gpart_gs, op->sc.ng);
       src = dst;
     }
     ProfScope ps(op, PC_RESTRICT, 8.0 * (c->d + 1) * n);
@@ -483,7 +485,7 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
                       (mode == ST_IDENT ? 0.0 : 8.0 * op->nstore + (pre ? 8.0 : 0.0));
     ProfScope ps(op, PC_STENCIL, by * n);
     launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream,
-                   wait);
+                   wait, op->sc.gpart_gs, op->sc.ng);
   }
   if (c->prof) {  // s~ = P Z^T w, then the two tile streams (t = W s~, y = P^T W^T t)
     {
@@ -562,7 +564,8 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   } else {
     ProfScope ps(op, PC_STENCIL, (8.0 * op->nstore + (pre ? 24.0 : 16.0)) * n);
     launch_stencil(ST_APPLY, pre, true, A, op->n_pad, V + (long long)j * op->vstride,
-                   op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream, wait);
+                   op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream, wait,
+                   op->sc.gpart_gs, op->sc.ng);
   }
   {
     ProfScope ps(op, PC_PROJECT,

@@ -81,8 +81,11 @@ struct Scal {
   double* gpart;          // [quantities x kGroupTickets] group partials of reduce_grouped
   double* hist;    // [max_iters+1]
   int* restart_of; // [max_iters+1]
-  unsigned* post;  // [m+1] early-start flags (nullptr: off): post[j] = 1 once k_gs(j) has
-                   // published sigma_{j+1}; the next stencil starts on it
+  unsigned* post;  // [2(m+1)] early-start counters (nullptr: off): post[j] counts the group
+                   // totals of k_gs(j)'s norm, post[m+1+j] those of the projection's dots; the
+                   // next grid starts when all ng are in
+  double* gpart_gs;  // group partials of k_gs's norm (apart from the projection's)
+  int ng;            // groups of the grouped reductions
   int m;
 };
 
@@ -243,9 +246,32 @@ __device__ __forceinline__ void reduce_partials(const double* part, int nq, int 
 // true in that one block.  One L2 round trip per level instead of G / 32 dependent loads per
 // quantity for a single-level sweep.  gticket: kGroupTickets zeroed counters (reset on exit).
 constexpr int kGroup = 32, kGroupTickets = 32;
+// The final level's arithmetic for quantity q by one thread (bitwise equal to the block's):
+// early-started consumers recompute a total from the group partials themselves.
+__device__ __forceinline__ double grouped_total(const double* gpart, int q, int ng,
+                                               bool global = true) {
+  double t[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    double v[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const double* a = gpart + (size_t)q * ng + 8 * h + b;
+      v[b] = (8 * h + b < ng) ? (global ? __ldcg(a) : *a) : 0.0;
+    }
+    double a = 0.0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) a += v[b];
+    t[h] = a;
+  }
+  return ((t[0] + t[1]) + t[2]) + t[3];
+}
+
+// post_cnt (nullptr: none): every group's last block adds one once its group partials are
+// visible; a consumer that sees ng arrivals may form the totals with grouped_total.
 __device__ __forceinline__ bool reduce_grouped(const double* part, int nq, int G,
                                                unsigned int* gticket, double* gpart,
-                                               double* out) {
+                                               double* out, unsigned* post_cnt = nullptr) {
   __shared__ int s_flag;
   const int ng = (G + kGroup - 1) / kGroup;
   const int g = blockIdx.x / kGroup, gb = g * kGroup;
@@ -278,6 +304,7 @@ __device__ __forceinline__ bool reduce_grouped(const double* part, int nq, int G
   }
   __threadfence();
   __syncthreads();
+  if (threadIdx.x == 0 && post_cnt != nullptr) atomicAdd(post_cnt, 1u);
   if (threadIdx.x == 0)
     s_flag = (atomicAdd(&gticket[kGroupTickets - 1], 1u) == (unsigned)(ng - 1));
   __syncthreads();

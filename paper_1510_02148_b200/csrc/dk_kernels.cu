@@ -153,17 +153,19 @@ __device__ __forceinline__ void stencil_restrict_tail(const double (&rr)[8], con
 }
 
 // Early start of an iteration's stencil (wait != nullptr): the grid is launched while k_gs of
-// the previous iteration finishes its reduction and Givens update.  It starts once k_gs has
-// published sigma (post flag) instead of on the whole grid's completion, and waits for that
-// completion (griddepcontrol.wait) only before it exits, so every later kernel still sees
-// k_gs's control state.  A gate already closed means the previous k_gs did not run (it
+// the previous iteration finishes its reduction and Givens update.  It starts once all groups
+// of k_gs's norm reduction are in (post counter == ng) and forms sigma itself from the group
+// partials (the same arithmetic as k_gs's last block), instead of waiting for the whole grid;
+// it waits for that completion (griddepcontrol.wait) only before it exits, so every later
+// kernel still sees k_gs's control state.  A gate already closed means the previous k_gs did not run (it
 // would have posted otherwise): skip.  Returns false when the block skips.
-__device__ __forceinline__ bool early_start(const unsigned* wait, const int* gate) {
+__device__ __forceinline__ bool early_start(const unsigned* wait, const int* gate,
+                                            unsigned need) {
   __shared__ int s_go;
   if (threadIdx.x == 0) {
     int go = gate == nullptr || *reinterpret_cast<const volatile int*>(gate) != 0;
     if (go) {
-      while (ld_flag(wait) == 0u) __nanosleep(64);
+      while (ld_flag(wait) < need) __nanosleep(64);
       __threadfence();
     }
     s_go = go;
@@ -171,6 +173,15 @@ __device__ __forceinline__ bool early_start(const unsigned* wait, const int* gat
   __syncthreads();
   if (!s_go) pdl_wait();
   return s_go != 0;
+}
+
+// sigma = 1 / ||u|| from k_gs's group partials: one thread forms it (k_gs's last-block
+// arithmetic), the block shares it
+__device__ __forceinline__ double early_sigma(const double* gsig, int ng) {
+  __shared__ double s_sig;
+  if (threadIdx.x == 0) s_sig = 1.0 / sqrt(grouped_total(gsig, 0, ng));
+  __syncthreads();
+  return s_sig;
 }
 
 // ======================================================================================
@@ -188,9 +199,10 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
                                                       const int* __restrict__ run_slot,
                                                       double* __restrict__ run_part,
                                                       const int* __restrict__ gate,
-                                                      const unsigned* wait) {
+                                                      const unsigned* wait, const double* gsig,
+                                                      int ng) {
   if (wait != nullptr) {
-    if (!early_start(wait, gate)) return;
+    if (!early_start(wait, gate, (unsigned)ng)) return;
   } else {
     pdl_wait();
     if (gate != nullptr && *gate == 0) return;
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
   __shared__ __align__(16) double sp[STAGE ? kTile + 2 * kHalo : 2];
   const long long base = (long long)blockIdx.x * kTile;
   const bool has_scale = (MODE == ST_APPLY) && scale != nullptr;
-  const double sc = has_scale ? __ldcg(scale) : 1.0;
+  const double sc = !has_scale ? 1.0 : wait != nullptr ? early_sigma(gsig, ng) : __ldcg(scale);
   if (STAGE) {
     for (int e = threadIdx.x; e < (kTile + 2 * kHalo) / 2; e += kThreads) {
       const long long i = base - kHalo + 2 * e;
@@ -363,7 +375,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
                                                            const int* __restrict__ run_slot,
                                                            double* __restrict__ run_part,
                                                            const int* __restrict__ gate, int H,
-                                                           const unsigned* wait) {
+                                                           const unsigned* wait,
+                                                           const double* gsig, int ng) {
   if (wait != nullptr) {
     // the tile's operator diagonals, M^-1 and labels are final: into L2 while waiting
     const long long b0 = (long long)blockIdx.x * kTile;
@@ -371,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
     if (t < 4) l2_prefetch(A.co[3 + t] + b0, kTile * 8);
     if (PRE && t == 4) l2_prefetch(A.inv + b0, kTile * 8);
     if (RESTRICT && t == 5) l2_prefetch(lab + b0, kTile * 4);
-    if (!early_start(wait, gate)) return;
+    if (!early_start(wait, gate, (unsigned)ng)) return;
   } else {
     pdl_wait();
     if (gate != nullptr && *gate == 0) return;
@@ -383,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_stencil_sym7(Dia A, const doubl
   const long long base = (long long)blockIdx.x * kTile;
   const long long nx = A.off[5], nz = A.off[6];
   const bool has_scale = scale != nullptr;
-  const double sc = has_scale ? __ldcg(scale) : 1.0;
+  const double sc = !has_scale ? 1.0 : wait != nullptr ? early_sigma(gsig, ng) : __ldcg(scale);
   Sym7Pair q0, q1;
   sym7_load<PRE>(q0, A, v, base + 2 * threadIdx.x, nx, nz);
   sym7_load<PRE>(q1, A, v, base + 2 * threadIdx.x + 512, nx, nz);
@@ -448,7 +461,7 @@ static int sym7_halo(const Dia& A) {
 template <bool PRE, bool R, bool W>
 static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, const double* scale,
                        double* out, const RunMap* rm, const int* gate, cudaStream_t s,
-                       const unsigned* wait) {
+                       const unsigned* wait, const double* gsig, int ng) {
   const unsigned grid = (unsigned)(n_pad / kTile);
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
   static size_t attr = 0;
@@ -459,45 +472,49 @@ static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, co
   }
   launch_pdl(k_stencil_sym7<PRE, R, W>, dim3(grid), dim3(kThreads), smem, s, A, v, scale, out,
              rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
-             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H, wait);
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H, wait, gsig, ng);
 }
 
 template <int MODE, bool PRE, bool R, bool W>
 static void stencil_t(const Dia& A, long long n_pad, const double* v, const double* scale,
                       const double* b, double* out, const RunMap* rm, const int* gate,
-                      cudaStream_t s, const unsigned* wait = nullptr) {
+                      cudaStream_t s, const unsigned* wait = nullptr,
+                      const double* gsig = nullptr, int ng = 0) {
   const unsigned grid = (unsigned)(n_pad / kTile);
   launch_pdl(k_stencil<MODE, PRE, R, W>, dim3(grid), dim3(kThreads), 0, s, A, v, scale, b, out,
              rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
-             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, wait);
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, wait, gsig, ng);
 }
 
 template <int MODE, bool PRE>
 static void stencil_rw(bool write, const Dia& A, long long n_pad, const double* v,
                        const double* scale, const double* b, double* out, const RunMap* rm,
-                       const int* gate, cudaStream_t s, const unsigned* wait = nullptr) {
+                       const int* gate, cudaStream_t s, const unsigned* wait = nullptr,
+                       const double* gsig = nullptr, int ng = 0) {
   if (rm) {
-    if (write) stencil_t<MODE, PRE, true, true>(A, n_pad, v, scale, b, out, rm, gate, s, wait);
-    else stencil_t<MODE, PRE, true, false>(A, n_pad, v, scale, b, out, rm, gate, s, wait);
+    if (write)
+      stencil_t<MODE, PRE, true, true>(A, n_pad, v, scale, b, out, rm, gate, s, wait, gsig, ng);
+    else stencil_t<MODE, PRE, true, false>(A, n_pad, v, scale, b, out, rm, gate, s, wait, gsig, ng);
   } else {
-    stencil_t<MODE, PRE, false, true>(A, n_pad, v, scale, b, out, rm, gate, s, wait);
+    stencil_t<MODE, PRE, false, true>(A, n_pad, v, scale, b, out, rm, gate, s, wait, gsig, ng);
   }
 }
 
 void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
                     const double* scale, const double* b, double* out, const RunMap* rm,
-                    const int* gate, cudaStream_t s, const unsigned* wait) {
+                    const int* gate, cudaStream_t s, const unsigned* wait, const double* gsig,
+                    int ng) {
   if (mode != ST_APPLY) wait = nullptr;
   const int H = (mode == ST_APPLY && !getenv("DK_GENERIC_STENCIL")) ? sym7_halo(A) : 0;
   if (H > 0) {
     if (pre && rm && write)
-      stencil7_t<true, true, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
-    else if (pre && rm) stencil7_t<true, true, false>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
-    else if (pre) stencil7_t<true, false, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+      stencil7_t<true, true, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng);
+    else if (pre && rm) stencil7_t<true, true, false>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng);
+    else if (pre) stencil7_t<true, false, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng);
     else if (rm && write)
-      stencil7_t<false, true, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
-    else if (rm) stencil7_t<false, true, false>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
-    else stencil7_t<false, false, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait);
+      stencil7_t<false, true, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng);
+    else if (rm) stencil7_t<false, true, false>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng);
+    else stencil7_t<false, false, true>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng);
     return;
   }
   if (mode == ST_IDENT) {
@@ -505,9 +522,9 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
   } else if (mode == ST_RESID) {
     stencil_rw<ST_RESID, false>(write, A, n_pad, v, scale, b, out, rm, gate, s);
   } else if (pre) {
-    stencil_rw<ST_APPLY, true>(write, A, n_pad, v, scale, b, out, rm, gate, s, wait);
+    stencil_rw<ST_APPLY, true>(write, A, n_pad, v, scale, b, out, rm, gate, s, wait, gsig, ng);
   } else {
-    stencil_rw<ST_APPLY, false>(write, A, n_pad, v, scale, b, out, rm, gate, s, wait);
+    stencil_rw<ST_APPLY, false>(write, A, n_pad, v, scale, b, out, rm, gate, s, wait, gsig, ng);
   }
 }
 
@@ -848,13 +865,6 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
       sh_g[(nvec - 1) * nvec + v] = g;
     }
   }
-  if (sc.post != nullptr) {  // early start of k_gs: the coefficients are final here
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicExch(sc.post + (m + 1) + j, 1u);
-    }
-  }
   if (stage)
     for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
       const int i = e / (nvec - 1), k = e % (nvec - 1);
@@ -1015,7 +1025,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
     for (int w2 = 0; w2 < kWarps; ++w2) s += red[q * kWarps + w2];
     part[(size_t)q * G + blockIdx.x] = s;
   }
-  if (!reduce_grouped(part, nq, G, sc.gticket, sc.gpart, red)) return;
+  if (!reduce_grouped(part, nq, G, sc.gticket, sc.gpart, red,
+                      (MODE == PJ_ITER && sc.post != nullptr) ? sc.post + (sc.m + 1) + j
+                                                              : nullptr))
+    return;
   State* st = sc.st;
   const int m = sc.m;
   if (MODE == PJ_RESTART) {
@@ -1288,7 +1301,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
         (int)threadIdx.x < nvec)
       l2_prefetch(V + (long long)threadIdx.x * vstride + (long long)blockIdx.x * kChunk,
                   kChunk * 8);
-    if (!early_start(wait, gate)) return;
+    if (!early_start(wait, gate, (unsigned)sc.ng)) return;
   } else {
     pdl_wait();
     if (*gate == 0) return;
@@ -1297,8 +1310,19 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   double* cf = sh;                                  // [nvec]
   double* red = sh + nvec;                          // [kWarps] (+ scratch)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = threadIdx.x; q < nvec; q += blockDim.x)
-    cf[q] = REORTH ? sc.corr[q] : __ldcg(sc.coef + q);
+  if (!REORTH && wait != nullptr) {
+    // the projection's coefficients, as its last block forms them, from its group partials
+    double* gp = red;  // nvec x ng staged (red is free until the sweep's partial sums)
+    for (int e = threadIdx.x; e < nvec * sc.ng; e += blockDim.x) gp[e] = __ldcg(sc.gpart + e);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nvec; q += blockDim.x) {
+      const double sv = __ldcg(sc.sigma + q);
+      cf[q] = (grouped_total(gp, q, sc.ng, false) * sv) * sv;
+    }
+    __syncthreads();
+  } else {
+    for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = REORTH ? sc.corr[q] : sc.coef[q];
+  }
   for (int q = threadIdx.x; q < kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
@@ -1424,13 +1448,11 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     for (int w2 = 0; w2 < kWarps; ++w2) s += red[w2];
     part[blockIdx.x] = s;
   }
-  if (!reduce_grouped(part, 1, G, sc.gticket, sc.gpart, red)) return;
+  const bool early = !REORTH && sc.post != nullptr;  // the next stencil forms sigma itself
+  if (!reduce_grouped(part, 1, G, sc.gticket, early ? sc.gpart_gs : sc.gpart, red,
+                      early ? sc.post + j : nullptr))
+    return;
   const double hj1 = sqrt(red[0]);
-  if (!REORTH && sc.post != nullptr && threadIdx.x == 0) {  // early start of the next stencil
-    sc.sigma[j + 1] = 1.0 / hj1;
-    __threadfence();
-    atomicExch(sc.post + j, 1u);
-  }
   __syncthreads();
   if (!REORTH && !second && sc.st->reorth) return;  // the separate second pass finishes it
   finish_iteration_block(sc, j, hj1, red);
@@ -1439,6 +1461,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
 static size_t gs_smem(const Scal& sc, int nvec) {
   int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
   if (slots < 261) slots = 261;  // reduce_grouped scratch
+  if (slots < (sc.m + 1) * sc.ng) slots = (sc.m + 1) * sc.ng;  // early start: group partials
   return ((size_t)nvec + (size_t)slots) * sizeof(double);
 }
 

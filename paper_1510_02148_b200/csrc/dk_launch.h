@@ -36,7 +36,8 @@ constexpr int kShortRuns = 16;
 // completion (the scale is read after it), wait for the predecessor only before exiting.
 void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pad, const double* v,
                     const double* scale, const double* b, double* out, const RunMap* rm,
-                    const int* gate, cudaStream_t s, const unsigned* wait = nullptr);
+                    const int* gate, cudaStream_t s, const unsigned* wait = nullptr,
+                    const double* gsig = nullptr, int ng = 0);
 // s[s_pos[L]] (s[L] without s_pos) = sum of run partials of label L, fixed order.
 void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s);
 // y = M x, M d x d row-major with leading dimension ld.
