@@ -165,8 +165,7 @@ struct TileGemv {
   const int* rfirst = nullptr; // first warp of each output block
   const int* rslot = nullptr;  // partial-slot base of a block split across warps
   const int* rnp = nullptr;    // warps holding pieces of the block
-  double* part = nullptr;      // [slots][32]
-  unsigned* cnt = nullptr;     // arrival tickets per output block (reset by the last)
+  double* part = nullptr;      // [slots][32] pieces of split blocks (sentinel when empty)
   long long nt = 0;
   int nw = 0;                  // warps holding tiles (min(kTgGrid * warps per CTA, nt))
   int nrows = 0;

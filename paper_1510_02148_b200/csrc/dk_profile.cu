@@ -130,9 +130,18 @@ __global__ void k_tile_pack(const double* __restrict__ X, int d, int ld, const i
 // row r, so the row sum accumulates in a register across the warp's tiles of one output
 // block.  Lane c holds x_{col(t)}[c] (read after the dependency wait, the first kXPre tiles'
 // segments prefetched at once) and broadcasts it by shuffle.  A block whose tiles span
-// several warps is finished by the last of them to arrive (row ticket), summing the pieces
-// in warp order: deterministic.  With scatter, output row i goes to y[scatter[i]].
+// several warps is finished by the first of them, which reads the others' pieces from
+// self-validating slots (sentinel until written; no fence, no ticket) and sums them in warp
+// order: deterministic.  With scatter, output row i goes to y[scatter[i]].
 constexpr int kXPre = 8;
+
+// partial-row slots hold this bit pattern until written (a negative NaN with a full payload:
+// never the result of arithmetic, which yields the canonical NaN)
+__device__ __forceinline__ double sentinel_f64() { return __longlong_as_double(-1ll); }
+__device__ __forceinline__ bool is_sentinel(double v) { return __double_as_longlong(v) == -1ll; }
+__device__ __forceinline__ double ld_volatile_f64(const double* p) {
+  return *reinterpret_cast<const volatile double*>(p);
+}
 
 // bulk copy of one tile on an mbarrier (evict-first: each tile is read once per pass)
 __device__ __forceinline__ void tg_issue(unsigned char* b, const double* T,
@@ -221,20 +230,34 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
     double out = racc;
     bool write = true;
     if (np > 1) {
-      const int q0 = g.rslot[R] + (int)(w - g.rfirst[R]);
-      g.part[(long long)q0 * kPT + lane] = racc;
-      __threadfence();
-      __syncwarp();
-      unsigned old = 0;
-      if (lane == 0) old = atomicAdd(g.cnt + R, 1u);
-      old = __shfl_sync(0xffffffffu, old, 0);
-      write = old == (unsigned)(np - 1);
-      if (write) {
-        __threadfence();
-        out = 0.0;
-        const double* p0 = g.part + (long long)g.rslot[R] * kPT;
-        for (int q = 0; q < np; ++q) out += __ldcg(p0 + (long long)q * kPT + lane);
-        if (lane == 0) g.cnt[R] = 0u;
+      // A block split across warps is finished by its first warp (whose range ends with it,
+      // so the others' pieces, at the starts of their ranges, are normally in by then).  The
+      // pieces are self-validating: a slot holds the sentinel until its value lands, so no
+      // fence or ticket is needed; the finisher re-arms the slots.  Sum in warp order.
+      const int q = (int)(w - g.rfirst[R]);
+      double* slots = g.part + (long long)g.rslot[R] * kPT + lane;
+      if (q != 0) {
+        slots[(long long)q * kPT] = racc;
+        write = false;
+      } else {
+        out = 0.0 + racc;
+        for (int k0 = 1; k0 < np; k0 += 8) {  // eight slots in flight, then the in-order sum
+          double v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            v[i] = k0 + i < np ? ld_volatile_f64(slots + (long long)(k0 + i) * kPT) : 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (k0 + i >= np) break;
+            double* sl = slots + (long long)(k0 + i) * kPT;
+            while (is_sentinel(v[i])) {
+              __nanosleep(32);
+              v[i] = ld_volatile_f64(sl);
+            }
+            out += v[i];
+            *sl = sentinel_f64();
+          }
+        }
       }
     }
     if (write) {
@@ -608,8 +631,8 @@ int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost
   g.rnp = rnp;
   if (e == cudaSuccess)
     e = cudaMallocAsync(&g.part, (size_t)h.nslots * kPT * sizeof(double), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&g.cnt, (size_t)nrows * sizeof(unsigned), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(g.cnt, 0, (size_t)nrows * sizeof(unsigned), s);
+  if (e == cudaSuccess)  // every slot starts as the sentinel (all bits set)
+    e = cudaMemsetAsync(g.part, 0xff, (size_t)h.nslots * kPT * sizeof(double), s);
   if (e != cudaSuccess) return (int)e;
   // the tile stream itself (big_alloc'd by the caller into g.T)
   k_tile_pack<<<148 * 8, 256, 0, s>>>(W, d, ld, trow, tcol, h.nt, trans ? 1 : 0,
@@ -619,12 +642,11 @@ int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost
 
 void free_stream(TileGemv& g, cudaStream_t s) {
   void* bufs[] = {(void*)g.trow, (void*)g.tcol, (void*)g.rfirst, (void*)g.rslot, (void*)g.rnp,
-                  (void*)g.part, (void*)g.cnt};
+                  (void*)g.part};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);
   g.trow = g.tcol = g.rfirst = g.rslot = g.rnp = nullptr;
   g.part = nullptr;
-  g.cnt = nullptr;
 }
 
 // (warps per CTA, stages per warp) of k_tgemv; DK_TG_CFG picks one (set-up and launch agree)
