@@ -465,7 +465,7 @@ static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, co
   const unsigned grid = (unsigned)(n_pad / kTile);
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
   static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  if (smem > attr) {  // static + dynamic above 48 KB needs the opt-in (wide grids: nx = 512)
     cudaFuncSetAttribute(k_stencil_sym7<PRE, R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
