@@ -952,28 +952,48 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   Trace tr;
   const long long n = op->n, n_pad = op->n_pad;
   // host copy of the labels (input may live on the device)
-  std::vector<int> lab(n_pad, -1);
-  DK_TRY(cudaMemcpy(lab.data(), col_of_cell, (size_t)n * sizeof(int), cudaMemcpyDefault));
-  std::vector<long long> count(d, 0);
-  for (long long i = 0; i < n; ++i) {
-    if (lab[i] < -1 || lab[i] >= d) return fail(DK_EINVAL, "column label out of range");
-    if (lab[i] >= 0) count[lab[i]]++;
+  std::vector<int> lab(n_pad);
+  {
+    cudaPointerAttributes pa{};
+    const bool on_device = cudaPointerGetAttributes(&pa, col_of_cell) == cudaSuccess &&
+                           (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+    cudaGetLastError();  // a plain host pointer may leave an error behind on old drivers
+    if (on_device)
+      DK_TRY(cudaMemcpy(lab.data(), col_of_cell, (size_t)n * sizeof(int), cudaMemcpyDefault));
+    else
+      std::memcpy(lab.data(), col_of_cell, (size_t)n * sizeof(int));
+    std::fill(lab.begin() + n, lab.end(), -1);
   }
+  // one pass: validation, column sizes and the runs (maximal equal-label ranges in linear
+  // order; every tile start is a head)
+  std::vector<long long> count(d, 0);
+  const long long ntiles = n_pad / kTile;
+  std::vector<int> tile_off(ntiles + 1, 0);
+  std::vector<int> run_label;
+  run_label.reserve(n_pad / 8 + 16);
+  for (long long t = 0; t < ntiles; ++t) {
+    tile_off[t] = (int)run_label.size();
+    const long long i0 = t * kTile;
+    int prev = lab[i0];
+    if (prev < -1 || prev >= d) return fail(DK_EINVAL, "column label out of range");
+    run_label.push_back(prev);
+    if (prev >= 0) count[prev]++;
+    for (long long i = i0 + 1; i < i0 + kTile; ++i) {
+      const int L = lab[i];
+      if (L != prev) {
+        if (L < -1 || L >= d) return fail(DK_EINVAL, "column label out of range");
+        run_label.push_back(L);
+        prev = L;
+      }
+      if (L >= 0) count[L]++;
+    }
+  }
+  tile_off[ntiles] = (int)run_label.size();
   for (int L = 0; L < d; ++L)
     if (count[L] == 0) {
       // an empty indicator column makes E exactly singular (deflation.py:27-28 / sparse.py:135)
       return fail(DK_ESINGULAR, "zero pivot in LU factorization");
     }
-  // runs: maximal equal-label ranges in linear order, every tile start is a head
-  const long long ntiles = n_pad / kTile;
-  std::vector<int> tile_off(ntiles + 1, 0);
-  std::vector<int> run_label;
-  run_label.reserve(n_pad / 8 + 16);
-  for (long long i = 0; i < n_pad; ++i) {
-    if (i % kTile == 0) tile_off[i / kTile] = (int)run_label.size();
-    if (i % kTile == 0 || lab[i] != lab[i - 1]) run_label.push_back(lab[i]);
-  }
-  tile_off[ntiles] = (int)run_label.size();
   const long long nruns = (long long)run_label.size();
   if (nruns >= (1ll << 31)) return fail(DK_EUNSUPPORTED, "too many label runs");
   std::vector<int> ptr(d + 1, 0);
