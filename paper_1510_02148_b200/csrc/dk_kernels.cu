@@ -524,6 +524,11 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
 // K2: per-column sum of run partials (label-major slots: one thread per column, a warp per
 // column with more than kShortRuns runs; fixed order).
 // ======================================================================================
+#ifndef DK_LONG_BATCH
+#define DK_LONG_BATCH 16
+#endif
+constexpr int kLongBatch = DK_LONG_BATCH;  // loads per lane in flight for a long column
+
 __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __restrict__ run_part,
                                                              const int* __restrict__ ptr, int d,
                                                              const int* __restrict__ long_ids,
@@ -549,19 +554,20 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
     s[s_pos ? s_pos[L] : L] = acc;
     return;
   }
-  // one warp per long column (lane-strided, eight loads per lane in flight, fixed xor tree)
+  // one warp per long column (lane-strided, kLongBatch loads per lane in flight, fixed xor tree)
   const int wl = ((blockIdx.x - short_blocks) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wl >= nlong) return;
   const int L = long_ids[wl];
   double acc = 0.0;
   const int lo = ptr[L], hi = ptr[L + 1];
-  for (int k0 = lo + lane; k0 < hi; k0 += 32 * 8) {
-    double v[8];
+  for (int k0 = lo + lane; k0 < hi; k0 += 32 * kLongBatch) {
+    double v[kLongBatch];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = k0 + 32 * i < hi ? __ldcg(run_part + k0 + 32 * i) : 0.0;
+    for (int i = 0; i < kLongBatch; ++i)
+      v[i] = k0 + 32 * i < hi ? __ldcg(run_part + k0 + 32 * i) : 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kLongBatch; ++i)
       if (k0 + 32 * i < hi) acc += v[i];
   }
   acc = warp_sum(acc);
