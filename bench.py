@@ -331,7 +331,7 @@ def run_ours(args, world, rank, local, pg):
             e2e_sec += sec
     e2e_v = e2e_its / e2e_sec
     ndiag = len(off)
-    h2d = 8 * n * ndiag + 8 * n + 4 * n + 8 * n + 8 * n  # diagonals, M^-1, labels, b, x0
+    h2d = 8 * n * ndiag + 8 * n + 4 * n + 8 * n  # diagonals, M^-1, labels, b (x0 = 0: none)
     d2h = 8 * n + 8 * (case.max_iters + 1) + 4 * (case.max_iters + 1)
     # ---------------- CPU baseline (rank 0, N = 1) ---------------------------------------
     cpu = None

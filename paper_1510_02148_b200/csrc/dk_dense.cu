@@ -712,6 +712,7 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
   const int nslots = (int)jobs.size() + (int)tree.size() + 1;
   double* dpmin = nullptr;
   int2* djobs = nullptr;
+  double *X = nullptr, *T = nullptr;
   cudaMallocAsync(&dpmin, (size_t)nslots * sizeof(double), s);
   cudaMemsetAsync(dpmin, 0x7f, (size_t)nslots * sizeof(double), s);  // large positive
   if (!jobs.empty()) {
@@ -720,34 +721,10 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
     k_chol_diag<<<(unsigned)jobs.size(), 32 * DNW, kDiagSmem, s>>>(E, ld, 0, 0, W, dpmin, 0,
                                                                      djobs);
   }
-  // Independent subtrees run concurrently: nodes with a separator of at most DB labels (one
-  // factorisation CTA, no host synchronisation) go round-robin to auxiliary streams, larger
-  // ones to the caller's stream; every node first waits for its children's completion events.
-  // Each stream has its own X / T scratch.
-  constexpr int kAux = 3;
-  static cudaStream_t aux[64][kAux] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const bool concurrent = getenv("DK_SERIAL_TREE") == nullptr;
-  if (concurrent && aux[dev & 63][0] == nullptr)
-    for (auto& a : aux[dev & 63]) cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking);
-  cudaStream_t strm[kAux + 1] = {s, aux[dev & 63][0], aux[dev & 63][1], aux[dev & 63][2]};
-  const int nstrm = concurrent ? kAux + 1 : 1;
-  double* Xs[kAux + 1] = {};
-  double* Ts[kAux + 1] = {};
-  if (xmax > 0)
-    for (int k = 0; k < nstrm; ++k) {
-      cudaMallocAsync(&Xs[k], (size_t)xmax * sizeof(double), s);
-      cudaMallocAsync(&Ts[k], (size_t)xmax * sizeof(double), s);
-    }
-  std::vector<cudaEvent_t> done(tree.size(), nullptr);
-  cudaEvent_t start_ev = nullptr;
-  if (concurrent) {
-    cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming);
-    cudaEventRecord(start_ev, s);  // the leaves and the scratch allocations
-    for (int k = 1; k < nstrm; ++k) cudaStreamWaitEvent(strm[k], start_ev, 0);
+  if (xmax > 0) {
+    cudaMallocAsync(&X, (size_t)xmax * sizeof(double), s);
+    cudaMallocAsync(&T, (size_t)xmax * sizeof(double), s);
   }
-  int rr = 0;
   double host_min = INFINITY;
   int slot = (int)jobs.size();
   const bool trace = getenv("DK_TRACE_TREE") != nullptr;
@@ -758,24 +735,9 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
     cudaEventSynchronize(tev[0]);
   }
   auto t_start = std::chrono::steady_clock::now();
-  for (size_t ni = 0; ni < tree.size(); ++ni) {
-    const auto& n = tree[ni];
+  for (const auto& n : tree) {
     const int ns = n.s1 - n.s0, nd = n.s0 - n.t0;
     if (ns <= 0 || (nd == 0 && ns <= DB)) continue;
-    int si = 0;
-    if (concurrent && ns <= DB && !trace) si = 1 + (rr++ % kAux);
-    const cudaStream_t s = strm[si];  // this node's stream (shadows the caller's)
-    double* X = Xs[si];
-    double* T = Ts[si];
-    if (concurrent) {  // a child without work of its own (a component split) stands for its kids
-      std::vector<int> wait_on(n.kids.begin(), n.kids.end());
-      while (!wait_on.empty()) {
-        const int k = wait_on.back();
-        wait_on.pop_back();
-        if (done[k]) cudaStreamWaitEvent(s, done[k], 0);
-        else wait_on.insert(wait_on.end(), tree[k].kids.begin(), tree[k].kids.end());
-      }
-    }
     if (trace) cudaEventRecord(tev[1], s);
     if (nd > 0) {
       const int ldx = nd;
@@ -811,10 +773,6 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
     if (nd > 0)
       gemm_mma(false, false, at(W, n.s0, n.s0), ld, T, nd, at(W, n.s0, n.t0), ld, ns, nd, ns,
                -1.0, 0.0, 0, INT_MIN, s);
-    if (concurrent) {
-      cudaEventCreateWithFlags(&done[ni], cudaEventDisableTiming);
-      cudaEventRecord(done[ni], s);
-    }
     if (trace) {
       cudaEventRecord(tev[2], s);
       cudaEventSynchronize(tev[2]);
@@ -833,23 +791,14 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
             ms, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                           t_start).count());
   }
-  if (concurrent) {  // join: the caller's stream waits for every node
-    for (auto e : done)
-      if (e) cudaStreamWaitEvent(s, e, 0);
-  }
   std::vector<double> pm(slot > 0 ? slot : 1, INFINITY);
   if (slot > 0)
     cudaMemcpyAsync(pm.data(), dpmin, (size_t)slot * sizeof(double), cudaMemcpyDeviceToHost, s);
   const cudaError_t e = cudaStreamSynchronize(s);
   cudaFreeAsync(dpmin, s);
   if (djobs) cudaFreeAsync(djobs, s);
-  for (int k = 0; k < nstrm; ++k) {
-    if (Xs[k]) cudaFreeAsync(Xs[k], s);
-    if (Ts[k]) cudaFreeAsync(Ts[k], s);
-  }
-  for (auto e : done)
-    if (e) cudaEventDestroy(e);
-  if (start_ev) cudaEventDestroy(start_ev);
+  if (X) cudaFreeAsync(X, s);
+  if (T) cudaFreeAsync(T, s);
   double mn = host_min;
   for (int i = 0; i < slot; ++i) mn = (pm[i] != pm[i] || mn != mn) ? NAN : fmin(mn, pm[i]);
   *min_diag_sq = mn;

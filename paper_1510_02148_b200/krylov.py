@@ -155,7 +155,8 @@ class _Cycles:
         cout = _lib.CycleCtl()
         resume = self.ctl is not None
         rc = op._lib.dk_gmres_ex(op.h, ctx.h if ctx is not None else None, _lib.ptr(self.b),
-                                 None if resume else _lib.ptr(self.x0), int(m), float(self.tol),
+                                 None if resume or self.x0 is None else _lib.ptr(self.x0),
+                                 int(m), float(self.tol),
                                  int(self.max_iters), int(self.min_iters), _lib.ptr(self.x),
                                  _lib.ptr(self.hist), _lib.ptr(self.rof), _lib.ptr(hbar),
                                  _lib.ptr(gram), C.byref(info), C.byref(cin), C.byref(cout))
@@ -240,10 +241,9 @@ def gmres(A: SparseMatrix, b, x0=None, M: Preconditioner | None = None, m: int =
     b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
     if b.shape != (A.n,):
         raise ValueError("right-hand side has wrong length")
-    if x0 is None:
-        x0 = np.zeros(A.n)
-    x0 = np.ascontiguousarray(np.asarray(x0, dtype=np.float64))
-    if x0.shape != (A.n,):
+    if x0 is not None:  # None: the device starts from zeros (no upload)
+        x0 = np.ascontiguousarray(np.asarray(x0, dtype=np.float64))
+    if x0 is not None and x0.shape != (A.n,):
         raise ValueError("initial guess has wrong length")
     if M is None:
         M = Preconditioner.identity()
