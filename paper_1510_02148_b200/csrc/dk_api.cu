@@ -546,6 +546,10 @@ void issue_restart(dk_op* op, dk_defl* c) {
 int read_state(dk_op* op);
 
 void issue_iteration(dk_op* op, dk_defl* c, int j) {
+  // an event-profiled (launch-per-kernel) solve serialises the kernel boundaries, so each
+  // kernel's event time is its own (no early start across the control tails)
+  Scal sc = op->sc;
+  if (op->prof) sc.post = nullptr;
   State* st = op->st;
   const bool pre = op->inv != nullptr;
   const bool am = c && c->ap == DK_AP_AM;
@@ -557,27 +561,27 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   const double pro_bytes = !c ? 0.0 : c->dense ? 8.0 * c->d * n
                                                : 37.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
   // from the second iteration of a cycle on, the stencil starts on k_gs's published sigma
-  const unsigned* wait = (op->sc.post != nullptr && j >= 1) ? op->sc.post + (j - 1) : nullptr;
+  const unsigned* wait = (sc.post != nullptr && j >= 1) ? sc.post + (j - 1) : nullptr;
   if (c) {
-    coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, op->sc.sigma + j,
+    coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, sc.sigma + j,
                  nullptr, op->w, &st->active, wait);
   } else {
     ProfScope ps(op, PC_STENCIL, (8.0 * op->nstore + (pre ? 24.0 : 16.0)) * n);
     launch_stencil(ST_APPLY, pre, true, A, op->n_pad, V + (long long)j * op->vstride,
-                   op->sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream, wait,
-                   op->sc.gpart_gs, op->sc.ng);
+                   sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream, wait,
+                   sc.gpart_gs, sc.ng);
   }
   {
     ProfScope ps(op, PC_PROJECT,
                  c ? (24.0 + 8.0 * nvec) * n + pro_bytes : (16.0 + 8.0 * nvec) * n);
     launch_project(PJ_ITER, defl_kind(c), am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
-                   op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j,
+                   op->w, op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G, sc, j,
                    &st->active, op->stream);
   }
   {
     ProfScope ps(op, PC_GS, (16.0 + 8.0 * nvec) * n);
     launch_gs(false, op->w, V + (long long)(j + 1) * op->vstride, V, op->vstride, nvec,
-              op->n_pad, op->part, op->G, op->sc, j, &st->active, op->gs_fuse, op->stream);
+              op->n_pad, op->part, op->G, sc, j, &st->active, op->gs_fuse, op->stream);
   }
   if (op->gs_fuse) return;  // the second pass, when needed, runs inside k_gs
   // second Gram-Schmidt pass, gated on the device-side test (krylov.py:167-170)
@@ -588,9 +592,9 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
     ProfScope ps(op, PC_REORTH, (16.0 + 16.0 * nvec) * n);
     launch_project(PJ_REDOTS, DK_NONE, false, A, Prolong{}, nullptr,
                    V + (long long)(j + 1) * op->vstride, nullptr, V, op->vstride, nvec, op->n_pad,
-                   op->part, op->G, op->sc, j, &st->reorth, op->stream);
+                   op->part, op->G, sc, j, &st->reorth, op->stream);
     launch_gs(true, V + (long long)(j + 1) * op->vstride, V + (long long)(j + 1) * op->vstride, V,
-              op->vstride, nvec, op->n_pad, op->part, op->G, op->sc, j, &st->reorth, false,
+              op->vstride, nvec, op->n_pad, op->part, op->G, sc, j, &st->reorth, false,
               op->stream);
   }
 }
