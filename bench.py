@@ -11,10 +11,12 @@ seeded inputs (paper_1510_02148_b200/configs.py).
   e2e       the same metric through the public API `pdgmres` with HOST numpy buffers: operator
             upload, deflation setup (E assembly, LU, E^-1, x*), solve and x download per step
   roofline  the dominant kernel class of an event-profiled solve: algorithmic bytes / time
-  cpu_baseline  the CPU oracle port (oracle/dk_oracle.py) on a bounded sample, rank 0, N = 1
+  cpu_baseline  the reference solver on the host cores (CpuReference), rank 0, N = 1
 
---impl reference times the CPU port of the reference algorithm with all host threads on a
-bounded sample of the same workload (10 GMRES iterations per step).
+--impl reference times the reference's own `_run_cycles` (the unmodified package installed
+under baseline/_ref) with all host threads, one GMRES(m) cycle per step, on the same
+workload, with inputs and labels built without the device library (no libdk.so in the
+process; the JSON line lists the repo .so files mapped, which must be none).
 Multi-GPU: the path does not shard (BASELINE north_star: one GPU), so N ranks run N
 independent replicas (weak scaling, no collective on the data path).
 """
@@ -144,61 +146,132 @@ def barrier(pg):
 
 
 # ---------------------------------------------------------------------------------------
-def cpu_port_rate(case, A, b, basis, max_iters: int, threads: int):
-    """The CPU port (oracle) on a bounded sample: returns (iters/s, iterations, seconds)."""
-    from threadpoolctl import threadpool_limits
-    from oracle import dk_oracle as O
-    off, dg = A.dia()
-    Ac = O.csr_from_dia(A.n, off, dg)
-    inv = 1.0 / dg[list(off).index(0)]
-    defl = O.LabelDeflation(Ac, basis.labels, basis.d, b, inv)
-    with threadpool_limits(threads):
-        t = time.perf_counter()
-        r = O.run_cycles(Ac, b, None, inv, case.m, case.tol, max_iters, 0, defl)
-        sec = time.perf_counter() - t
-    return r["iterations"] / sec, r["iterations"], sec
+def load_reference():
+    """The unmodified reference package (`defkrylov`, pure Python) installed under
+    baseline/_ref by `pip install --target baseline/_ref`; None if absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "defkrylov" / "__init__.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import defkrylov
+    return defkrylov
+
+
+def native_libs_loaded():
+    """Shared objects of this repo mapped into the process (the reference arm must have none)."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1] for ln in maps
+                   if ln.endswith(".so") and str(ROOT) in ln and "baseline/_ref" not in ln})
+
+
+def config_dict(case, idx: int, n: int, d: int, seed: int, world: int) -> dict:
+    """The workload description; identical in both arms (`same_config`)."""
+    vmb = (case.m + 1) * 8.0 * n / 1e6
+    return {"workload": case.name, "config_index": idx, "n_cells": n,
+            "d": d, "m": case.m, "tol": case.tol, "seed": seed,
+            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "l2": (f"inputs larger than L2: the basis V alone is {vmb:.0f} MB and every "
+                   f"iteration streams hundreds of MB (126 MB L2), no flush needed"
+                   if vmb > 126 else
+                   f"L2-resident working set (V = {vmb:.0f} MB < 126 MB L2, not flushed): "
+                   f"a latency measurement, not the BASELINE workload")}
+
+
+class CpuReference:
+    """The reference solver on the host cores, built without the device library.
+
+    Inputs: the seeded k field (configs.py generator, numpy), the host TPFA assembly
+    (bit-identical to the reference's assemble_pressure, tests/test_testbed.py) and labels
+    from the oracle's labeller (pinned to the reference's label CRCs).  Solver: the
+    reference's own `_run_cycles` (krylov.py:107-236) from baseline/_ref with the
+    label-based context of SURVEY.md §0.3 (O.ReferenceLabelContext: R.spmv, R.dense_lu,
+    R.lu_solve), or — when baseline/_ref is missing — the oracle port (oracle/dk_oracle.py).
+    One step = one GMRES(m) cycle (m iterations) from x0 = 0, plus the reference's
+    reconstruct and true-residual epilogue.
+    """
+
+    def __init__(self, case, idx: int, A=None, b=None):
+        from oracle import dk_oracle as O
+        self.O = O
+        self.case = case
+        self.idx = idx
+        t0 = time.perf_counter()
+        if A is None:
+            A, b = case.problem()
+        off, dg = A.dia()
+        self.n = A.n
+        self.b = b
+        Ac = O.csr_from_dia_lean(A.n, off, dg)
+        g = case.grid
+        px, py, pz = case.boxes
+        lab, d, excl = O.subdomain_levelset_labels_boxwise(
+            case.band_field.kx, g.nx, g.ny, g.nz, px, py, pz, case.jump_threshold)
+        col, self.d = O.columns_from_labels(lab, d, excl)
+        self.R = load_reference()
+        if self.R is not None:
+            R = self.R
+            self.kind = "reference"
+            self.A = R.SparseMatrix(A.n, Ac.indptr, Ac.indices, Ac.data)
+            self.M = R.Preconditioner.jacobi(self.A)
+            self.ctx = O.ReferenceLabelContext(R, self.A, col, self.d, b)
+            from defkrylov.krylov import _run_cycles
+            self._run = _run_cycles
+        else:
+            self.kind = "port"
+            self.A = Ac
+            self.inv = 1.0 / dg[list(off).index(0)]
+            self.ctx = O.LabelDeflation(Ac, col, self.d, b, self.inv)
+        self.setup_s = time.perf_counter() - t0
+
+    def cycle(self) -> int:
+        c = self.case
+        if self.kind == "reference":
+            rep = self._run(self.A, self.b, np.zeros(self.n), self.M, c.m, c.tol, c.m, 0,
+                            self.ctx, None, False)
+            return int(rep.iterations)
+        r = self.O.run_cycles(self.A, self.b, None, self.inv, c.m, c.tol, c.m, 0, self.ctx)
+        return int(r["iterations"])
+
+    def sample(self, steps: int) -> str:
+        what = ("the reference's own _run_cycles (baseline/_ref defkrylov, krylov.py:107-236)"
+                " with a label-based deflation context" if self.kind == "reference" else
+                "the oracle port of _run_cycles (baseline/_ref not installed)")
+        return (f"{steps} x one GMRES({self.case.m}) cycle ({self.case.m} iterations) of "
+                f"config {self.idx} from x0=0: {what}, d={self.d}; set-up "
+                f"(operator, labels, E + LU, x*) {self.setup_s:.1f}s excluded")
 
 
 def run_reference_arm(args, world, rank):
-    """--impl reference: the CPU port of the reference algorithm, all host threads."""
+    """--impl reference: the reference solver on the host cores, rank 0 only."""
     if rank != 0:
         return
     threads = host_threads()
     from threadpoolctl import threadpool_limits
     threadpool_limits(threads)
-    from oracle import dk_oracle as O
     from paper_1510_02148_b200 import configs
-    from paper_1510_02148_b200.physics import partition_to_basis
-    case = configs.make_case(args.config)
-    A, b = case.problem()
-    basis = partition_to_basis(case.partition())
-    off, dg = A.dia()
-    Ac = O.csr_from_dia(A.n, off, dg)
-    inv = 1.0 / dg[list(off).index(0)]
-    t0 = time.perf_counter()
-    defl = O.LabelDeflation(Ac, basis.labels, basis.d, b, inv)
-    setup = time.perf_counter() - t0
-    per_step = args.ref_iters
+    case = configs.make_case(args.config, seed=args.seed)
+    ref = CpuReference(case, args.config)
     for _ in range(args.warmup):
-        O.run_cycles(Ac, b, None, inv, case.m, case.tol, per_step, 0, defl)
+        ref.cycle()
     its = 0
     t = time.perf_counter()
     for _ in range(args.steps):
-        its += O.run_cycles(Ac, b, None, inv, case.m, case.tol, per_step, 0, defl)["iterations"]
+        its += ref.cycle()
     sec = time.perf_counter() - t
     v = its / sec
-    sample = (f"{per_step} GMRES({case.m}) iterations of config {args.config} from x0=0 per "
-              f"step (label-based deflation, d={basis.d}); setup {setup:.1f}s excluded")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": case.name, "config_index": args.config,
-                                        "n_cells": A.n, "d": basis.d, "m": case.m,
-                                        "tol": case.tol, "l2": "n/a (CPU)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+        "data": "synthetic", "config": config_dict(case, args.config, ref.n, ref.d, args.seed, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": ref.kind,
+                         "sample": ref.sample(args.steps)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_libs_loaded": native_libs_loaded(),
     }), flush=True)
 
 
@@ -337,22 +410,22 @@ def run_ours(args, world, rank, local, pg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = host_threads()
-        v, ci, cs = cpu_port_rate(case, A, b, basis, args.cpu_iters, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"first {ci} GMRES({case.m}) iterations of config {args.config} from "
-                         f"x0=0 ({cs:.1f}s, label-based oracle, d={basis.d}, setup excluded)"}
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(threads):
+            ref = CpuReference(case, args.config, A, b)
+            ref.cycle()  # warm-up
+            t = time.perf_counter()
+            ci = sum(ref.cycle() for _ in range(args.cpu_cycles))
+            cs = time.perf_counter() - t
+        cpu = {"value": ci / cs, "unit": UNIT, "cores": threads, "kind": ref.kind,
+               "sample": ref.sample(args.cpu_cycles)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": case.name, "config_index": args.config, "n_cells": n,
-                       "d": basis.d, "m": case.m, "tol": case.tol, "seed": args.seed,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": f"inputs larger than L2 (per-iteration stream "
-                             f"{bytes_per_iter / 1e6:.0f} MB on average; the basis V alone "
-                             f"{(case.m + 1) * 8.0 * n / 1e6:.0f} MB; no flush needed)"},
+            "config": config_dict(case, args.config, n, basis.d, args.seed, world),
             "iterations_per_solve": iters_per_solve, "converged": converged,
             "final_relres": relres, "time_to_solve_s": ms_max * 1e-3 / args.steps,
             "setup_s": setup_s, "setup_ms": setup_ms,
@@ -378,8 +451,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-iters", type=int, default=50)
-    ap.add_argument("--ref-iters", type=int, default=10)
+    ap.add_argument("--cpu-cycles", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -14,7 +14,7 @@
  *   dk_gmres                         <- _run_cycles via gmres / pdgmres
  *                                                                    (krylov.py:107-266,
  *                                                                     physics.py:183-198)
- *   dk_levelset_labels               <- subdomain_levelset_partition / levelset_partition
+ *   dk_levelset_labels_device        <- subdomain_levelset_partition / levelset_partition
  *                                       (6-connected components + first-occurrence order)
  *                                                                    (physics.py:44-143)
  *
@@ -172,16 +172,12 @@ int dk_last_basis_vector(dk_op* op, int32_t i, double* out);
 /* ---- deflation-vector construction ------------------------------------------------ */
 /* Labels of the 6-connected components of equal `band` value inside each subdomain box
  * (px x py x pz near-equal boxes, remainders to the leading blocks; physics.py:57-78),
- * numbered by first occurrence in linear cell order ix + nx*(iy + ny*iz).  band is int64
- * per cell (-1 = zero-permeability band).  Writes labels[n], *ncomp, and
- * comp_band[ncomp] (the band of each component, capacity n).  Host pointers. */
-int dk_levelset_labels(int64_t nx, int64_t ny, int64_t nz, const int64_t* band, int32_t px,
-                       int32_t py, int32_t pz, int64_t* labels, int64_t* ncomp,
-                       int64_t* comp_band);
-
-/* The same labels computed on the current device (lock-free union-find whose roots are the
- * component minima, then a prefix scan over the roots); bit-identical to dk_levelset_labels.
- * Pointers may be host or device memory. */
+ * numbered by first occurrence in linear cell order ix + nx*(iy + ny*iz)
+ * (physics.py:44-54, 119-143).  band is int64 per cell (-1 = zero-permeability band).
+ * Writes labels[n], *ncomp, and comp_band[ncomp] (the band of each component, capacity n).
+ * Computed on the current device: lock-free union-find whose roots are the component
+ * minima, then a prefix scan over the roots.  Pointers may be host or device memory.
+ * Without a device: DK_ECUDA (no host fallback). */
 int dk_levelset_labels_device(int64_t nx, int64_t ny, int64_t nz, const int64_t* band,
                               int32_t px, int32_t py, int32_t pz, int64_t* labels,
                               int64_t* ncomp, int64_t* comp_band);

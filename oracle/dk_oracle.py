@@ -49,6 +49,59 @@ def csr_from_dia(n, offsets, diags) -> scipy.sparse.csr_matrix:
     return A
 
 
+def csr_from_dia_lean(n, offsets, diags) -> scipy.sparse.csr_matrix:
+    """csr_from_dia without the O(nnz) int64 coordinate lists (BASELINE configs 4 and 5).
+
+    Same stored entries in the same (sorted) column order: each row keeps its nonzero
+    off-diagonals and its diagonal (testbed.py:160-211 stores exactly the couplings t > 0
+    plus the diagonal).  Peak memory is the CSR itself plus one n-vector per pass.
+    """
+    order = np.argsort(np.asarray(offsets))
+    offsets = np.asarray(offsets)[order]
+    i = np.arange(n)
+    keep = []
+    for k, o in zip(order, offsets):
+        ok = (i + o >= 0) & (i + o < n) & ((diags[k] != 0.0) | (o == 0))
+        keep.append(ok)
+    counts = np.zeros(n, dtype=np.int64)
+    for ok in keep:
+        counts += ok
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    nnz = int(indptr[-1])
+    idx_t = np.int32 if nnz < 2**31 and n < 2**31 else np.int64
+    indices = np.empty(nnz, dtype=idx_t)
+    data = np.empty(nnz, dtype=np.float64)
+    pos = indptr[:-1].copy()
+    for (k, o), ok in zip(zip(order, offsets), keep):
+        rows = np.flatnonzero(ok)
+        p = pos[rows]
+        indices[p] = (rows + o).astype(idx_t)
+        data[p] = diags[k][rows]
+        pos[rows] += 1
+    A = scipy.sparse.csr_matrix((data, indices, indptr.astype(idx_t)), shape=(n, n))
+    A.has_sorted_indices = True
+    return A
+
+
+def sketch(x, rows: int = 16, seed: int = 20251020, chunk: int = 1 << 22):
+    """Johnson-Lindenstrauss sketch S x with S a seeded n-column Rademacher matrix (±1).
+
+    For any vector e, mean((S e)_i^2) is an unbiased estimate of |e|_2^2 (rows = 16: the
+    estimate is within a factor 2 with probability > 0.99), so |S(x - x_ref)| / sqrt(rows)
+    estimates the full-vector 2-norm difference from 16 stored numbers when x_ref is too
+    large to commit (BASELINE configs 4 and 5).  Chunked, so any n fits.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    out = np.zeros(rows)
+    rng = np.random.default_rng(seed)
+    for lo in range(0, len(x), chunk):
+        xs = x[lo:lo + chunk]
+        s = rng.integers(0, 2, size=(rows, len(xs)), dtype=np.int8).astype(np.float64)
+        out += (2.0 * s - 1.0) @ xs
+    return out
+
+
 # ---------------------------------------------------------------------------------------
 # deflation context (deflation.py:40-89, label form)
 # ---------------------------------------------------------------------------------------
@@ -63,11 +116,17 @@ class LabelDeflation:
         # A_p = A or A M^-1 (deflation.py:50-51): column scaling by inv_diag
         Ap = A if ap == "A" else (A @ scipy.sparse.diags(inv_diag)).tocsr()
         self.Ap = Ap
-        coo = Ap.tocoo()
-        lr, lc = self.lab[coo.row], self.lab[coo.col]
-        ok = (lr >= 0) & (lc >= 0)
-        E = np.zeros((self.d, self.d))
-        np.add.at(E, (lr[ok], lc[ok]), coo.data[ok])
+        # E = sum of A_p's nonzeros by (label_row, label_col), in row blocks (bounded memory)
+        E = np.zeros(self.d * self.d)
+        n = Ap.shape[0]
+        step = 1 << 22
+        for r0 in range(0, n, step):
+            blk = Ap[r0:min(n, r0 + step)].tocoo()
+            lr, lc = self.lab[blk.row + r0], self.lab[blk.col]
+            ok = (lr >= 0) & (lc >= 0)
+            E += np.bincount(lr[ok] * self.d + lc[ok], weights=blk.data[ok],
+                             minlength=self.d * self.d)
+        E = E.reshape(self.d, self.d)
         self.E = E
         # dense_lu (sparse.py:121-137)
         lu, piv = scipy.linalg.lu_factor(E, check_finite=True)
@@ -297,6 +356,60 @@ def subdomain_levelset_labels(kx, nx, ny, nz, px, py, pz, thr):
     return labels, len(ids), excl
 
 
+def subdomain_levelset_labels_boxwise(kx, nx, ny, nz, px, py, pz, thr):
+    """The same labels as subdomain_levelset_labels, one ndimage.label per box sub-volume.
+
+    physics.py:119-143 labels `in_box & band == b` on the full grid; every component of that
+    mask lies inside the box, so labelling the box's sub-volume finds the same components.
+    A box is a product of index ranges, so its C-order ravel visits cells in increasing
+    linear index: a component's first cell in the sub-volume is its minimum linear index,
+    which is what _relabel_by_first_occurrence (physics.py:44-54) orders by.  Returns
+    (labels int64, d, excluded ids).  O(n): seconds at BASELINE configs 4 and 5, where the
+    full-grid form takes an hour.
+    """
+    band = band_ids(kx, thr).reshape(nz, ny, nx)
+    st = ndimage.generate_binary_structure(3, 1)
+
+    def bounds(nc, p):
+        sizes = np.full(p, nc // p)
+        sizes[:nc % p] += 1
+        return np.concatenate([[0], np.cumsum(sizes)])
+
+    bx, by, bz = bounds(nx, px), bounds(ny, py), bounds(nz, pz)
+    comp = np.empty((nz, ny, nx), dtype=np.int64)     # global component id per cell
+    first, zero = [], []                              # per component: min linear index, band
+    lin_box = None
+    nxt = 0
+    for kz in range(pz):
+        for ky in range(py):
+            for kx_ in range(px):
+                sl = np.s_[bz[kz]:bz[kz + 1], by[ky]:by[ky + 1], bx[kx_]:bx[kx_ + 1]]
+                sub = band[sl]
+                lin_box = (np.arange(bx[kx_], bx[kx_ + 1])[None, None, :]
+                           + nx * (np.arange(by[ky], by[ky + 1])[None, :, None]
+                                   + ny * np.arange(bz[kz], bz[kz + 1])[:, None, None]))
+                out = np.empty(sub.shape, dtype=np.int64)
+                for bnd in np.unique(sub):
+                    lab, nc = ndimage.label(sub == bnd, structure=st)
+                    if nc == 0:
+                        continue
+                    flat = lab.ravel()
+                    sel = flat > 0
+                    ids, idx = np.unique(flat[sel], return_index=True)
+                    first.append(lin_box.ravel()[np.flatnonzero(sel)[idx]])
+                    zero.append(np.full(nc, bnd == -1))
+                    out[lab > 0] = lab[lab > 0] - 1 + nxt
+                    nxt += nc
+                comp[sl] = out
+    first = np.concatenate(first)
+    zero = np.concatenate(zero)
+    rank = np.empty(nxt, dtype=np.int64)
+    rank[np.argsort(first, kind="stable")] = np.arange(nxt)
+    labels = rank[comp.ravel()]
+    excl = {int(r) for r in rank[zero]}
+    return labels, nxt, excl
+
+
 def columns_from_labels(labels, d, exclude):
     """partition_to_basis column map (physics.py:167-180): kept labels in order, -1 else."""
     keep = np.ones(d, dtype=bool)
@@ -305,3 +418,56 @@ def columns_from_labels(labels, d, exclude):
     col = np.full(d, -1, dtype=np.int64)
     col[keep] = np.arange(int(keep.sum()))
     return col[labels], int(keep.sum())
+
+
+# ---------------------------------------------------------------------------------------
+# the reference's own solver on a label-based context (bench.py's reference arm)
+# ---------------------------------------------------------------------------------------
+class ReferenceLabelContext:
+    """Duck-typed deflation context for the REFERENCE's `_run_cycles`.
+
+    `_run_cycles` (krylov.py:107-236) only calls ctx.apply_p1 and ctx.reconstruct; this
+    context provides them in label form with the reference's own kernels — R.spmv
+    (sparse.py:101-106), R.dense_lu / R.lu_solve (sparse.py:121-145) — where the shipped
+    DeflationContext (deflation.py:40-68) would need a dense n x d Z (98 GB at BASELINE
+    config 3).  Restriction Z^T v = bincount(labels, v); prolongation A Z y = spmv(A,
+    y[labels]); E = Z^T A Z from A's nonzeros by label pair; x* = Z E^-1 Z^T b.
+    """
+
+    def __init__(self, R, A, col_labels, d, b):
+        self.R = R
+        self.A = A
+        self.lab = np.asarray(col_labels, dtype=np.int64)
+        self.keep = self.lab >= 0
+        self.d = int(d)
+        csr = scipy.sparse.csr_matrix((A.values, A.col_indices, A.row_offsets),
+                                      shape=(A.n, A.n))
+        E = np.zeros(self.d * self.d)
+        step = 1 << 22
+        for r0 in range(0, A.n, step):
+            blk = csr[r0:min(A.n, r0 + step)].tocoo()
+            lr, lc = self.lab[blk.row + r0], self.lab[blk.col]
+            ok = (lr >= 0) & (lc >= 0)
+            E += np.bincount(lr[ok] * self.d + lc[ok], weights=blk.data[ok],
+                             minlength=self.d * self.d)
+        self.E_lu = R.dense_lu(E.reshape(self.d, self.d))
+        self.x_star = self._prolong(R.lu_solve(self.E_lu, self._restrict(b)))
+
+    def _restrict(self, v):
+        return np.bincount(self.lab[self.keep], weights=v[self.keep], minlength=self.d)
+
+    def _prolong(self, y):
+        out = np.zeros(len(self.lab))
+        out[self.keep] = y[self.lab[self.keep]]
+        return out
+
+    def apply_p1(self, v):
+        R = self.R
+        return v - R.spmv(self.A, self._prolong(R.lu_solve(self.E_lu, self._restrict(v))))
+
+    def apply_p2(self, v):
+        R = self.R
+        return v - self._prolong(R.lu_solve(self.E_lu, self._restrict(R.spmv(self.A, v))))
+
+    def reconstruct(self, xh):
+        return self.x_star + self.apply_p2(xh)

@@ -5,7 +5,8 @@
 Writes tests/golden/*.npz.  Inputs are built with this repo's seeded generators (so the GPU
 box can rebuild them without the reference); every output is produced by the reference's
 own public API (defkrylov.pdgmres / gmres / assemble_pressure / subdomain_levelset_partition).
-`--big` also runs config 2 (dense-Z reference, ~30 s, ~6 GB) and the config-3 partition.
+`--big` also runs config 2 (dense-Z reference, ~30 s, ~6 GB) and the config-3 partition;
+`--labels 4 5` runs the reference partition of configs 4 and 5 (config5: about an hour).
 """
 from __future__ import annotations
 
@@ -143,7 +144,8 @@ def make_config2():
     t_pd = time.time() - t
     np.savez_compressed(
         HERE / "config2.npz", labels_crc=crc(part.labels.astype(np.int64)), d=part.d,
-        pd_history=rep.residual_history, pd_x_sample=rep.x[::97], pd_x_norm=np.linalg.norm(rep.x),
+        pd_history=rep.residual_history, pd_x=rep.x, pd_x_sample=rep.x[::97],
+        pd_x_norm=np.linalg.norm(rep.x),
         pd_iters=rep.iterations, pd_relres=rep.final_relres, seconds=t_pd)
     print(f"config2: d={part.d} pdgmres {rep.iterations} it ({t_pd:.1f}s)")
 
@@ -159,6 +161,29 @@ def make_config3_labels():
                         d=part.d, nexcl=len(part.default_exclude), seconds=sec,
                         sizes_head=np.bincount(part.labels)[:64])
     print(f"config3 labels: d={part.d} ({sec:.1f}s)")
+
+
+def make_labels_big(idx):
+    """Reference labels at BASELINE configs 4 and 5 (physics.py:119-143, run as shipped).
+
+    The reference labels each (box, band) with ndimage.label on the full grid and renumbers
+    in a Python loop over n cells: minutes at config 4, about an hour at config 5.  Stores
+    the CRC of the int64 label vector, d, the excluded ids and every column's cell count.
+    """
+    case = configs.make_case(idx)
+    fb = case.band_field
+    g = case.grid
+    fr = R.PermeabilityField(R.Grid(g.nx, g.ny, g.nz, g.dx, g.dy, g.dz), fb.kx, fb.ky, fb.kz)
+    px, py, pz = case.boxes
+    t = time.time()
+    part = R.subdomain_levelset_partition(fr, px, py, pz, case.jump_threshold)
+    sec = time.time() - t
+    np.savez_compressed(HERE / f"config{idx}_labels.npz",
+                        labels_crc=crc(part.labels.astype(np.int64)), d=part.d,
+                        excl=np.array(sorted(part.default_exclude), dtype=np.int64),
+                        nexcl=len(part.default_exclude), seconds=sec,
+                        sizes=np.bincount(part.labels, minlength=part.d))
+    print(f"config{idx} labels: d={part.d} excl={len(part.default_exclude)} ({sec:.1f}s)")
 
 
 def make_harmonic():
@@ -216,6 +241,13 @@ def make_harmonic():
 
 
 if __name__ == "__main__":
+    if "--config2" in sys.argv:
+        make_config2()
+        sys.exit(0)
+    if "--labels" in sys.argv:
+        for i in sys.argv[sys.argv.index("--labels") + 1:]:
+            make_labels_big(int(i))
+        sys.exit(0)
     make_sandwich()
     make_random_hetero()
     make_config1()

@@ -53,14 +53,16 @@ def test_no_device_means_loud_failure():
     assert rc == _lib.DK_ECUDA and "no CUDA device" in _lib.last_error()
 
 
-def test_labels_entry_point_rejects_bad_boxes():
+def test_labels_entry_point_validates_then_needs_a_device():
     lib = _lib.load()
     band = np.zeros(8, dtype=np.int64)
     out = np.empty(8, dtype=np.int64)
     cb = np.empty(8, dtype=np.int64)
     n = C.c_int64()
-    assert lib.dk_levelset_labels(2, 2, 2, band.ctypes.data, 3, 1, 1, out.ctypes.data,
-                                  C.byref(n), cb.ctypes.data) == _lib.DK_EINVAL
-    assert lib.dk_levelset_labels(2, 2, 2, band.ctypes.data, 2, 2, 2, out.ctypes.data,
-                                  C.byref(n), cb.ctypes.data) == _lib.DK_OK
-    assert n.value == 8 and list(out) == list(range(8))
+    assert lib.dk_levelset_labels_device(2, 2, 2, band.ctypes.data, 3, 1, 1, out.ctypes.data,
+                                         C.byref(n), cb.ctypes.data) == _lib.DK_EINVAL
+    if _lib.device_count() == 0:
+        assert lib.dk_levelset_labels_device(2, 2, 2, band.ctypes.data, 2, 2, 2,
+                                             out.ctypes.data, C.byref(n),
+                                             cb.ctypes.data) == _lib.DK_ECUDA
+        assert "no CUDA device" in _lib.last_error()

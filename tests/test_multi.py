@@ -67,14 +67,15 @@ def test_reference_arm_nonzero_ranks_exit_without_work(monkeypatch):
 
 def test_reference_arm_json_contract():
     """`bench.py --impl reference` prints the driver's JSON line (metric / unit / config of our
-    arm, impl, cpu_baseline, e2e with zero transfer bytes) using the oracle port on the host."""
+    arm, impl, cpu_baseline, e2e with zero transfer bytes) by running the reference's own
+    solver on the host, with no repo .so mapped into the process."""
     import json
     import subprocess
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1",
-                          "--steps", "1", "--warmup", "1", "--ref-iters", "2"], cwd=root,
+                          "--steps", "1", "--warmup", "0"], cwd=root,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -83,6 +84,7 @@ def test_reference_arm_json_contract():
     assert j["impl"] == "reference" and j["unit"] == "iters/s" and j["value"] > 0
     assert j["higher_is_better"] is True and j["n_gpus"] == 1
     assert j["config"]["config_index"] == 1
-    assert j["cpu_baseline"]["kind"] == "port" and j["cpu_baseline"]["cores"] >= 1
+    assert j["cpu_baseline"]["kind"] in ("reference", "port") and j["cpu_baseline"]["cores"] >= 1
+    assert j["native_libs_loaded"] == []
     assert j["e2e"]["value"] == j["value"]
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0

@@ -1,12 +1,8 @@
 """Device set-up paths (labels, TPFA assembly) and the reference CSV/summary formats."""
 from __future__ import annotations
 
-import zlib
-
 import numpy as np
 import pytest
-from hypothesis import given, settings
-from hypothesis import strategies as st
 
 import paper_1510_02148_b200 as dk
 from conftest import GOLDEN
@@ -37,48 +33,6 @@ def test_summary_line_format():
 
 
 # ---- device set-up (GPU) ------------------------------------------------------------------
-@pytest.mark.gpu
-@pytest.mark.parametrize("idx,name", [(2, "config2"), (3, "config3_labels")])
-def test_device_labels_match_reference_crc(gpu, golden, idx, name):
-    g = golden(name)
-    c = configs.make_case(idx)
-    px, py, pz = c.boxes
-    p = dk.subdomain_levelset_partition(c.band_field, px, py, pz, c.jump_threshold,
-                                        backend="device")
-    assert p.d == int(g["d"])
-    assert zlib.crc32(np.ascontiguousarray(p.labels.astype(np.int64)).tobytes()) == \
-        int(g["labels_crc"])
-
-
-@pytest.mark.gpu
-@settings(max_examples=25, deadline=None)
-@given(st.integers(0, 2**31 - 1), st.integers(1, 4), st.integers(1, 3), st.integers(1, 3))
-def test_device_labels_equal_host_labels(gpu, seed, px, py, pz):
-    rng = np.random.default_rng(seed)
-    nx, ny, nz = int(rng.integers(px, 17)), int(rng.integers(py, 11)), int(rng.integers(pz, 9))
-    n = nx * ny * nz
-    kx = 10.0 ** rng.integers(-3, 3, n).astype(float)
-    kx[rng.random(n) < 0.1] = 0.0
-    f = dk.PermeabilityField(dk.Grid(nx, ny, nz), kx, kx, kx)
-    a = dk.subdomain_levelset_partition(f, px, py, pz, 1.0, backend="device")
-    b = dk.subdomain_levelset_partition(f, px, py, pz, 1.0, backend="host")
-    np.testing.assert_array_equal(a.labels, b.labels)
-    assert a.d == b.d and a.default_exclude == b.default_exclude
-
-
-@pytest.mark.gpu
-def test_device_labels_large_grid(gpu):
-    """Config 4 (16.8 M cells): device and host union-find agree bit for bit."""
-    c = configs.make_case(4)
-    px, py, pz = c.boxes
-    a = dk.subdomain_levelset_partition(c.band_field, px, py, pz, c.jump_threshold,
-                                        backend="device")
-    b = dk.subdomain_levelset_partition(c.band_field, px, py, pz, c.jump_threshold,
-                                        backend="host")
-    assert a.d == b.d
-    np.testing.assert_array_equal(a.labels, b.labels)
-
-
 @pytest.mark.gpu
 def test_device_assembly_bit_identical(gpu, golden):
     g = golden("hetero")
