@@ -14,6 +14,7 @@
  *   dk_gmres                         <- _run_cycles via gmres / pdgmres
  *                                                                    (krylov.py:107-266,
  *                                                                     physics.py:183-198)
+ *   dk_dense_lu / dk_lu_solve        <- dense_lu / lu_solve          (sparse.py:109-145)
  *   dk_levelset_labels_device        <- subdomain_levelset_partition / levelset_partition
  *                                       (6-connected components + first-occurrence order)
  *                                                                    (physics.py:44-143)
@@ -181,6 +182,20 @@ int dk_last_basis_vector(dk_op* op, int32_t i, double* out);
 int dk_levelset_labels_device(int64_t nx, int64_t ny, int64_t nz, const int64_t* band,
                               int32_t px, int32_t py, int32_t pz, int64_t* labels,
                               int64_t* ncomp, int64_t* comp_band);
+
+/* ---- dense LU (the reference's public LU helpers) ------------------------------------ */
+/* dense_lu (sparse.py:121-137): P A = L U with partial pivoting on the device.  a is n x n
+ * row-major; lu receives the combined factors in LAPACK getrf's layout (unit L strictly
+ * below the diagonal, U on and above it, row-major) and piv[k] the 0-based row interchanged
+ * with row k (scipy.linalg.lu_factor's convention).  *min_pivot (may be NULL) = min |U_kk|.
+ * Returns DK_ESINGULAR when min |U_kk| < 1e-300 (factors are still written).
+ * Host or device pointers. */
+int dk_dense_lu(int64_t n, const double* a, double* lu, int32_t* piv, double* min_pivot);
+/* lu_solve (sparse.py:140-145): X = A^-1 B from dk_dense_lu's factors (getrs: row
+ * interchanges, unit-lower then upper triangular solves on the device).  b and x are
+ * n x nrhs row-major (numpy's stacked right-hand sides); x may alias b. */
+int dk_lu_solve(int64_t n, const double* lu, const int32_t* piv, int64_t nrhs, const double* b,
+                double* x);
 
 /* ---- operator assembly ------------------------------------------------------------- */
 /* TPFA pressure operator on the device (testbed.py:133-211 arithmetic): diags_out is 7 x n

@@ -29,7 +29,7 @@ EXPORTS = (
     "dk_defl_reconstruct", "dk_defl_x_star", "dk_defl_coarse", "dk_defl_setup_ms",
     "dk_gmres", "dk_gmres_ex", "dk_last_basis_vector",
     "dk_levelset_labels_device", "dk_assemble_tpfa", "dk_defl_create_dense",
-    "dk_defl_create_ritz", "dk_defl_coarse_kind",
+    "dk_defl_create_ritz", "dk_defl_coarse_kind", "dk_dense_lu", "dk_lu_solve",
 )
 
 
@@ -102,6 +102,8 @@ def _declare(lib):
         "dk_last_basis_vector": (C.c_int, [_P, C.c_int32, _P]),
         "dk_levelset_labels_device": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _P, C.c_int32,
                                                 C.c_int32, C.c_int32, _P, _I64, _P]),
+        "dk_dense_lu": (C.c_int, [C.c_int64, _P, _P, _P, _D]),
+        "dk_lu_solve": (C.c_int, [C.c_int64, _P, _P, C.c_int64, _P, _P]),
         "dk_assemble_tpfa": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                        C.c_double, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_double,
                                        _P, _P]),

@@ -18,7 +18,7 @@ ROOT = PKG.parent
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libdk.so"
 
-SOURCES = ["dk_kernels.cu", "dk_coarse.cu", "dk_dense.cu", "dk_profile.cu", "dk_setup.cu", "dk_api.cu"]
+SOURCES = ["dk_device.cu", "dk_kernels.cu", "dk_coarse.cu", "dk_dense.cu", "dk_profile.cu", "dk_setup.cu", "dk_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

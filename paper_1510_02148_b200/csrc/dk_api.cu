@@ -734,7 +734,7 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   const long long nch = op->n_pad / kChunk;
   // reduction grid: up to 4 blocks per SM stream the chunks (fixed block -> chunk map, so the
   // per-block partial sums, and hence every reduction, are deterministic)
-  op->G = (int)std::min<long long>(nch, 148 * 4);
+  op->G = (int)std::min<long long>(nch, (long long)num_sms() * 4);
   // all diagonals, guarded, ascending offsets
   DK_TRY(cudaMallocAsync(&op->dia, (size_t)ndiag * op->vlen * sizeof(double), op->stream));
   DK_TRY(cudaMemsetAsync(op->dia, 0, (size_t)ndiag * op->vlen * sizeof(double), op->stream));
@@ -760,7 +760,7 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
       int one_h = 1;
       DK_TRY(cudaMallocAsync(&f, sizeof(int), op->stream));
       DK_TRY(cudaMemcpyAsync(f, &one_h, sizeof(int), cudaMemcpyHostToDevice, op->stream));
-      k_check_pair<<<148 * 4, 256, 0, op->stream>>>(op->dia + (size_t)k * op->vlen + op->guard,
+      k_check_pair<<<num_sms() * 4, 256, 0, op->stream>>>(op->dia + (size_t)k * op->vlen + op->guard,
                                                     op->dia + (size_t)partner * op->vlen +
                                                         op->guard,
                                                     o, n - o, f);
@@ -1291,6 +1291,79 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
 // Dense basis context (deflation.py:71-89 for a general n x d Z, d <= kDenseMaxD): rows Z_k
 // (written by `fill`), A_p Z_k by the stencil, E_ik = Z_i . A_p Z_k by multi-dots, pivoted
 // LU + E^-1 (the reference's singularity rule), x* = Z E^-1 Z^T b.
+int dk_dense_lu(int64_t n, const double* a, double* lu, int32_t* piv, double* min_pivot) {
+  if (n < 1 || n >= (1ll << 31)) return fail(DK_EINVAL, "matrix order must be in [1, 2^31)");
+  if (!a || !lu || !piv) return fail(DK_EINVAL, "null argument");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt < 1) {
+    cudaGetLastError();
+    return fail(DK_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  const int d = (int)n;
+  const size_t row = (size_t)d * sizeof(double);
+  cudaStream_t s;
+  DK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double* E = nullptr;
+  int* dpiv = nullptr;
+  double mp = 0.0;
+  cudaError_t e = cudaMallocAsync(&E, row * d, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dpiv, (size_t)d * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(E, a, row * d, cudaMemcpyDefault, s);
+  // the pivoted panel path always: pivots are LAPACK getrf's (first row of maximal |a|)
+  if (e == cudaSuccess) e = (cudaError_t)lu_factor(E, d, d, dpiv, false, &mp, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(lu, E, row * d, cudaMemcpyDefault, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(piv, dpiv, (size_t)d * sizeof(int), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(E, s);
+  cudaFreeAsync(dpiv, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return cuda_fail(e, "dk_dense_lu");
+  if (min_pivot) *min_pivot = mp;
+  if (!(mp >= 1e-300)) return fail(DK_ESINGULAR, "zero pivot in LU factorization");
+  return DK_OK;
+}
+
+int dk_lu_solve(int64_t n, const double* lu, const int32_t* piv, int64_t nrhs, const double* b,
+                double* x) {
+  if (n < 1 || n >= (1ll << 31)) return fail(DK_EINVAL, "matrix order must be in [1, 2^31)");
+  if (nrhs < 1 || nrhs >= (1ll << 31)) return fail(DK_EINVAL, "nrhs must be >= 1");
+  if (!lu || !piv || !b || !x) return fail(DK_EINVAL, "null argument");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt < 1) {
+    cudaGetLastError();
+    return fail(DK_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  const int d = (int)n, nc = (int)nrhs;
+  cudaStream_t s;
+  DK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  double *E = nullptr, *X = nullptr;
+  int* dpiv = nullptr;
+  cudaError_t e = cudaMallocAsync(&E, (size_t)d * d * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&X, (size_t)d * nc * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dpiv, (size_t)d * sizeof(int), s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(E, lu, (size_t)d * d * sizeof(double), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dpiv, piv, (size_t)d * sizeof(int), cudaMemcpyDefault, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(X, b, (size_t)d * nc * sizeof(double), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) {
+    lu_solve_rows(E, d, d, dpiv, X, nc, nc, false, s);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(x, X, (size_t)d * nc * sizeof(double), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(E, s);
+  cudaFreeAsync(X, s);
+  cudaFreeAsync(dpiv, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return cuda_fail(e, "dk_lu_solve");
+  return DK_OK;
+}
+
 }  // extern "C"
 template <class Fill>
 static int defl_create_dense(dk_defl** out, dk_op* op, int32_t d, int32_t ap_choice,
@@ -1745,7 +1818,7 @@ int dk_last_basis_vector(dk_op* op, int32_t i, double* out) {
     // the reference never fills V[j+1] when the cycle stopped at j (krylov.py:195-197)
     DK_TRY(cudaMemsetAsync(op->t, 0, (size_t)op->n * sizeof(double), op->stream));
   } else {
-    k_scale_copy<<<148 * 4, 256, 0, op->stream>>>(V + (long long)i * op->vstride, op->sc.sigma + i,
+    k_scale_copy<<<num_sms() * 4, 256, 0, op->stream>>>(V + (long long)i * op->vstride, op->sc.sigma + i,
                                                   op->t, op->n);
   }
   DK_TRY(cudaGetLastError());

@@ -91,15 +91,11 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(const double* __restrict_
 void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
                  cudaStream_t s) {
   const size_t smem = (size_t)ld * sizeof(double);
-  const int ctas_max = 148;
+  const int ctas_max = num_sms();
   int rows_per_cta = (d + ctas_max - 1) / ctas_max;
   const unsigned grid = (unsigned)((d + rows_per_cta - 1) / rows_per_cta);
   if (smem <= 200 * 1024) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set = true;
-    }
+    smem_optin((const void*)k_gemv<true>, 200 * 1024);
     launch_pdl(k_gemv<true>, dim3(grid), dim3(kGemvThreads), smem, s, M, d, ld, x, y,
                rows_per_cta, gate);
   } else {
@@ -308,7 +304,7 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_symv_reduce(const double* __
 void symv_segments(int d, std::vector<int>& ptr, std::vector<int>& slots) {
   const long long nb = (d + kST - 1) / kST;
   const long long ntiles = nb * (nb + 1) / 2;
-  const long long W = 148LL * kSymvWarps;
+  const long long W = (long long)num_sms() * kSymvWarps;
   std::vector<long long> starts;
   for (long long ww = 0; ww < W; ++ww) {
     const long long r0 = ww * ntiles / W, r1 = (ww + 1) * ntiles / W;
@@ -344,7 +340,7 @@ int coarse_is_symmetric(const double* E, int d, int ld, cudaStream_t s) {
   int* f = nullptr;
   cudaMallocAsync(&f, sizeof(int), s);
   cudaMemcpyAsync(f, &h, sizeof(int), cudaMemcpyHostToDevice, s);
-  k_check_sym<<<148 * 8, 256, 0, s>>>(E, d, ld, f);
+  k_check_sym<<<num_sms() * 8, 256, 0, s>>>(E, d, ld, f);
   cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
   cudaFreeAsync(f, s);
@@ -358,7 +354,7 @@ long long symv_tiles(int d) {
 
 void launch_symv_pack(const double* Einv, int d, int ld, double* P, cudaStream_t s) {
   const int nb = (d + kST - 1) / kST;
-  k_symv_pack<<<148 * 8, 256, 0, s>>>(Einv, d, ld, nb, P);
+  k_symv_pack<<<num_sms() * 8, 256, 0, s>>>(Einv, d, ld, nb, P);
 }
 
 void launch_symv(const double* P, int d, const double* x, double* rowpart, double* colpart,
@@ -366,12 +362,8 @@ void launch_symv(const double* P, int d, const double* x, double* rowpart, doubl
   const int nb = (d + kST - 1) / kST;
   const size_t smem =
       (size_t)kSymvWarps * kSymvStages * kTileBytes + (size_t)nb * kST * sizeof(double);
-  static size_t attr_set = 0;
-  if (smem > attr_set) {
-    cudaFuncSetAttribute(k_symv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = smem;
-  }
-  const unsigned grid = 148;
+  smem_optin((const void*)k_symv, smem);
+  const unsigned grid = (unsigned)num_sms();
   launch_pdl(k_symv, dim3(grid), dim3(kSymvWarps * 32), smem, s, P, d, nb, x, rowpart, colpart,
              gate);
 }
@@ -477,7 +469,7 @@ int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const R
   double *v_in = nullptr, *v_out = nullptr, *sdiag = nullptr;
   int total = 0, last_cnt = 0;
   size_t tmp_bytes = 0, need = 0;
-  const unsigned grid = 148 * 8;
+  const unsigned grid = (unsigned)num_sms() * 8;
   long long nk = 0;
 #define DKC(x)                       \
   do {                               \
@@ -843,14 +835,9 @@ __global__ void __launch_bounds__(256) k_trsm_rows(double* __restrict__ E, int d
   }
 }
 
-int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min_pivot,
-                   float* ms_lu, float* ms_inv, cudaStream_t s) {
-  cudaEvent_t e0, e1, e2;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventCreate(&e2);
-  cudaEventRecord(e0, s);
-  const unsigned cgrid = (unsigned)((d + 255) / 256);
+// Column test for the pivot-free path (see k_col_dominance); `strict` drops the rounding
+// allowance, so the pivots equal partial pivoting's exactly (the public dense_lu).
+static int column_dominant(const double* E, int d, int ld, cudaStream_t s) {
   int* dflag = nullptr;
   int dominant = 1;
   cudaMallocAsync(&dflag, sizeof(int), s);
@@ -859,9 +846,20 @@ int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min
   cudaMemcpyAsync(&dominant, dflag, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
   cudaFreeAsync(dflag, s);
-  // Two-level right-looking LU: outer panels of kNB2 columns are factorised by kNB-wide
-  // steps whose rank-kNB updates stay inside the panel; the trailing matrix then receives
-  // one rank-kNB2 GEMM update per outer panel (compute-bound instead of C-traffic-bound).
+  return dominant;
+}
+
+// P E = L U in place (row-major; unit L below the diagonal, U on and above it; piv[k] = the
+// row interchanged with row k, 0-based — LAPACK getrf's layout, sparse.py:109-137).
+// Two-level right-looking LU: outer panels of kNB2 columns are factorised by kNB-wide steps
+// whose rank-kNB updates stay inside the panel; the trailing matrix then receives one
+// rank-kNB2 GEMM update per outer panel (compute-bound instead of C-traffic-bound).
+// `dominant`: the columns are diagonally dominant, so partial pivoting never interchanges
+// and the pivot-free path (k_diag_lu + k_trsm_rows) is the same factorisation.
+// Writes min |U_kk| to *min_pivot (host).
+int lu_factor(double* E, int d, int ld, int* piv, bool dominant, double* min_pivot,
+              cudaStream_t s) {
+  const unsigned cgrid = (unsigned)((d + 255) / 256);
   auto at = [&](int r, int c) { return E + (long long)r * ld + c; };
   for (int K0 = 0; K0 < d; K0 += kNB2) {
     const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
@@ -901,46 +899,71 @@ int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min
   cudaMallocAsync(&dmin, sizeof(double), s);
   k_min_pivot<<<1, 1024, 0, s>>>(E, d, ld, dmin);
   cudaMemcpyAsync(min_pivot, dmin, sizeof(double), cudaMemcpyDeviceToHost, s);
-  cudaEventRecord(e1, s);
   cudaStreamSynchronize(s);
   cudaFreeAsync(dmin, s);
-  if (!(*min_pivot >= 1e-300)) {  // singular (or NaN): no inverse
+  return (int)cudaGetLastError();
+}
+
+// X <- U^-1 L^-1 P X for the d x ncols block X (row-major, ldx): the row interchanges, then
+// the unit-lower and the upper triangular solves, each two-level (kNB-wide substitution
+// blocks, rank-kNB2 GEMM updates) — LAPACK getrs (sparse.py:140-145).  `lower_fill`: X = P
+// with no interchanges, so L^-1 X stays lower triangular and the forward sweep of row block
+// [K0, Kend) only touches columns [0, Kend).
+void lu_solve_rows(const double* E, int d, int ld, const int* piv, double* X, int ldx,
+                   int ncols, bool lower_fill, cudaStream_t s) {
+  const unsigned xgrid = (unsigned)((ncols + 255) / 256);
+  auto at = [&](int r, int c) { return E + (long long)r * ld + c; };
+  auto xt = [&](int r, int c) { return X + (long long)r * ldx + c; };
+  k_laswp<<<xgrid, 256, 0, s>>>(X, ncols, ldx, piv, 0, d, 0, 0);
+  for (int K0 = 0; K0 < d; K0 += kNB2) {  // L Y = P X
+    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
+    const int nc = lower_fill && Kend < ncols ? Kend : ncols;
+    for (int k = K0; k < Kend; k += kNB) {
+      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
+      k_trsm_block<false><<<(nc + 255) / 256, 256, 0, s>>>(E, ld, k, nb, X, ldx, 0, nc);
+      if (k + nb < Kend)
+        dgemm_sub(at(k + nb, k), ld, xt(k, 0), ldx, xt(k + nb, 0), ldx, Kend - k - nb, nc, nb,
+                  s);
+    }
+    if (Kend < d)
+      dgemm_sub(at(Kend, K0), ld, xt(K0, 0), ldx, xt(Kend, 0), ldx, d - Kend, nc, Kend - K0, s);
+  }
+  const int lastK0 = ((d - 1) / kNB2) * kNB2;
+  for (int K0 = lastK0; K0 >= 0; K0 -= kNB2) {  // U X = Y, from the bottom
+    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
+    const int lastk = K0 + ((Kend - K0 - 1) / kNB) * kNB;
+    for (int k = lastk; k >= K0; k -= kNB) {
+      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
+      k_trsm_block<true><<<xgrid, 256, 0, s>>>(E, ld, k, nb, X, ldx, 0, ncols);
+      if (k > K0) dgemm_sub(at(K0, k), ld, xt(k, 0), ldx, xt(K0, 0), ldx, k - K0, ncols, nb, s);
+    }
+    if (K0 > 0)
+      dgemm_sub(at(0, K0), ld, xt(K0, 0), ldx, xt(0, 0), ldx, K0, ncols, Kend - K0, s);
+  }
+}
+
+int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min_pivot,
+                   float* ms_lu, float* ms_inv, cudaStream_t s) {
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventRecord(e0, s);
+  const bool dominant = column_dominant(E, d, ld, s) != 0;
+  int err = lu_factor(E, d, ld, piv, dominant, min_pivot, s);
+  cudaEventRecord(e1, s);
+  if (err || !(*min_pivot >= 1e-300)) {  // singular (or NaN): no inverse
+    cudaStreamSynchronize(s);
     cudaEventElapsedTime(ms_lu, e0, e1);
     *ms_inv = 0.f;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
-    return (int)cudaGetLastError();
+    return err ? err : (int)cudaGetLastError();
   }
   // Einv = U^-1 L^-1 P I
-  k_identity<<<148 * 8, 256, 0, s>>>(Einv, d, ld);
-  k_laswp<<<cgrid, 256, 0, s>>>(Einv, d, ld, piv, 0, d, 0, 0);
-  auto xt = [&](int r, int c) { return Einv + (long long)r * ld + c; };
-  for (int K0 = 0; K0 < d; K0 += kNB2) {  // L Y = P, two-level
-    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
-    // without row interchanges Y = L^-1 is lower triangular: rows < Kend have nonzeros only
-    // in columns [0, Kend)
-    const int ncol = dominant ? Kend : d;
-    for (int k = K0; k < Kend; k += kNB) {
-      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
-      k_trsm_block<false><<<(ncol + 255) / 256, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, ncol);
-      if (k + nb < Kend)
-        dgemm_sub(at(k + nb, k), ld, xt(k, 0), ld, xt(k + nb, 0), ld, Kend - k - nb, ncol, nb, s);
-    }
-    if (Kend < d)
-      dgemm_sub(at(Kend, K0), ld, xt(K0, 0), ld, xt(Kend, 0), ld, d - Kend, ncol, Kend - K0, s);
-  }
-  const int lastK0 = ((d - 1) / kNB2) * kNB2;
-  for (int K0 = lastK0; K0 >= 0; K0 -= kNB2) {  // U X = Y, two-level from the bottom
-    const int Kend = (d - K0 < kNB2) ? d : K0 + kNB2;
-    const int lastk = K0 + ((Kend - K0 - 1) / kNB) * kNB;
-    for (int k = lastk; k >= K0; k -= kNB) {
-      const int nb = (Kend - k < kNB) ? Kend - k : kNB;
-      k_trsm_block<true><<<cgrid, 256, 0, s>>>(E, ld, k, nb, Einv, ld, 0, d);
-      if (k > K0) dgemm_sub(at(K0, k), ld, xt(k, 0), ld, xt(K0, 0), ld, k - K0, d, nb, s);
-    }
-    if (K0 > 0) dgemm_sub(at(0, K0), ld, xt(K0, 0), ld, xt(0, 0), ld, K0, d, Kend - K0, s);
-  }
+  k_identity<<<num_sms() * 8, 256, 0, s>>>(Einv, d, ld);
+  lu_solve_rows(E, d, ld, piv, Einv, ld, d, dominant, s);
   cudaEventRecord(e2, s);
   cudaStreamSynchronize(s);
   cudaEventElapsedTime(ms_lu, e0, e1);

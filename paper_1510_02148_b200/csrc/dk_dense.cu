@@ -250,12 +250,7 @@ template <bool TA, bool TB, int NT, bool A8>
 void launch_mma_a(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
                   int N, int K, double alpha, double beta, int tri, int kshift, int kstop,
                   cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dgemm_mma<TA, TB, NT, A8>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem<NT>());
-    attr = true;
-  }
+  smem_optin((const void*)k_dgemm_mma<TA, TB, NT, A8>, gemm_smem<NT>());
   dim3 grid((N + 32 * NT - 1) / (32 * NT), (M + GM - 1) / GM);
   k_dgemm_mma<TA, TB, NT, A8><<<grid, 256, gemm_smem<NT>(), s>>>(A, lda, B, ldb, C, ldc, M, N,
                                                                 K, alpha, beta, tri, kshift,
@@ -493,7 +488,7 @@ __global__ void __launch_bounds__(256) k_mirror_upper(double* __restrict__ X, in
 }  // namespace
 
 void launch_row_first_nz(const double* X, int d, int ld, int* f, cudaStream_t s) {
-  k_row_first_nz<<<148 * 4, 256, 0, s>>>(X, d, ld, f);
+  k_row_first_nz<<<num_sms() * 4, 256, 0, s>>>(X, d, ld, f);
 }
 
 // X = W^T W (full) for lower-triangular W
@@ -537,11 +532,7 @@ static cudaStream_t side_stream() {
 
 int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float* ms_fac,
                 float* ms_inv, cudaStream_t s, bool form_inverse, bool clear_w) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
-    attr = true;
-  }
+  smem_optin((const void*)k_chol_diag, kDiagSmem);
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -559,7 +550,7 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
     int* df = nullptr;
     std::vector<int> f(d);
     cudaMallocAsync(&df, (size_t)d * sizeof(int), s);
-    k_row_first_nz<<<148 * 4, 256, 0, s>>>(L, d, ld, df);
+    k_row_first_nz<<<num_sms() * 4, 256, 0, s>>>(L, d, ld, df);
     cudaMemcpyAsync(f.data(), df, (size_t)d * sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(df, s);
     cudaStreamSynchronize(s);
@@ -692,11 +683,7 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
 // on the separator diagonal blocks; W must be zero on entry.
 int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tree, double* W,
                     double* min_diag_sq, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
-    attr = true;
-  }
+  smem_optin((const void*)k_chol_diag, kDiagSmem);
   auto at = [&](double* X, int r, int c) { return X + (long long)r * ld + c; };
   // leaves: batched diagonal factorisation + inversion
   std::vector<int2> jobs;

@@ -456,12 +456,8 @@ static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, co
                        const unsigned* wait, const double* gsig, int ng) {
   const unsigned grid = (unsigned)(n_pad / kTile);
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
-  static size_t attr = 0;
-  if (smem > attr) {  // static + dynamic above 48 KB needs the opt-in (wide grids: nx = 512)
-    cudaFuncSetAttribute(k_stencil_sym7<PRE, R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = smem;
-  }
+  // static + dynamic above 48 KB needs the opt-in (wide grids: nx = 512)
+  smem_optin((const void*)k_stencil_sym7<PRE, R, W>, smem);
   launch_pdl(k_stencil_sym7<PRE, R, W>, dim3(grid), dim3(kThreads), smem, s, A, v, scale, out,
              rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
              rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H, wait, gsig, ng);
@@ -794,10 +790,10 @@ void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad
                           int2* flab, double2* fco, unsigned char* mask,
                           unsigned long long* nmasked, cudaStream_t s) {
   if (am)
-    k_prolong_setup<true><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, flab, fco, mask,
+    k_prolong_setup<true><<<num_sms() * 8, kThreads, 0, s>>>(A, lab, n_pad, own, flab, fco, mask,
                                                          nmasked);
   else
-    k_prolong_setup<false><<<148 * 8, kThreads, 0, s>>>(A, lab, n_pad, own, flab, fco, mask,
+    k_prolong_setup<false><<<num_sms() * 8, kThreads, 0, s>>>(A, lab, n_pad, own, flab, fco, mask,
                                                           nmasked);
 }
 
@@ -1066,12 +1062,8 @@ static void project_t(const Dia& A, const Prolong& lab, const double* yc, const 
   if (MODE == PJ_ITER && tail > slots) slots = tail;
   if (nq + 260 > slots) slots = nq + 260;  // reduce_grouped scratch
   const size_t smem = (size_t)slots * sizeof(double);
-  static bool attr = false;  // one per instantiation: dynamic + 32 KB static > 48 KB default
-  if (!attr) {
-    cudaFuncSetAttribute(k_project<MODE, DEFL, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         160 * 1024);
-    attr = true;
-  }
+  // one per instantiation and device: dynamic + 32 KB static > 48 KB default
+  smem_optin((const void*)k_project<MODE, DEFL, AM>, 160 * 1024);
   launch_pdl(k_project<MODE, DEFL, AM>, dim3(G), dim3(kThreads), smem, s, A, lab, yc, w_in,
              w_out, V, vstride, nvec, n_pad, part, G, sc, j, gate);
 }
@@ -1201,7 +1193,7 @@ __global__ void k_dense_recon(const double* __restrict__ Z, long long zs, int nz
 void launch_dense_recon(const double* Z, long long zs, int nz, const double* y, const double* xs,
                         const double* xh, double* out, long long n_pad, int mode,
                         cudaStream_t s) {
-  k_dense_recon<<<148 * 8, kThreads, 0, s>>>(Z, zs, nz, y, xs, xh, out, n_pad, mode);
+  k_dense_recon<<<num_sms() * 8, kThreads, 0, s>>>(Z, zs, nz, y, xs, xh, out, n_pad, mode);
 }
 
 // out_j = sum_i Y[i + j nrows] sigma_i R_i, eight outputs per sweep over the rows
@@ -1234,7 +1226,7 @@ __global__ void __launch_bounds__(kThreads) k_combine_rows(const double* __restr
 void launch_combine_rows(const double* R, long long rs, const double* sigma, int nrows,
                          const double* Y, int nout, double* out, long long os, long long n_pad,
                          cudaStream_t s) {
-  k_combine_rows<<<148 * 8, kThreads, 0, s>>>(R, rs, sigma, nrows, Y, nout, out, os, n_pad);
+  k_combine_rows<<<num_sms() * 8, kThreads, 0, s>>>(R, rs, sigma, nrows, Y, nout, out, os, n_pad);
 }
 
 // ======================================================================================
@@ -1555,11 +1547,7 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
 void launch_cycle_end(const Scal& sc, cudaStream_t s) {
   const size_t m = (size_t)sc.m;
   const size_t smem = (m + 1 + (sc.m <= kStageGram ? m * m : 0)) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_cycle_end, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)k_cycle_end, 160 * 1024);
   launch_pdl(k_cycle_end, dim3(1), dim3(32), smem, s, sc);
 }
 // x += M^-1 (sum_{i<cols} y_i V_i)   (krylov.py:206)
@@ -1598,7 +1586,7 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(Dia A, double* __restrict_
 void launch_xupdate(const Dia& A, double* x, const double* V, long long vstride, long long n_pad,
                     const Scal& sc, cudaStream_t s) {
   const size_t smem = (size_t)(sc.m + 1) * sizeof(double);
-  launch_pdl(k_xupdate, dim3(148 * 8), dim3(kThreads), smem, s, A, x, V, vstride, n_pad, sc);
+  launch_pdl(k_xupdate, dim3(num_sms() * 8), dim3(kThreads), smem, s, A, x, V, vstride, n_pad, sc);
 }
 
 // ======================================================================================
@@ -1619,14 +1607,14 @@ __global__ void k_recon(const int* __restrict__ lab, const double* __restrict__ 
 
 void launch_recon(const int* lab, const double* y, const double* xs, const double* xh, double* out,
                   long long n_pad, cudaStream_t s) {
-  k_recon<<<148 * 8, kThreads, 0, s>>>(lab, y, xs, xh, out, n_pad, 0);
+  k_recon<<<num_sms() * 8, kThreads, 0, s>>>(lab, y, xs, xh, out, n_pad, 0);
 }
 void launch_bcast(const int* lab, const double* y, double* out, long long n_pad, cudaStream_t s) {
-  k_recon<<<148 * 8, kThreads, 0, s>>>(lab, y, nullptr, nullptr, out, n_pad, 1);
+  k_recon<<<num_sms() * 8, kThreads, 0, s>>>(lab, y, nullptr, nullptr, out, n_pad, 1);
 }
 void launch_sub_bcast(const int* lab, const double* y, const double* v, double* out,
                       long long n_pad, cudaStream_t s) {
-  k_recon<<<148 * 8, kThreads, 0, s>>>(lab, y, nullptr, v, out, n_pad, 2);
+  k_recon<<<num_sms() * 8, kThreads, 0, s>>>(lab, y, nullptr, v, out, n_pad, 2);
 }
 
 __global__ void __launch_bounds__(kThreads) k_norm(const double* __restrict__ v, long long n_pad,

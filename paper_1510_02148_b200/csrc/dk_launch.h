@@ -10,6 +10,15 @@
 
 namespace dk {
 
+// ---- per-device properties (dk_device.cu) ----
+constexpr int kMaxDevices = 64;
+int current_device();
+// SM count of the current device (cached per ordinal; grids are sized from it)
+int num_sms();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) for `fn` on the current device,
+// once per (kernel, device); no-op at or below the 48 KB default.  0 or a cuda error code.
+int smem_optin(const void* fn, size_t bytes);
+
 // Stencil modes of launch_stencil.
 enum StencilMode {
   ST_APPLY = 0,  // out = A (M^-1 (scale * v))          (krylov.py:159 / deflation.py:50-51)
@@ -131,6 +140,14 @@ int coarse_is_symmetric(const double* E, int d, int ld, cudaStream_t s);
 // E (d x d, ld) = Z^T A_p Z, deterministic.  Returns 0 or a cuda error code.
 int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const RunMap& rm,
                  double* E, int ld, double* scratch_q, cudaStream_t s);
+// In-place P E = L U with partial pivoting (LAPACK getrf layout, row-major; piv[k] = row
+// interchanged with row k).  dominant: the pivot-free path (columns diagonally dominant).
+// *min_pivot receives min |U_kk| (host).  Returns 0 or a cuda error code.
+int lu_factor(double* E, int d, int ld, int* piv, bool dominant, double* min_pivot,
+              cudaStream_t s);
+// X <- U^-1 L^-1 P X for a d x ncols row-major block (getrs).
+void lu_solve_rows(const double* E, int d, int ld, const int* piv, double* X, int ldx,
+                   int ncols, bool lower_fill, cudaStream_t s);
 // In-place LU with partial pivoting of E, then Einv = U^-1 L^-1 P.  *min_pivot receives
 // min |U_kk| (host).  Returns 0 or a cuda error code.
 int lu_and_inverse(double* E, int d, int ld, double* Einv, int* piv, double* min_pivot,

@@ -491,7 +491,7 @@ int coarse_pattern(const double* E, int d, int ld, std::vector<int>& ptr, std::v
   int* dptr = nullptr;
   int* dcol = nullptr;
   cudaMallocAsync(&dcnt, (size_t)d * sizeof(int), s);
-  k_row_nnz<<<148 * 4, 256, 0, s>>>(E, d, ld, dcnt);
+  k_row_nnz<<<num_sms() * 4, 256, 0, s>>>(E, d, ld, dcnt);
   std::vector<int> cnt(d);
   cudaMemcpyAsync(cnt.data(), dcnt, (size_t)d * sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaError_t e = cudaStreamSynchronize(s);
@@ -502,7 +502,7 @@ int coarse_pattern(const double* E, int d, int ld, std::vector<int>& ptr, std::v
   cudaMallocAsync(&dptr, (size_t)(d + 1) * sizeof(int), s);
   cudaMallocAsync(&dcol, (size_t)std::max(ptr[d], 1) * sizeof(int), s);
   cudaMemcpyAsync(dptr, ptr.data(), (size_t)(d + 1) * sizeof(int), cudaMemcpyHostToDevice, s);
-  k_row_cols<<<148 * 4, 256, 0, s>>>(E, d, ld, dptr, dcol);
+  k_row_cols<<<num_sms() * 4, 256, 0, s>>>(E, d, ld, dptr, dcol);
   if (ptr[d] > 0)
     cudaMemcpyAsync(col.data(), dcol, (size_t)ptr[d] * sizeof(int), cudaMemcpyDeviceToHost, s);
   e = cudaStreamSynchronize(s);
@@ -514,12 +514,12 @@ int coarse_pattern(const double* E, int d, int ld, std::vector<int>& ptr, std::v
 
 void launch_permute_sym(const double* E, int d, int ld, const int* perm, double* out,
                         cudaStream_t s) {
-  k_permute_sym<<<148 * 8, 256, 0, s>>>(E, d, ld, perm, out);
+  k_permute_sym<<<num_sms() * 8, 256, 0, s>>>(E, d, ld, perm, out);
 }
 
 void launch_unpermute_sym(const double* X, int d, int ld, const int* perm, double* out, int ldo,
                           cudaStream_t s) {
-  k_unpermute_sym<<<148 * 8, 256, 0, s>>>(X, d, ld, perm, out, ldo);
+  k_unpermute_sym<<<num_sms() * 8, 256, 0, s>>>(X, d, ld, perm, out, ldo);
 }
 
 int tgemv_warps_per_cta();
@@ -579,7 +579,7 @@ int profile_streams(const double* W, int d, int ld, const std::vector<int>& fW,
   cudaMallocAsync(&dfl, nc * sizeof(int), s);
   cudaMemcpyAsync(dti, ci.data(), nc * sizeof(int), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dtj, cj.data(), nc * sizeof(int), cudaMemcpyHostToDevice, s);
-  k_tile_nz<<<148 * 8, 256, 0, s>>>(W, d, ld, dti, dtj, nc, dfl);
+  k_tile_nz<<<num_sms() * 8, 256, 0, s>>>(W, d, ld, dti, dtj, nc, dfl);
   std::vector<int> fl(nc);
   cudaMemcpyAsync(fl.data(), dfl, nc * sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaError_t e = cudaStreamSynchronize(s);
@@ -635,7 +635,7 @@ int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost
     e = cudaMemsetAsync(g.part, 0xff, (size_t)h.nslots * kPT * sizeof(double), s);
   if (e != cudaSuccess) return (int)e;
   // the tile stream itself (big_alloc'd by the caller into g.T)
-  k_tile_pack<<<148 * 8, 256, 0, s>>>(W, d, ld, trow, tcol, h.nt, trans ? 1 : 0,
+  k_tile_pack<<<num_sms() * 8, 256, 0, s>>>(W, d, ld, trow, tcol, h.nt, trans ? 1 : 0,
                                       const_cast<double*>(g.T));
   return (int)cudaGetLastError();
 }
@@ -663,23 +663,13 @@ int tgemv_cfg() {
 int tgemv_warps_per_cta() { return kTgCfg[tgemv_cfg()][0]; }
 
 // SMs of the current device (the tile streams are split over tg_grid() CTAs)
-int tg_grid() {
-  static int n[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!n[dev & 63]) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  return n[dev & 63];
-}
+int tg_grid() { return num_sms(); }
 
 template <int KW, int KS>
 static void launch_tg(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
                       const int* gate, cudaStream_t s) {
   const size_t smem = (size_t)KW * KS * kPTileBytes;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tgemv<KW, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)k_tgemv<KW, KS>, smem);
   const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
   launch_pdl(k_tgemv<KW, KS>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d, gate);
 }

@@ -114,7 +114,7 @@ int device_levelset_labels(long long nx, long long ny, long long nz, const long 
   size_t tmp_bytes = 0;
   int last_rank = 0, last_flag = 0;
   cudaError_t e = cudaSuccess;
-  const unsigned grid = 148 * 8;
+  const unsigned grid = (unsigned)num_sms() * 8;
 #define DKS(x)                     \
   do {                             \
     e = (x);                       \
@@ -267,7 +267,7 @@ int device_assemble_tpfa(int nx, int ny, int nz, double dx, double dy, double dz
     DKS(cudaMallocAsync(&qq, n * sizeof(double), s));
     DKS(cudaMemcpyAsync(qq, q, n * sizeof(double), cudaMemcpyDefault, s));
   }
-  k_tpfa<<<148 * 8, 256, 0, s>>>(nx, ny, nz, dx, dy, dz, k, k + n, k + 2 * n, qq, F, bperm, dia,
+  k_tpfa<<<num_sms() * 8, 256, 0, s>>>(nx, ny, nz, dx, dy, dz, k, k + n, k + 2 * n, qq, F, bperm, dia,
                                  bb);
   DKS(cudaGetLastError());
   DKS(cudaMemcpyAsync(diags_out, dia, 7 * n * sizeof(double), cudaMemcpyDefault, s));

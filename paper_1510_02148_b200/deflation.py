@@ -88,6 +88,7 @@ class DeflationContext:
     def __init__(self, basis: DeflationBasis, A: SparseMatrix, M, A_p_choice: str, h, lib):
         self.basis, self.A, self.M, self.A_p_choice = basis, A, M, A_p_choice
         self.h, self._lib = h, lib
+        self._E_lu = None
         self._fin = weakref.finalize(self, lib.dk_defl_destroy, h)
 
     def close(self) -> None:
@@ -132,11 +133,23 @@ class DeflationContext:
     def d(self) -> int:
         return self.basis.d
 
-    def coarse_matrix(self):
-        """(E, E^-1) copied from the device (d x d)."""
+    @property
+    def E_lu(self):
+        """LUFactors of E (deflation.py:46), factorised on the device on first access.
+
+        The solver itself applies E^-1 through its own factor (Cholesky in nested-dissection
+        order for a symmetric E, pivoted LU otherwise — dk_defl_coarse_kind); this is the
+        reference's getrf-layout view for callers of lu_solve(ctx.E_lu, ...)."""
+        if self._E_lu is None:
+            from .sparse import dense_lu
+            self._E_lu = dense_lu(self.coarse_matrix(inverse=False)[0])
+        return self._E_lu
+
+    def coarse_matrix(self, inverse: bool = True):
+        """(E, E^-1) copied from the device (d x d); E^-1 is None when inverse=False."""
         d = self.basis.d
         E = np.empty((d, d))
-        Einv = np.empty((d, d))
+        Einv = np.empty((d, d)) if inverse else None
         _lib.check(self._lib.dk_defl_coarse(self.h, _lib.ptr(E), _lib.ptr(Einv)))
         return E, Einv
 

@@ -242,3 +242,64 @@ def spmv(A: SparseMatrix, x) -> np.ndarray:
     if x.shape != (A.n,):
         raise ValueError(f"dimension mismatch: matrix is {A.n}, vector is {x.shape}")
     return A.device().spmv(x)
+
+
+# ---- dense LU helpers (sparse.py:109-145) --------------------------------------------------
+class LUFactors:
+    """Combined LU storage with pivot permutation, LAPACK getrf layout (sparse.py:109-118):
+    `lu` holds unit L strictly below the diagonal and U on and above it, `piv[k]` the 0-based
+    row interchanged with row k; `n` the order."""
+
+    __slots__ = ("lu", "piv", "n")
+
+    def __init__(self, lu, piv):
+        self.lu = lu
+        self.piv = piv
+        self.n = lu.shape[0]
+
+    def __repr__(self) -> str:
+        return f"LUFactors(n={self.n})"
+
+
+def dense_lu(M) -> LUFactors:
+    """P M = L U with partial pivoting on the device (sparse.py:121-137, dk_dense_lu).
+
+    Raises SingularCoarseMatrix on a pivot below 1e-300, ValueError for a non-square or
+    non-finite matrix.
+    """
+    M = np.asarray(M, dtype=np.float64)
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise ValueError("matrix must be square")
+    if M.size == 0:
+        return LUFactors(M.reshape(0, 0), np.zeros(0, dtype=np.int32))
+    if not np.isfinite(M).all():  # scipy.linalg.lu_factor(check_finite=True)
+        raise ValueError("array must not contain infs or NaNs")
+    lib = _lib.load()
+    _lib.require_device()
+    a = np.ascontiguousarray(M)
+    n = a.shape[0]
+    lu = np.empty((n, n))
+    piv = np.empty(n, dtype=np.int32)
+    mp = C.c_double(0.0)
+    rc = lib.dk_dense_lu(n, _lib.ptr(a), _lib.ptr(lu), _lib.ptr(piv), C.byref(mp))
+    _lib.check(rc, "dk_dense_lu")  # DK_ESINGULAR -> SingularCoarseMatrix
+    return LUFactors(lu, piv)
+
+
+def lu_solve(f: LUFactors, b) -> np.ndarray:
+    """Solve M x = b from dense_lu's factors (sparse.py:140-145); b is a vector or stacked
+    right-hand sides (n x k).  Triangular solves on the device (dk_lu_solve)."""
+    b = np.asarray(b, dtype=np.float64)
+    if f.n == 0:
+        return np.zeros_like(b)
+    if b.shape[0] != f.n or b.ndim not in (1, 2):
+        raise ValueError("right-hand side has wrong shape")
+    lib = _lib.load()
+    _lib.require_device()
+    rhs = np.ascontiguousarray(b.reshape(f.n, -1))
+    x = np.empty_like(rhs)
+    lu = np.ascontiguousarray(f.lu, dtype=np.float64)
+    piv = np.ascontiguousarray(f.piv, dtype=np.int32)
+    _lib.check(lib.dk_lu_solve(f.n, _lib.ptr(lu), _lib.ptr(piv), rhs.shape[1], _lib.ptr(rhs),
+                               _lib.ptr(x)), "dk_lu_solve")
+    return x.reshape(b.shape)
