@@ -289,12 +289,13 @@ def run_cycles(A, b, x0=None, inv_diag=None, m=30, tol=1e-6, max_iters=300, min_
         y = scipy.linalg.solve_triangular(R[:cols, :cols], g[:cols], check_finite=False)
         x = x + pre(V[:cols].T @ y)
         cycle += 1
+    x_hat = x
     if defl is not None:
         x = defl.reconstruct(x)
     nr = float(np.linalg.norm(b - A @ x))
     n0 = float(np.linalg.norm(b - A @ x0))
     return {
-        "x": x, "converged": converged, "iterations": its, "restarts": max(cycle - 1, 0),
+        "x": x, "x_hat": x_hat, "converged": converged, "iterations": its, "restarts": max(cycle - 1, 0),
         "cycles": cycle, "history": np.array(hist), "restart_of": np.array(rof),
         "final_relres": nr / (n0 if n0 > 0 else 1.0), "warning": warning, "reorths": reorths,
     }

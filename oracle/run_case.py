@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--max-cycles", type=int, default=None)
     ap.add_argument("--full-x", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--save-xhat", default=None, help="x before reconstruct (.npy, not committed)")
     a = ap.parse_args()
     t0 = time.time()
     case, Ac, b, inv, col, dcol = oracle_inputs(a.config)
@@ -69,6 +70,8 @@ def main():
           f"relres={r['final_relres']:.3e} reorths={r['reorths']} setup={t1 - t0:.1f}s "
           f"solve={t2 - t1:.1f}s threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
           flush=True)
+    if a.save_xhat:
+        np.save(a.save_xhat, r["x_hat"])
     if a.out:
         extra = {"x": r["x"]} if a.full_x else {}
         np.savez_compressed(a.out, iters=r["iterations"], history=r["history"],

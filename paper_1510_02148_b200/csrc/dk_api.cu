@@ -396,13 +396,20 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   sc.gcol = p; p += m + 1;
   sc.gticket = op->gticket;
   sc.gpart = op->gpart;
-  op->gs_fuse = gs_can_fuse(op->G, sc) && getenv("DK_NO_GS_FUSE") == nullptr;
-  // early start of each iteration's stencil on k_gs's published sigma (needs the fused second
-  // Gram-Schmidt pass: k_gs then always finishes the iteration itself)
-  sc.post = (op->gs_fuse && getenv("DK_NO_EARLY") == nullptr) ? reinterpret_cast<unsigned*>(p)
-                                                               : nullptr;
-  p += m + 1;
   sc.ng = (op->G + kGroup - 1) / kGroup;
+  // early start of each iteration's stencil on k_gs's published sigma (needs the fused second
+  // Gram-Schmidt pass: k_gs then always finishes the iteration itself).  The fused pass needs
+  // the whole k_gs grid co-resident at the shared-memory size it launches with, which early
+  // start enlarges (group partials): check with early start, then without it.
+  const bool no_fuse = getenv("DK_NO_GS_FUSE") != nullptr;
+  sc.post = getenv("DK_NO_EARLY") == nullptr ? reinterpret_cast<unsigned*>(p) : nullptr;
+  op->gs_fuse = !no_fuse && gs_can_fuse(op->G, sc);
+  if (!op->gs_fuse && sc.post != nullptr) {
+    sc.post = nullptr;
+    op->gs_fuse = !no_fuse && gs_can_fuse(op->G, sc);
+  }
+  if (!op->gs_fuse) sc.post = nullptr;
+  p += m + 1;
   sc.gpart_gs = op->gpart + (size_t)(op->part_q - 1) * kGroupTickets;  // past the dots' rows
   sc.hist = op->hist;
   sc.restart_of = op->rof;
@@ -735,6 +742,9 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   // reduction grid: up to 4 blocks per SM stream the chunks (fixed block -> chunk map, so the
   // per-block partial sums, and hence every reduction, are deterministic)
   op->G = (int)std::min<long long>(nch, (long long)num_sms() * 4);
+  // reduce_grouped's group counters share gticket with the fused pass's barrier (the last
+  // three slots): at most kGroupTickets - 3 groups
+  op->G = std::min(op->G, (kGroupTickets - 3) * kGroup);
   // all diagonals, guarded, ascending offsets
   DK_TRY(cudaMallocAsync(&op->dia, (size_t)ndiag * op->vlen * sizeof(double), op->stream));
   DK_TRY(cudaMemsetAsync(op->dia, 0, (size_t)ndiag * op->vlen * sizeof(double), op->stream));

@@ -39,7 +39,7 @@ int num_sms() {
 }
 
 int smem_optin(const void* fn, size_t bytes) {
-  if (bytes <= 48 * 1024) return 0;
+  // no shortcut below 48 KB: the limit applies to static + dynamic shared memory
   const int dev = current_device();
   std::lock_guard<std::mutex> lk(g_mu);
   int& have = g_smem[{fn, dev}];

@@ -1451,23 +1451,31 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
 static size_t gs_smem(const Scal& sc, int nvec) {
   int slots = (kWarps > 3 * (sc.m + 1) ? kWarps : 3 * (sc.m + 1));
   if (slots < 261) slots = 261;  // reduce_grouped scratch
-  if (slots < (sc.m + 1) * sc.ng) slots = (sc.m + 1) * sc.ng;  // early start: group partials
+  // early start: the projection's group partials, staged (only when early start is on)
+  if (sc.post != nullptr && slots < (sc.m + 1) * sc.ng) slots = (sc.m + 1) * sc.ng;
   return ((size_t)nvec + (size_t)slots) * sizeof(double);
 }
 
 bool gs_can_fuse(int G, const Scal& sc) {
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs<false>, kThreads,
-                                                gs_smem(sc, sc.m + 1));
-  return (long long)per_sm * nsm >= G;
+  int per_sm = 0;
+  const size_t smem = gs_smem(sc, sc.m + 1);
+  if (smem_optin((const void*)k_gs<false>, smem) != 0) {
+    cudaGetLastError();
+    return false;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs<false>, kThreads, smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (long long)per_sm * num_sms() >= G;
 }
 
 void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, long long vstride,
                int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
                const int* gate, bool fuse, cudaStream_t s) {
   const size_t smem = gs_smem(sc, nvec);
+  smem_optin(reorth ? (const void*)k_gs<true> : (const void*)k_gs<false>, smem);
   if (reorth)
     launch_pdl(k_gs<true>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
                n_pad, part, G, sc, j, gate, 0, (const unsigned*)nullptr);

@@ -16,7 +16,8 @@ int current_device();
 // SM count of the current device (cached per ordinal; grids are sized from it)
 int num_sms();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) for `fn` on the current device,
-// once per (kernel, device); no-op at or below the 48 KB default.  0 or a cuda error code.
+// once per (kernel, device) and size (static + dynamic above 48 KB needs it).  0 or a cuda
+// error code.
 int smem_optin(const void* fn, size_t bytes);
 
 // Stencil modes of launch_stencil.

@@ -18,6 +18,9 @@ pytestmark = pytest.mark.gpu
 
 X_TOL = 1e-8
 IT_TOL = 2
+# residual histories (absolute LS residual estimates, krylov.py:180-184) against the
+# reference / oracle run on the same inputs
+HIST_RTOL = 1e-6
 
 
 def test_sandwich_golden_history(gpu, golden):
@@ -102,28 +105,29 @@ def test_config1_plain_parity(gpu, golden):
 
 
 def test_config2_parity(gpu, golden):
-    """128x128x64, d = 112: against the reference's dense-Z pdgmres run."""
+    """128x128x64, d = 112: against the reference's dense-Z pdgmres run (full x, history)."""
     g = golden("config2")
     case, A, b, part, basis, rep = _case_solve(2)
     assert part.d == int(g["d"])
     assert rep.converged and abs(rep.iterations - int(g["pd_iters"])) <= IT_TOL
-    xs = rep.x[::97]
-    assert np.linalg.norm(xs - g["pd_x_sample"]) / np.linalg.norm(g["pd_x_sample"]) <= X_TOL
-    assert abs(np.linalg.norm(rep.x) - float(g["pd_x_norm"])) <= X_TOL * float(g["pd_x_norm"])
+    assert rel(rep.x, g["pd_x"]) <= X_TOL
+    k = min(len(rep.residual_history), len(g["pd_history"]))
+    np.testing.assert_allclose(rep.residual_history[:k], g["pd_history"][:k], rtol=HIST_RTOL)
 
 
 def test_config3_parity(gpu):
-    """60x220x85, d = 10,917: against the label-based oracle's full run (golden), plus
-    size-independent properties (true residual, coarse-space orthogonality of P1 r)."""
+    """60x220x85, d = 10,917: against the label-based oracle's full run (full x, history),
+    plus size-independent properties (true residual, coarse-space orthogonality of P1 r)."""
     path = GOLDEN / "config3_oracle.npz"
     if not path.exists():
-        pytest.fail("tests/golden/config3_oracle.npz missing (oracle/run_case.py 3)")
+        pytest.fail("tests/golden/config3_oracle.npz missing (oracle/run_case.py 3 --full-x)")
     g = np.load(path)
     case, A, b, part, basis, rep = _case_solve(3)
     assert basis.d == int(g["d"]) == 10917
     assert rep.converged and abs(rep.iterations - int(g["iters"])) <= IT_TOL
-    xs = rep.x[::97]
-    assert np.linalg.norm(xs - g["x_sample"]) / np.linalg.norm(g["x_sample"]) <= X_TOL
+    assert rel(rep.x, g["x"]) <= X_TOL
+    k = min(len(rep.residual_history), len(g["history"]))
+    np.testing.assert_allclose(rep.residual_history[:k], g["history"][:k], rtol=HIST_RTOL)
     assert rep.final_relres < 1e-6
     # the deflated residual is Z-orthogonal: Z^T (b - A x) ~ 0 (P1 annihilates range(Z^T))
     r = b - dk.spmv(A, rep.x)
