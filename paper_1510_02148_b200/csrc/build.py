@@ -46,6 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = OUT_DIR / "obj"
     tmp.mkdir(exist_ok=True)
     cc = nvcc()
+    cmds = []
     for src in SOURCES:
         obj = tmp / (Path(src).stem + ".o")
         cmd = [cc, "-c", str(CSRC / src), "-o", str(obj), "-O3", "-std=c++17",
@@ -55,11 +56,20 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         else:
             cmd = [shutil.which("g++") or "g++", "-c", str(CSRC / src), "-o", str(obj), "-O3",
                    "-std=c++17", "-fPIC", "-I", str(ROOT / "include")]
+        cmds.append(cmd)
+        objs.append(str(obj))
+
+    def compile_one(cmd):
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL,
-                       stderr=None if verbose else subprocess.STDOUT)
-        objs.append(str(obj))
+        r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+        if verbose or r.returncode:
+            print(r.stdout, flush=True)
+        r.check_returncode()
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(compile_one, cmds))
     tmp_lib = LIB.with_suffix(".so.tmp")
     cmd = [cc, "-shared", *ARCH, "-o", str(tmp_lib), *objs, "-cudart", "static"]
     if verbose:

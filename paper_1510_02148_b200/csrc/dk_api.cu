@@ -171,8 +171,7 @@ struct dk_defl {
   int* perm = nullptr;   // perm[i] = label at position i
   int* iperm = nullptr;  // position of label L
   double* tv = nullptr;  // t = W s~
-  double* T1 = nullptr;  // stream of W's tiles by block row
-  double* T2 = nullptr;  // stream of W^T's tiles
+  double* T1 = nullptr;  // W's nonzero tiles by block row (both passes read them)
   TileGemv tg1{}, tg2{};
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
@@ -1201,11 +1200,10 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
           return cleanup_fail(err > 0 ? (cudaError_t)err : cudaErrorUnknown, "profile_streams");
         }
         DKD(big_alloc((void**)&c->T1, (size_t)h1.nt * 1024 * sizeof(double), s));
-        DKD(big_alloc((void**)&c->T2, (size_t)h2.nt * 1024 * sizeof(double), s));
         c->tg1.T = c->T1;
-        c->tg2.T = c->T2;
-        err = upload_stream(c->Einv, d, c->ld, false, h1, c->tg1, s);
-        if (!err) err = upload_stream(c->Einv, d, c->ld, true, h2, c->tg2, s);
+        c->tg2.T = c->T1;  // pass 2 applies pass 1's tiles transposed
+        err = upload_stream(c->Einv, d, c->ld, true, h1, c->tg1, s);
+        if (!err) err = upload_stream(c->Einv, d, c->ld, false, h2, c->tg2, s);
         if (err) {
           big_free(Ework, s);
           return cleanup_fail((cudaError_t)err, "upload_stream");
@@ -1528,7 +1526,6 @@ int dk_defl_destroy(dk_defl* c) {
   big_free(c->Einv, s);
   big_free(c->P, s);
   big_free(c->T1, s);
-  big_free(c->T2, s);
   free_stream(c->tg1, s);
   free_stream(c->tg2, s);
   void* bufs[] = {c->perm,     c->iperm,        c->tv,

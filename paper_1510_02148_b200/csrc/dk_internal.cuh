@@ -157,6 +157,13 @@ __device__ __forceinline__ unsigned long long l2_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// set-up constants re-read every iteration (the W tile stream): kept in L2 across the
+// per-iteration basis sweeps, which carry evict-first
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ double2 ld2_stream(const double* ptr, unsigned long long pol) {
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"

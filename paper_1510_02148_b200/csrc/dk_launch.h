@@ -177,7 +177,9 @@ void lauum_into(const double* W, int d, int ld, double* X, cudaStream_t s);
 // ---- coarse solve through W = L^-1 in nested-dissection order (dk_profile.cu) ----
 // a tile stream of k_tgemv: nt 32 x 32 tiles grouped by output block (trow ascending)
 struct TileGemv {
-  const double* T = nullptr;   // [nt][16][32][2]
+  const double* T = nullptr;   // [tiles][16][32][2]
+  const int* tid = nullptr;    // storage index of stream tile t (nullptr: t itself)
+  bool trans = false;          // the stream applies the stored tiles transposed
   const int* trow = nullptr;   // output block per tile
   const int* tcol = nullptr;   // input block per tile
   const int* rfirst = nullptr; // first warp of each output block
@@ -192,6 +194,7 @@ struct TileGemvHost {
   long long nt = 0;
   int nw = 0;
   std::vector<int> trow, tcol, rfirst, rslot, rnp;
+  std::vector<int> tid;  // empty: tiles stored in stream order
   int nslots = 1;
 };
 // E's off-diagonal pattern (CSR, host)
@@ -214,11 +217,14 @@ void launch_permute_sym(const double* E, int d, int ld, const int* perm, double*
                         cudaStream_t s);
 void launch_unpermute_sym(const double* X, int d, int ld, const int* perm, double* out, int ldo,
                           cudaStream_t s);
-// nonzero tiles of W (row profile fW) as the two streams t = W s~ and y~ = W^T t
+// nonzero tiles of W (row profile fW) as the two streams t = W s~ and y~ = W^T t; the tiles
+// are stored once (pass 1's order), pass 2 visits them by block column and applies them
+// transposed
 int profile_streams(const double* W, int d, int ld, const std::vector<int>& fW,
                     TileGemvHost& p1, TileGemvHost& p2, cudaStream_t s);
-// metadata to the device and the tiles packed into g.T (allocated by the caller, nt x 8 KB)
-int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost& h, TileGemv& g,
+// metadata to the device; with pack, W's tiles packed into g.T (allocated by the caller,
+// nt x 8 KB).  A transposed stream (h.tid set) shares the tiles of the packed one.
+int upload_stream(const double* W, int d, int ld, bool pack, const TileGemvHost& h, TileGemv& g,
                   cudaStream_t s);
 void free_stream(TileGemv& g, cudaStream_t s);
 // y[scatter ? scatter[i] : i] = (sum over the stream's tiles) for rows i < d

@@ -157,7 +157,25 @@ __device__ __forceinline__ void tg_issue(unsigned char* b, const double* T,
       : "memory");
 }
 
-template <int KW, int KS>
+// Transposed tile product: lane r holds x_r of the tile's input block and accumulates
+// acc[c] += T[r][c] x_r over every tile of the output block (no shuffles per tile); at the
+// block's end a butterfly transpose-reduction (31 shuffles) leaves column `lane`'s sum in
+// acc[0] of lane `lane`.  The pairing is fixed: deterministic.
+__device__ __forceinline__ double butterfly_sum32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? v[k] : v[k + h];
+      const double keep = up ? v[k + h] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
+template <int KW, int KS, bool TRANS>
 __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* __restrict__ x,
                                                       double* __restrict__ y,
                                                       const int* __restrict__ scatter, int d,
@@ -170,7 +188,13 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   const long long Wn = g.nw;
   const long long w = (long long)blockIdx.x * KW + wl;
   const long long t0 = w < Wn ? w * g.nt / Wn : g.nt, t1 = w < Wn ? (w + 1) * g.nt / Wn : g.nt;
-  const unsigned long long pol = l2_evict_first();
+  // W is re-read by both passes of every iteration: evict-last keeps it L2-resident across
+  // the basis sweeps (evict-first) in between
+  const unsigned long long pol = l2_evict_last();
+  auto tile_ptr = [&](long long t) {
+    const long long q = TRANS ? (long long)__ldg(g.tid + t) : t;
+    return g.T + q * (kPT * kPT);
+  };
   if (lane == 0)
     for (int s = 0; s < KS; ++s) mbar_init1(&bars[wl][s]);
   mbar_init_fence();
@@ -182,7 +206,7 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   const int my_col = (t0 + lane < t1) ? g.tcol[t0 + lane] : 0;
   if (lane == 0)
     for (int s = 0; s < nfirst; ++s)
-      tg_issue(wbuf + s * kPTileBytes, g.T + (t0 + s) * (kPT * kPT), &bars[wl][s], pol);
+      tg_issue(wbuf + s * kPTileBytes, tile_ptr(t0 + s), &bars[wl][s], pol);
   pdl_wait();
   const bool off = gate != nullptr && *gate == 0;
   if (off || t0 >= t1) {  // drain the copies already in flight, then leave
@@ -197,6 +221,9 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   }
   int R = __shfl_sync(0xffffffffu, my_row, 0);
   double racc = 0.0;
+  double acc[TRANS ? 32 : 1];
+#pragma unroll
+  for (int c = 0; c < (TRANS ? 32 : 1); ++c) acc[c] = 0.0;
   for (long long t = t0; t < t1; ++t) {
     const int k = (int)(t - t0);
     const int s = k % KS;
@@ -214,18 +241,32 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
     }
     mbar_wait_parity(&bars[wl][s], parity);
     const double2* T = reinterpret_cast<const double2*>(wbuf + s * kPTileBytes);
+    if constexpr (TRANS) {
 #pragma unroll
-    for (int p = 0; p < 16; ++p) {
-      const double2 a = T[p * kPT + lane];
-      racc = fma(a.x, __shfl_sync(0xffffffffu, xv, 2 * p), racc);
-      racc = fma(a.y, __shfl_sync(0xffffffffu, xv, 2 * p + 1), racc);
+      for (int p = 0; p < 16; ++p) {
+        const double2 a = T[p * kPT + lane];
+        acc[2 * p] = fma(a.x, xv, acc[2 * p]);
+        acc[2 * p + 1] = fma(a.y, xv, acc[2 * p + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        const double2 a = T[p * kPT + lane];
+        racc = fma(a.x, __shfl_sync(0xffffffffu, xv, 2 * p), racc);
+        racc = fma(a.y, __shfl_sync(0xffffffffu, xv, 2 * p + 1), racc);
+      }
     }
     __syncwarp();
     if (lane == 0 && t + KS < t1)  // refill this stage
-      tg_issue(wbuf + s * kPTileBytes, g.T + (t + KS) * (kPT * kPT), &bars[wl][s], pol);
+      tg_issue(wbuf + s * kPTileBytes, tile_ptr(t + KS), &bars[wl][s], pol);
     const int Rn = (t + 1 < t1) ? row_n : -1;
     if (Rn == R) continue;
     // output block R ends in this warp's range
+    if constexpr (TRANS) {
+      racc = butterfly_sum32(acc, lane);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+    }
     const int np = g.rnp[R];
     double out = racc;
     bool write = true;
@@ -597,16 +638,18 @@ int profile_streams(const double* W, int d, int ld, const std::vector<int>& fW,
   std::vector<long long> idx(ai.size());
   for (size_t k = 0; k < idx.size(); ++k) idx[k] = (long long)k;
   std::stable_sort(idx.begin(), idx.end(), [&](long long a, long long b) { return aj[a] < aj[b]; });
-  std::vector<int> bi(ai.size()), bj(ai.size());
+  std::vector<int> bi(ai.size()), bj(ai.size()), bt(ai.size());
   for (size_t k = 0; k < idx.size(); ++k) {
     bi[k] = aj[idx[k]];  // output block of W^T
     bj[k] = ai[idx[k]];  // input block
+    bt[k] = (int)idx[k];  // the tile in pass 1's storage
   }
   if (build_stream(ai, aj, nb, p1) || build_stream(bi, bj, nb, p2)) return -1;
+  p2.tid = std::move(bt);
   return 0;
 }
 
-int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost& h, TileGemv& g,
+int upload_stream(const double* W, int d, int ld, bool pack, const TileGemvHost& h, TileGemv& g,
                   cudaStream_t s) {
   const int nrows = (int)h.rnp.size();
   g.nt = h.nt;
@@ -619,6 +662,10 @@ int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost
       e = cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, s);
   };
   int *trow = nullptr, *tcol = nullptr, *rfirst = nullptr, *rslot = nullptr, *rnp = nullptr;
+  int* tid = nullptr;
+  if (!h.tid.empty()) up(&tid, h.tid);
+  g.tid = tid;
+  g.trans = !h.tid.empty();
   up(&trow, h.trow);
   up(&tcol, h.tcol);
   up(&rfirst, h.rfirst);
@@ -635,17 +682,18 @@ int upload_stream(const double* W, int d, int ld, bool trans, const TileGemvHost
     e = cudaMemsetAsync(g.part, 0xff, (size_t)h.nslots * kPT * sizeof(double), s);
   if (e != cudaSuccess) return (int)e;
   // the tile stream itself (big_alloc'd by the caller into g.T)
-  k_tile_pack<<<num_sms() * 8, 256, 0, s>>>(W, d, ld, trow, tcol, h.nt, trans ? 1 : 0,
-                                      const_cast<double*>(g.T));
+  if (pack)
+    k_tile_pack<<<num_sms() * 8, 256, 0, s>>>(W, d, ld, trow, tcol, h.nt, 0,
+                                              const_cast<double*>(g.T));
   return (int)cudaGetLastError();
 }
 
 void free_stream(TileGemv& g, cudaStream_t s) {
   void* bufs[] = {(void*)g.trow, (void*)g.tcol, (void*)g.rfirst, (void*)g.rslot, (void*)g.rnp,
-                  (void*)g.part};
+                  (void*)g.part, (void*)g.tid};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);
-  g.trow = g.tcol = g.rfirst = g.rslot = g.rnp = nullptr;
+  g.trow = g.tcol = g.rfirst = g.rslot = g.rnp = g.tid = nullptr;
   g.part = nullptr;
 }
 
@@ -669,9 +717,16 @@ template <int KW, int KS>
 static void launch_tg(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
                       const int* gate, cudaStream_t s) {
   const size_t smem = (size_t)KW * KS * kPTileBytes;
-  smem_optin((const void*)k_tgemv<KW, KS>, smem);
   const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
-  launch_pdl(k_tgemv<KW, KS>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d, gate);
+  if (g.trans) {
+    smem_optin((const void*)k_tgemv<KW, KS, true>, smem);
+    launch_pdl(k_tgemv<KW, KS, true>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d,
+               gate);
+  } else {
+    smem_optin((const void*)k_tgemv<KW, KS, false>, smem);
+    launch_pdl(k_tgemv<KW, KS, false>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d,
+               gate);
+  }
 }
 
 void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
