@@ -206,10 +206,14 @@ def _rotate(col, cs, sn, g, j):
 
 
 def run_cycles(A, b, x0=None, inv_diag=None, m=30, tol=1e-6, max_iters=300, min_iters=0,
-               defl=None, max_cycles=None):
+               defl=None, max_cycles=None, gs="mgs"):
     """Restarted right-preconditioned GMRES(m) on P1 A M^-1 (krylov.py:107-236).
 
-    Returns a dict with the SolveReport fields the device path reports.
+    gs="mgs" is the reference's modified Gram-Schmidt (krylov.py:163-166); gs="cgs" is the
+    classical variant (all h_i = V_i . w from the same w, then one update) that the device
+    path computes — used to separate the MGS-vs-CGS rounding spread from device error on
+    ill-conditioned cases (config 4).  Returns a dict with the SolveReport fields the device
+    path reports.
     """
     n = A.shape[0]
     pre = (lambda v: v) if inv_diag is None else (lambda v: v * inv_diag)
@@ -253,10 +257,15 @@ def run_cycles(A, b, x0=None, inv_diag=None, m=30, tol=1e-6, max_iters=300, min_
             if defl is not None:
                 w = defl.apply_p1(w)
             w0 = float(np.linalg.norm(w))
-            for i in range(j + 1):          # modified Gram-Schmidt
-                h = float(V[i] @ w)
-                H[i, j] = h
-                w -= h * V[i]
+            if gs == "cgs":                 # classical Gram-Schmidt
+                h = V[:j + 1] @ w
+                H[:j + 1, j] = h
+                w -= V[:j + 1].T @ h
+            else:
+                for i in range(j + 1):      # modified Gram-Schmidt
+                    h = float(V[i] @ w)
+                    H[i, j] = h
+                    w -= h * V[i]
             c = V[:j + 1] @ w               # selective re-orthogonalisation
             if np.max(np.abs(c), initial=0.0) > REORTH_TOL * max(w0, 1e-300):
                 w -= V[:j + 1].T @ c

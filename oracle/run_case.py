@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--plain", action="store_true", help="no deflation (gmres)")
     ap.add_argument("--max-cycles", type=int, default=None)
     ap.add_argument("--full-x", action="store_true")
+    ap.add_argument("--cgs", action="store_true", help="classical Gram-Schmidt (the device's)")
     ap.add_argument("--out", default=None)
     ap.add_argument("--save-xhat", default=None, help="x before reconstruct (.npy, not committed)")
     a = ap.parse_args()
@@ -63,11 +64,11 @@ def main():
         defl = O.LabelDeflation(Ac, col, dcol, b, inv)
     t1 = time.time()
     r = O.run_cycles(Ac, b, None, inv, case.m, case.tol, case.max_iters, 0, defl,
-                     max_cycles=a.max_cycles)
+                     max_cycles=a.max_cycles, gs="cgs" if a.cgs else "mgs")
     t2 = time.time()
     print(f"config{a.config} {'plain' if a.plain else 'deflated'} d={d} "
           f"iters={r['iterations']} cycles={r['cycles']} converged={r['converged']} "
-          f"relres={r['final_relres']:.3e} reorths={r['reorths']} setup={t1 - t0:.1f}s "
+          f"gs={'cgs' if a.cgs else 'mgs'} relres={r['final_relres']:.3e} reorths={r['reorths']} setup={t1 - t0:.1f}s "
           f"solve={t2 - t1:.1f}s threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
           flush=True)
     if a.save_xhat:

@@ -1889,3 +1889,38 @@ int dk_assemble_tpfa(int32_t nx, int32_t ny, int32_t nz, double dx, double dy, d
 }
 
 }  // extern "C"
+
+#ifdef DK_TIMELINE
+// ---- diagnostic builds only: the kernel timeline (tools/timeline.py) -------------------
+namespace dk {
+void tl_set_kernels(const TlBuf& b);
+void tl_set_profile(const TlBuf& b);
+}  // namespace dk
+static dk::TlBuf g_tl_host{};
+extern "C" int dk_timeline_enable(uint32_t cap) {
+  if (g_tl_host.rec) {
+    cudaFree(g_tl_host.rec);
+    cudaFree(g_tl_host.cnt);
+    g_tl_host = {};
+  }
+  if (cap) {
+    cudaMalloc(&g_tl_host.rec, (size_t)cap * 16);
+    cudaMalloc(&g_tl_host.cnt, sizeof(unsigned));
+    cudaMemset(g_tl_host.cnt, 0, sizeof(unsigned));
+    g_tl_host.cap = cap;
+  }
+  dk::tl_set_kernels(g_tl_host);
+  dk::tl_set_profile(g_tl_host);
+  return (int)cudaDeviceSynchronize();
+}
+extern "C" int64_t dk_timeline_read(uint64_t* out, uint32_t cap) {
+  unsigned n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(&n, g_tl_host.cnt, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  if (n > g_tl_host.cap) n = g_tl_host.cap;
+  if (n > cap) n = cap;
+  cudaMemcpy(out, g_tl_host.rec, (size_t)n * 16, cudaMemcpyDeviceToHost);
+  cudaMemset(g_tl_host.cnt, 0, sizeof(unsigned));
+  return n;
+}
+#endif

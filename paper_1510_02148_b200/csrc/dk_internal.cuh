@@ -136,6 +136,55 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return e;
 }
 
+// ---- timeline instrumentation (diagnostic builds with -DDK_TIMELINE only) ------------
+// Thread 0 of a block records (globaltimer ns, kernel kind, phase, block) at phase points;
+// tools/timeline.py reads the records back (dk_timeline_* in dk_api.cu) and lays out the
+// kernels of one iteration.  Each translation unit holds its own copy of the buffer handle.
+struct TlBuf {
+  unsigned long long* rec;
+  unsigned* cnt;
+  unsigned cap;
+};
+#ifdef DK_TIMELINE
+static __device__ TlBuf g_tl;
+__device__ __forceinline__ void tl_mark(unsigned kind, unsigned phase) {
+  if (threadIdx.x == 0 && g_tl.rec != nullptr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(g_tl.cnt, 1u);
+    if (i < g_tl.cap) {
+      g_tl.rec[2 * i] = t;
+      g_tl.rec[2 * i + 1] = ((unsigned long long)kind << 56) |
+                            ((unsigned long long)phase << 48) | (unsigned long long)blockIdx.x;
+    }
+  }
+}
+// per-warp variant (lane 0 of each warp; "block" field = block * 32 + warp)
+__device__ __forceinline__ void tl_mark_warp(unsigned kind, unsigned phase) {
+  if ((threadIdx.x & 31) == 0 && g_tl.rec != nullptr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(g_tl.cnt, 1u);
+    if (i < g_tl.cap) {
+      g_tl.rec[2 * i] = t;
+      g_tl.rec[2 * i + 1] = ((unsigned long long)kind << 56) |
+                            ((unsigned long long)phase << 48) |
+                            (unsigned long long)(blockIdx.x * 32 + (threadIdx.x >> 5));
+    }
+  }
+}
+#define DK_TL(kind, phase) ::dk::tl_mark(kind, phase)
+#define DK_TLW(kind, phase) ::dk::tl_mark_warp(kind, phase)
+#define DK_TL_SETTER(fn) \
+  void fn(const TlBuf& b) { cudaMemcpyToSymbol(g_tl, &b, sizeof(TlBuf)); }
+#else
+#define DK_TL(kind, phase) ((void)0)
+#define DK_TLW(kind, phase) ((void)0)
+#define DK_TL_SETTER(fn)
+#endif
+enum TlKind { TL_STENCIL = 1, TL_RESTRICT = 2, TL_TG1 = 3, TL_TG2 = 4, TL_PROJECT = 5, TL_GS = 6,
+              TL_TG1W = 7, TL_TG2W = 8 };
+
 // ---- small device helpers -------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -168,6 +217,30 @@ __device__ __forceinline__ double2 ld2_stream(const double* ptr, unsigned long l
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(v.x), "=d"(v.y)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+// Set-up constants read once per iteration (operator diagonals, M^-1, labels, prolongation
+// map) also stream with evict-first: only the W tile stream (evict-last) is meant to stay in
+// L2 across iterations.
+__device__ __forceinline__ int2 ldi2_stream(const int* ptr, unsigned long long pol) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int4 ldi4_stream(const int* ptr, unsigned long long pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ unsigned short ldu16_stream(const void* ptr, unsigned long long pol) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+               : "=h"(v)
                : "l"(ptr), "l"(pol));
   return v;
 }

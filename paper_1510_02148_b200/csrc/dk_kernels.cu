@@ -319,19 +319,20 @@ struct Sym7Pair {
 
 template <bool PRE>
 __device__ __forceinline__ void sym7_load(Sym7Pair& q, const Dia& A, const double* __restrict__ v,
-                                          long long i, long long nx, long long nz) {
-  q.c = ld2(A.co[3] + i);
-  q.u1 = ld2(A.co[4] + i);
-  q.u1m = ld2(A.co[4] + i - 2);
-  q.ux = ld2(A.co[5] + i);
-  q.uxm = ld2(A.co[5] + i - nx);
-  q.uz = ld2(A.co[6] + i);
-  q.uzm = ld2(A.co[6] + i - nz);
+                                          long long i, long long nx, long long nz,
+                                          unsigned long long pol) {
+  q.c = ld2_stream(A.co[3] + i, pol);
+  q.u1 = ld2_stream(A.co[4] + i, pol);
+  q.u1m = ld2_stream(A.co[4] + i - 2, pol);
+  q.ux = ld2_stream(A.co[5] + i, pol);
+  q.uxm = ld2_stream(A.co[5] + i - nx, pol);
+  q.uz = ld2_stream(A.co[6] + i, pol);
+  q.uzm = ld2_stream(A.co[6] + i - nz, pol);
   q.vm = ld2(v + i - nz);
   q.vp = ld2(v + i + nz);
   if (PRE) {
-    q.im = ld2(A.inv + i - nz);
-    q.ip = ld2(A.inv + i + nz);
+    q.im = ld2_stream(A.inv + i - nz, pol);
+    q.ip = ld2_stream(A.inv + i + nz, pol);
   }
 }
 
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
                                                            const int* __restrict__ gate, int H,
                                                            const unsigned* wait,
                                                            const double* gsig, int ng) {
+  DK_TL(TL_STENCIL, 0);
   if (wait != nullptr) {
     // the tile's operator diagonals, M^-1 and labels are final: into L2 while waiting
     const long long b0 = (long long)blockIdx.x * kTile;
@@ -390,6 +392,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
     pdl_wait();
     if (gate != nullptr && *gate == 0) return;
   }
+  DK_TL(TL_STENCIL, 1);
+  pdl_trigger();  // the next grid launches while this one runs (it still waits for it)
   extern __shared__ __align__(16) double sp[];  // [H | kTile | H]
   __shared__ double sw[RESTRICT ? kTilePad : 2];
   __shared__ int sl[RESTRICT ? kTilePad : 2];
@@ -398,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
   const long long nx = A.off[5], nz = A.off[6];
   const bool has_scale = scale != nullptr;
   const double sc = !has_scale ? 1.0 : wait != nullptr ? early_sigma(gsig, ng) : __ldcg(scale);
+  const unsigned long long pol = l2_evict_first();
   for (int e = threadIdx.x; e < (kTile + 2 * H) / 2; e += kThreads) {
     const long long i = base - H + 2 * e;
     double2 x = ld2(v + i);
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
       x.y = __dmul_rn(x.y, sc);
     }
     if (PRE) {
-      const double2 m = ld2(A.inv + i);
+      const double2 m = ld2_stream(A.inv + i, pol);
       x.x = __dmul_rn(x.x, m.x);
       x.y = __dmul_rn(x.y, m.y);
     }
@@ -416,14 +421,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
   if (RESTRICT)
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      lb[k] = *reinterpret_cast<const int2*>(lab + base + 2 * threadIdx.x + 512 * k);
+      lb[k] = ldi2_stream(lab + base + 2 * threadIdx.x + 512 * k, pol);
   __syncthreads();
   double rr[8];
   const double* pp = sp + H + 2 * threadIdx.x;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     Sym7Pair q;
-    sym7_load<PRE>(q, A, v, base + 2 * threadIdx.x + 512 * k, nx, nz);
+    sym7_load<PRE>(q, A, v, base + 2 * threadIdx.x + 512 * k, nx, nz, pol);
     const double2 r = sym7_apply<PRE>(q, pp + 512 * k, nx, sc, has_scale);
     rr[2 * k] = r.x;
     rr[2 * k + 1] = r.y;
@@ -434,7 +439,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
       st2(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
   if (RESTRICT)
     stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  DK_TL(TL_STENCIL, 3);
   if (wait != nullptr) pdl_wait();
+  DK_TL(TL_STENCIL, 4);
 }
 
 // halo of k_stencil_sym7, or 0 when the operator is not the symmetric even 7-point stencil
@@ -532,7 +539,10 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
                                                              double* __restrict__ s,
                                                              const int* __restrict__ s_pos,
                                                              const int* __restrict__ gate) {
+  DK_TL(TL_RESTRICT, 0);
+  pdl_trigger();  // the tile GEMV's prologue (tile prefetch) overlaps this grid
   pdl_wait();
+  DK_TL(TL_RESTRICT, 1);
   if (gate != nullptr && *gate == 0) return;
   if ((int)blockIdx.x < short_blocks) {
     // one thread per column with at most kShortRuns runs, serial in run order
@@ -548,6 +558,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
     for (int k = 0; k < kShortRuns; ++k)
       if (k < len) acc += v[k];
     s[s_pos ? s_pos[L] : L] = acc;
+    DK_TL(TL_RESTRICT, 4);
     return;
   }
   // one warp per long column (lane-strided, kLongBatch loads per lane in flight, fixed xor tree)
@@ -568,6 +579,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
   }
   acc = warp_sum(acc);
   if (lane == 0) s[s_pos ? s_pos[L] : L] = acc;
+  DK_TL(TL_RESTRICT, 4);
 }
 
 void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s) {
@@ -895,7 +907,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
                                                       long long vstride, int nvec, long long n_pad,
                                                       double* __restrict__ part, int G, Scal sc,
                                                       int j, const int* __restrict__ gate) {
+  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 0);
   pdl_wait();
+  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 1);
   // the stencil of this iteration has completed: re-arm its early-start flag
   if (MODE == PJ_ITER && sc.post != nullptr && j >= 1 && blockIdx.x == 0 && threadIdx.x == 0) {
     sc.post[j - 1] = 0u;            // consumed by this iteration's stencil
@@ -925,14 +939,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
       xin[k] = (MODE == PJ_REDOTS) ? ld2cg(w_in + i) : ld2(w_in + i);
     }
     if (DEFL == DK_LABELS) {
+      const unsigned long long cpol = l2_evict_first();
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const long long i = cb + 512 * k;
-        const int2 L = *reinterpret_cast<const int2*>(P.lab + i);
-        const double2 ow = ld2(P.own + i);
-        const int4 fl = *reinterpret_cast<const int4*>(P.flab + i);
-        const double4 fc = *reinterpret_cast<const double4*>(P.fco + i);
-        const uchar2 mk = *reinterpret_cast<const uchar2*>(P.mask + i);
+        const int2 L = ldi2_stream(P.lab + i, cpol);
+        const double2 ow = ld2_stream(P.own + i, cpol);
+        const int4 fl = ldi4_stream(reinterpret_cast<const int*>(P.flab + i), cpol);
+        const double2 fa = ld2_stream(reinterpret_cast<const double*>(P.fco + i), cpol);
+        const double2 fb = ld2_stream(reinterpret_cast<const double*>(P.fco + i) + 2, cpol);
+        const double4 fc = make_double4(fa.x, fa.y, fb.x, fb.y);
+        const unsigned short mw = ldu16_stream(P.mask + i, cpol);
+        const uchar2 mk = make_uchar2((unsigned char)(mw & 0xff), (unsigned char)(mw >> 8));
         xin[k].x = __dsub_rn(xin[k].x, prolong_cell<AM>(A, P, yc, i, L.x, ow.x, fl.x, fl.y,
                                                         fc.x, fc.y, mk.x));
         xin[k].y = __dsub_rn(xin[k].y, prolong_cell<AM>(A, P, yc, i + 1, L.y, ow.y, fl.z, fl.w,
@@ -959,6 +977,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
       w[2 * k + 1] = x.y;
       if (MODE != PJ_REDOTS && (DEFL != DK_NONE || w_out != w_in)) st2(w_out + i, x);
     }
+    if (MODE == PJ_ITER && ch == blockIdx.x) DK_TL(TL_PROJECT, 2);
     if (MODE == PJ_ITER || MODE == PJ_RESTART) {
       double nrm = 0.0;
 #pragma unroll
@@ -1011,6 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
       __syncthreads();  // the next chunk reuses s_w / s_vj
     }
   }
+  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 3);
   pdl_trigger();
   if (MODE == PJ_PLAIN) return;
   __syncthreads();
@@ -1021,8 +1041,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
   }
   if (!reduce_grouped(part, nq, G, sc.gticket, sc.gpart, red,
                       (MODE == PJ_ITER && sc.post != nullptr) ? sc.post + (sc.m + 1) + j
-                                                              : nullptr))
+                                                              : nullptr)) {
+    if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 4);
     return;
+  }
   State* st = sc.st;
   const int m = sc.m;
   if (MODE == PJ_RESTART) {
@@ -1048,6 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
   }
   (void)st;
   iter_finish(sc, j, nvec, red);
+  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 5);
 }
 
 template <int MODE, int DEFL, bool AM>
@@ -1283,6 +1306,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
                                                  double* __restrict__ part, int G, Scal sc, int j,
                                                  const int* __restrict__ gate, int fuse,
                                                  const unsigned* wait) {
+  if (!REORTH) DK_TL(TL_GS, 0);
   // early start (wait != nullptr): on the projection's published coefficients; its
   // re-orthogonalisation verdict is read after its completion (griddepcontrol.wait below)
   if (wait != nullptr) {
@@ -1296,6 +1320,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     pdl_wait();
     if (*gate == 0) return;
   }
+  if (!REORTH) DK_TL(TL_GS, 1);
   extern __shared__ double sh[];
   double* cf = sh;                                  // [nvec]
   double* red = sh + nvec;                          // [kWarps] (+ scratch)
@@ -1347,6 +1372,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     nrm = warp_sum(nrm);
     if (lane == 0) red[warp] += nrm;
   }
+  if (!REORTH) DK_TL(TL_GS, 3);
   if (wait != nullptr) pdl_wait();
   const bool second =
       !REORTH && fuse && *reinterpret_cast<const volatile int*>(&sc.st->reorth) != 0;
@@ -1440,12 +1466,15 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   }
   const bool early = !REORTH && sc.post != nullptr;  // the next stencil forms sigma itself
   if (!reduce_grouped(part, 1, G, sc.gticket, early ? sc.gpart_gs : sc.gpart, red,
-                      early ? sc.post + j : nullptr))
+                      early ? sc.post + j : nullptr)) {
+    if (!REORTH) DK_TL(TL_GS, 4);
     return;
+  }
   const double hj1 = sqrt(red[0]);
   __syncthreads();
   if (!REORTH && !second && sc.st->reorth) return;  // the separate second pass finishes it
   finish_iteration_block(sc, j, hj1, red);
+  if (!REORTH) DK_TL(TL_GS, 5);
 }
 
 static size_t gs_smem(const Scal& sc, int nvec) {
@@ -1712,5 +1741,7 @@ void launch_resume_state(const Scal& sc, int iterations, int cycles, int warning
                          double denom, double prev_beta, cudaStream_t s) {
   k_resume_state<<<1, 1, 0, s>>>(sc, iterations, cycles, warning, has_prev, denom, prev_beta);
 }
+
+DK_TL_SETTER(tl_set_kernels)
 
 }  // namespace dk

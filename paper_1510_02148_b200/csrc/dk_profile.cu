@@ -180,6 +180,8 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
                                                       double* __restrict__ y,
                                                       const int* __restrict__ scatter, int d,
                                                       const int* __restrict__ gate) {
+  DK_TL(TRANS ? TL_TG2 : TL_TG1, 0);
+  DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 0);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long bars[KW][KS];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -207,7 +209,11 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   if (lane == 0)
     for (int s = 0; s < nfirst; ++s)
       tg_issue(wbuf + s * kPTileBytes, tile_ptr(t0 + s), &bars[wl][s], pol);
+  // the next grid may launch now (its griddepcontrol.wait still waits for this one)
+  pdl_trigger();
   pdl_wait();
+  DK_TL(TRANS ? TL_TG2 : TL_TG1, 1);
+  DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 1);
   const bool off = gate != nullptr && *gate == 0;
   if (off || t0 >= t1) {  // drain the copies already in flight, then leave
     for (int s = 0; s < nfirst; ++s) mbar_wait_parity(&bars[wl][s], 0);
@@ -270,6 +276,7 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
     const int np = g.rnp[R];
     double out = racc;
     bool write = true;
+    if (np > 1 && w == g.rfirst[R]) DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 2 + (np > 32 ? 1 : 0));
     if (np > 1) {
       // A block split across warps is finished by its first warp (whose range ends with it,
       // so the others' pieces, at the starts of their ranges, are normally in by then).  The
@@ -282,13 +289,16 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
         write = false;
       } else {
         out = 0.0 + racc;
-        for (int k0 = 1; k0 < np; k0 += 8) {  // eight slots in flight, then the in-order sum
-          double v[8];
+        // kFin slots in flight (the long block rows of the root separators are split over
+        // tens of warps), then the in-order sum
+        constexpr int kFin = TRANS ? 8 : 32;
+        for (int k0 = 1; k0 < np; k0 += kFin) {
+          double v[kFin];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < kFin; ++i)
             v[i] = k0 + i < np ? ld_volatile_f64(slots + (long long)(k0 + i) * kPT) : 0.0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < kFin; ++i) {
             if (k0 + i >= np) break;
             double* sl = slots + (long long)(k0 + i) * kPT;
             while (is_sentinel(v[i])) {
@@ -304,10 +314,13 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
     if (write) {
       const int row = R * kPT + lane;
       if (row < d) y[scatter ? scatter[row] : row] = out;
+      if (np > 1) DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 4 + (np > 32 ? 1 : 0));
     }
     racc = 0.0;
     R = Rn;
   }
+  DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 6);
+  DK_TL(TRANS ? TL_TG2 : TL_TG1, 4);
 }
 
 }  // namespace
@@ -740,5 +753,7 @@ void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scat
     default: launch_tg<12, 2>(g, x, y, scatter, d, gate, s); break;
   }
 }
+
+DK_TL_SETTER(tl_set_profile)
 
 }  // namespace dk
