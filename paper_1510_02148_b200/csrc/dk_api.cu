@@ -41,6 +41,13 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(_e, #x);     \
   } while (0)
 
+// record the first error of a launch sequence (graph capture reports late)
+#define DK_LOG_ERR(x)                                                    \
+  do {                                                                   \
+    cudaError_t _e = (x);                                                \
+    if (_e != cudaSuccess && launch_error() == cudaSuccess) launch_error() = _e; \
+  } while (0)
+
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
 // ---- profiling classes ---------------------------------------------------------------
@@ -55,12 +62,13 @@ enum ProfClass {
   PC_XUPDATE,
   PC_RESTART,
   PC_COARSE_REDUCE,
+  PC_DOTS,
   PC_COUNT
 };
 const char* kProfNames[PC_COUNT] = {"stencil_restrict", "restrict_final", "coarse_gemv",
                                     "prolong_dots",     "gs_update",      "gs_reorth",
                                     "cycle_end",        "x_update",       "restart",
-                                    "coarse_reduce"};
+                                    "coarse_reduce",    "basis_dots"};
 
 unsigned long long g_ctx_serial = 0;
 
@@ -101,6 +109,11 @@ struct dk_op {
   double* nrm = nullptr;  // [4] device norms
   unsigned int* tickets = nullptr;
   bool gs_fuse = false;  // second Gram-Schmidt pass inside k_gs (whole grid co-resident)
+  // split iteration: the basis sweep runs on `aux` beside the coarse solve
+  bool split = false;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int G_dots = 1;
   unsigned int* gticket = nullptr;  // reduce_grouped counters
   double* gpart = nullptr;          // reduce_grouped group partials [part_q x kGroupTickets]
   int* one = nullptr;  // device constant 1 (gate of ungated launches)
@@ -130,6 +143,8 @@ struct dk_op {
   std::vector<double> ev_bytes;
   int launches = 0;
   bool has_last = false;
+  unsigned long long g_split = 0;  // split flag the graph was captured with
+  int cur_j = 0;                   // iteration being issued (split_fork)
 };
 
 struct dk_defl {
@@ -176,6 +191,11 @@ struct dk_defl {
   float ms[4] = {0, 0, 0, 0};
   RunMap rm{};
   double nmasked = 0;  // masked (third+ foreign label) coefficients (byte accounting)
+  // split iteration: run sums of A_p^T v_j and C = [c_0 .. c_m] (c_j = Z^T A_p^T v_j)
+  double* run_part2 = nullptr;
+  double* cmat = nullptr;
+  int cmat_rows = 0;
+  long long ldc = 0;
   // dense basis (non-indicator Z, d <= kDenseMaxD): rows Z_k and A_p Z_k, guarded like V
   int dense = 0;
   double* Z_base = nullptr;
@@ -362,7 +382,7 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   }
   if (op->scal_m < m) {
     if (op->scal) DK_TRY(cudaFreeAsync(op->scal, op->stream));
-    const size_t cnt = 7 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
+    const size_t cnt = 9 * (size_t)(m + 1) + 2 * (size_t)(m + 1) * m + 2 * (size_t)m +
                        (size_t)(m + 1) * (m + 1);
     DK_TRY(cudaMallocAsync(&op->scal, cnt * sizeof(double), op->stream));
     DK_TRY(cudaMemsetAsync(op->scal, 0, cnt * sizeof(double), op->stream));
@@ -409,10 +429,41 @@ int ensure_work(dk_op* op, int m, int max_iters) {
   }
   if (!op->gs_fuse) sc.post = nullptr;
   p += m + 1;
+  sc.hraw = p;
+  p += 2 * (size_t)(m + 1);
+  sc.split = 0;
+  sc.cmat = nullptr;
+  sc.ldc = 0;
+  sc.dco = 0;
   sc.gpart_gs = op->gpart + (size_t)(op->part_q - 1) * kGroupTickets;  // past the dots' rows
   sc.hist = op->hist;
   sc.restart_of = op->rof;
   return DK_OK;
+}
+
+// The W tile store is read twice per iteration.  DK_W_PERSIST=1: an L2 persisting set-aside
+// of its size for the tile GEMV launches (device-wide limit raised to the largest store in
+// use, never lowered).  Measured slower than the evict-last hints (6,250 vs 6,600 it/s at
+// config 3) and it does not keep pass 1's tiles resident either: off.
+void set_tile_window(dk_defl* c, size_t bytes) {
+  c->tg1.win_bytes = c->tg2.win_bytes = 0;
+  if (!getenv("DK_W_PERSIST")) return;
+  int dev = 0, maxp = 0, maxw = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (bytes > (size_t)maxp || bytes > (size_t)maxw) return;
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (cur < bytes && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  c->tg1.win_base = c->tg2.win_base = c->T1;
+  c->tg1.win_bytes = c->tg2.win_bytes = bytes;
 }
 
 // ---- launch bookkeeping (profiling) ---------------------------------------------------
@@ -464,9 +515,13 @@ void prof_collect(dk_op* op) {
 
 // ---- the deflation building blocks ------------------------------------------------------
 // s = Z^T (mode-applied v) ; y = E^-1 s
+void split_fork(dk_op* op, dk_defl* c, const double* vj);
+
+// split_row (split iteration, ST_APPLY): also c_j = Z^T A_p^T v_j into that row of C, and the
+// basis sweep forked onto the auxiliary stream right after the stencil
 void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const double* v,
                   const double* scale, const double* b, double* out, const int* gate,
-                  const unsigned* wait = nullptr) {
+                  const unsigned* wait = nullptr, double* split_row = nullptr) {
   const Dia A = make_dia(op, pre);
   const double n = (double)op->n;
   if (c->dense) {  // stencil (stored), then s = Z^T w and y = E^-1 s in one multi-dot kernel
@@ -490,13 +545,20 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
     const double by = 12.0 + (write ? 8.0 : 0.0) +
                       (mode == ST_IDENT ? 0.0 : 8.0 * op->nstore + (pre ? 8.0 : 0.0));
     ProfScope ps(op, PC_STENCIL, by * n);
-    launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream,
-                   wait, op->sc.gpart_gs, op->sc.ng);
+    if (split_row != nullptr)
+      launch_stencil_split(pre, c->ap == DK_AP_AM, A, op->n_pad, v, scale, out, c->rm,
+                           c->run_part2, gate, op->stream, wait, op->sc.gpart_gs, op->sc.ng);
+    else
+      launch_stencil(mode, pre, write, A, op->n_pad, v, scale, b, out, &c->rm, gate, op->stream,
+                     wait, op->sc.gpart_gs, op->sc.ng);
   }
+  if (split_row != nullptr) split_fork(op, c, v);
+  const double rbytes = (split_row ? 2.0 : 1.0) * (12.0 * (double)c->nlabelled + 8.0 * c->d);
   if (c->prof) {  // s~ = P Z^T w, then the two tile streams (t = W s~, y = P^T W^T t)
     {
-      ProfScope ps(op, PC_RESTRICT, 12.0 * (double)c->nlabelled + 8.0 * c->d);
-      launch_restrict_final(c->rm, c->s, gate, op->stream);
+      ProfScope ps(op, PC_RESTRICT, rbytes);
+      launch_restrict_final(c->rm, c->s, gate, op->stream, split_row ? c->run_part2 : nullptr,
+                            split_row);
     }
     ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)(c->tg1.nt + c->tg2.nt));
     launch_tgemv(c->tg1, c->s, c->tv, nullptr, c->d, gate, op->stream);
@@ -504,8 +566,9 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
     return;
   }
   {
-    ProfScope ps(op, PC_RESTRICT, 12.0 * (double)c->nlabelled + 8.0 * c->d);
-    launch_restrict_final(c->rm, c->s, gate, op->stream);
+    ProfScope ps(op, PC_RESTRICT, rbytes);
+    launch_restrict_final(c->rm, c->s, gate, op->stream, split_row ? c->run_part2 : nullptr,
+                          split_row);
   }
   {
     if (c->sym) {
@@ -522,6 +585,33 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
       launch_gemv(c->Einv, c->d, c->ld, c->s, c->y, gate, op->stream);
     }
   }
+}
+
+// The split iteration's basis sweep: h' = U^T w and the Gram column U^T u_j (reduced into
+// sc.hraw), on the auxiliary stream between ev_fork (after the stencil) and ev_join (waited
+// before the projection's fix-up).  An event-profiled solve keeps it on the main stream.
+void split_fork(dk_op* op, dk_defl* c, const double* vj) {
+  (void)c;
+  (void)vj;
+  State* st = op->st;
+  Scal sc = op->sc;
+  if (op->prof) sc.post = nullptr;
+  const int j = op->cur_j;
+  const int nvec = j + 1;
+  double* V = op->V_base + op->guard;
+  const double n = (double)op->n;
+  cudaStream_t s = op->prof ? op->stream : op->aux;
+  if (!op->prof) {
+    DK_LOG_ERR(cudaEventRecord(op->ev_fork, op->stream));
+    DK_LOG_ERR(cudaStreamWaitEvent(op->aux, op->ev_fork, 0));
+  }
+  {
+    ProfScope ps(op, PC_DOTS, (8.0 + 8.0 * nvec) * n);
+    launch_project(PJ_DOTS, DK_NONE, false, make_dia(op, false), Prolong{}, nullptr, op->w,
+                   op->w, V, op->vstride, nvec, op->n_pad, op->part, op->G_dots, sc, j,
+                   &st->active, s, op->prof);
+  }
+  if (!op->prof) DK_LOG_ERR(cudaEventRecord(op->ev_join, op->aux));
 }
 
 // One GMRES(m) cycle as a fixed kernel sequence (restart, m Arnoldi steps, cycle end).
@@ -550,8 +640,10 @@ void issue_restart(dk_op* op, dk_defl* c) {
 }
 
 int read_state(dk_op* op);
+int setup_split(dk_op* op, dk_defl* c, int m);
 
 void issue_iteration(dk_op* op, dk_defl* c, int j) {
+  op->cur_j = j;
   // an event-profiled (launch-per-kernel) solve serialises the kernel boundaries, so each
   // kernel's event time is its own (no early start across the control tails)
   Scal sc = op->sc;
@@ -568,7 +660,20 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
                                                : 37.0 * n + (am ? 20.0 : 12.0) * c->nmasked;
   // from the second iteration of a cycle on, the stencil starts on k_gs's published sigma
   const unsigned* wait = (sc.post != nullptr && j >= 1) ? sc.post + (j - 1) : nullptr;
-  if (c) {
+  if (c && op->split) {
+    // split iteration: stencil (+ c_j), fork of the basis sweep h' = U^T w onto aux, the
+    // coarse solve here, join; then w -= A_p Z y, h = sigma h' - C y and the H column
+    coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, sc.sigma + j,
+                 nullptr, op->w, &st->active, wait, c->cmat + (long long)j * c->ldc);
+    if (!op->prof) DK_LOG_ERR(cudaStreamWaitEvent(op->stream, op->ev_join, 0));
+    {
+      ProfScope ps(op, PC_PROJECT,
+                   24.0 * n + pro_bytes + 8.0 * (double)nvec * (c->d + 1) + 8.0 * c->d);
+      launch_project(PJ_FIX, DK_LABELS, am, Aam, c->pro, c->y, op->w, op->w, V, op->vstride,
+                     nvec, op->n_pad, op->part, op->G, sc, j, &st->active, op->stream,
+                     op->prof);
+    }
+  } else if (c) {
     coarse_solve(op, c, ST_APPLY, pre, true, V + (long long)j * op->vstride, sc.sigma + j,
                  nullptr, op->w, &st->active, wait);
   } else {
@@ -577,7 +682,7 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
                    sc.sigma + j, nullptr, op->w, nullptr, &st->active, op->stream, wait,
                    sc.gpart_gs, sc.ng);
   }
-  {
+  if (!(c && op->split)) {
     ProfScope ps(op, PC_PROJECT,
                  c ? (24.0 + 8.0 * nvec) * n + pro_bytes : (16.0 + 8.0 * nvec) * n);
     launch_project(PJ_ITER, defl_kind(c), am, Aam, c ? c->pro : Prolong{}, c ? c->y : nullptr,
@@ -623,7 +728,8 @@ int read_state(dk_op* op) {
 }
 
 int build_graph(dk_op* op, dk_defl* c, int m) {
-  if (op->gexec && op->g_m == m && op->g_ctx == (c ? c->serial : 0ull)) return DK_OK;
+  const unsigned long long key = (c ? c->serial : 0ull) * 2 + (op->split ? 1 : 0);
+  if (op->gexec && op->g_m == m && op->g_ctx == key) return DK_OK;
   if (op->gexec) {
     cudaGraphExecDestroy(op->gexec);
     op->gexec = nullptr;
@@ -648,7 +754,47 @@ int build_graph(dk_op* op, dk_defl* c, int m) {
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   op->g_m = m;
-  op->g_ctx = c ? c->serial : 0ull;
+  op->g_ctx = key;
+  return DK_OK;
+}
+
+// Split iteration for label deflation with the symmetric 7-point stencil
+// (DK_SPLIT=1: on): the auxiliary stream and events, run_part2 and C, the Scal fields.
+int setup_split(dk_op* op, dk_defl* c, int m) {
+  Scal& sc = op->sc;
+  sc.split = 0;
+  op->split = false;
+  // opt-in (DK_SPLIT=1): measured slower than the fused projection at config 3 — the basis
+  // sweep and the tile GEMV cannot share the SMs
+  if (!c || c->dense || !getenv("DK_SPLIT")) return DK_OK;
+  if (!sym7_supported(make_dia(op, op->inv != nullptr))) return DK_OK;
+  if (!op->aux) {
+    DK_TRY(cudaStreamCreateWithFlags(&op->aux, cudaStreamNonBlocking));
+    DK_TRY(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
+    DK_TRY(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
+  }
+  if (!c->run_part2)
+    DK_TRY(cudaMallocAsync(&c->run_part2, (size_t)std::max<long long>(c->nruns, 1) * sizeof(double),
+                           op->stream));
+  if (c->cmat_rows < m + 1) {
+    if (c->cmat) DK_TRY(cudaFreeAsync(c->cmat, op->stream));
+    c->ldc = round_up(c->d, 32);
+    DK_TRY(cudaMallocAsync(&c->cmat, (size_t)(m + 1) * c->ldc * sizeof(double), op->stream));
+    c->cmat_rows = m + 1;
+    op->g_m = -1;  // a graph of this context refers to the old C
+  }
+  // the basis sweep leaves SM room for the coarse solve beside it
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    const char* e = getenv("DK_DOTS_CTAS_PER_SM");
+    per_sm = e ? std::max(1, atoi(e)) : 2;
+  }
+  op->G_dots = std::min(op->G, per_sm * num_sms());
+  sc.split = 1;
+  sc.cmat = c->cmat;
+  sc.ldc = c->ldc;
+  sc.dco = c->d;
+  op->split = true;
   return DK_OK;
 }
 
@@ -864,6 +1010,12 @@ int dk_op_destroy(dk_op* op) {
   cudaStreamSynchronize(op->stream);
   if (op->gexec) cudaGraphExecDestroy(op->gexec);
   for (auto e : op->ev_pool) cudaEventDestroy(e);
+  if (op->aux) {
+    cudaStreamSynchronize(op->aux);
+    cudaStreamDestroy(op->aux);
+  }
+  if (op->ev_fork) cudaEventDestroy(op->ev_fork);
+  if (op->ev_join) cudaEventDestroy(op->ev_join);
   // all device buffers of an operator come from the stream-ordered pool
   big_free(op->V_base, op->stream);
   void* bufs[] = {op->dia,     op->inv_base, op->w_base, op->x_base, op->b_base,
@@ -1204,6 +1356,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
         c->tg2.T = c->T1;  // pass 2 applies pass 1's tiles transposed
         err = upload_stream(c->Einv, d, c->ld, true, h1, c->tg1, s);
         if (!err) err = upload_stream(c->Einv, d, c->ld, false, h2, c->tg2, s);
+        if (!err) set_tile_window(c, (size_t)h1.nt * 1024 * sizeof(double));
         if (err) {
           big_free(Ework, s);
           return cleanup_fail((cudaError_t)err, "upload_stream");
@@ -1533,7 +1686,7 @@ int dk_defl_destroy(dk_defl* c) {
                   c->lab_base, c->tile_run_off, c->run_part, c->lab_run_ptr, c->run_slot,
                   c->piv,      c->xs_base,      c->s,        c->y,           c->qv_base,
                   c->rowpart,  c->colpart,      c->own_base, c->mask_base,   c->flab_base, c->fco_base, c->seg_ptr,
-                  c->seg_slot, c->long_ids};
+                  c->seg_slot, c->long_ids,    c->run_part2,    c->cmat};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);
   if (c->op) cudaStreamSynchronize(s);
@@ -1654,6 +1807,7 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
     DK_TRY(cudaMemcpyAsync(op->x, op->x0, (size_t)op->n_pad * sizeof(double),
                            cudaMemcpyDeviceToDevice, op->stream));
   }
+  if ((rc = setup_split(op, c, m))) return rc;
   launch_init_state(op->sc, tol, m, max_iters, min_iters, op->stream);
   op->launches += 1;
   const bool resume = ctl_in && ctl_in->resume;
@@ -1667,7 +1821,7 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   const bool run_cycles = !(resume && ctl_in->iterations >= max_iters);
   // The cycle becomes a CUDA graph from the second solve with the same (context, m): a
   // one-off solve (the public pdgmres path) launches eagerly and skips the instantiation.
-  const unsigned long long key = c ? c->serial : 0ull;
+  const unsigned long long key = (c ? c->serial : 0ull) * 2 + (op->split ? 1 : 0);
   const bool use_graph =
       !op->prof && ((op->gexec && op->g_m == m && op->g_ctx == key) ||
                     (op->seen_m == m && op->seen_ctx == key));
@@ -1686,7 +1840,8 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   // restart (stencil chain + projection), m x (stencil chain, projection, update [+ the
   // separate second pass]), cycle end, x update
   const int per_cycle_launches =
-      coarse_launches + 1 + m * (coarse_launches + (op->gs_fuse ? 2 : 4)) + 2;
+      coarse_launches + 1 + m * (coarse_launches + (op->gs_fuse ? 2 : 4) + (op->split ? 1 : 0)) +
+      2;
   long long guard_cycles = run_cycles ? (long long)max_iters + 2 : 0;
   if (max_cycles > 0 && guard_cycles > max_cycles) guard_cycles = max_cycles;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {

@@ -21,6 +21,7 @@ constexpr int kTile = 2048;          // cells per stencil/restriction tile (8 pe
 constexpr int kChunk = 2048;         // cells per Gram-Schmidt chunk (8 per thread)
 constexpr int kMaxDiag = DK_MAX_DIAGONALS;
 constexpr int kWarps = kThreads / 32;
+static_assert(kWarps % 4 == 0, "k_project's basis sweep gives each warp one quarter-chunk");
 
 // A(i, i + off[q]) = co[q][i + csh[q]].  Non-symmetric operators store every diagonal
 // (csh = 0).  A symmetric operator stores the centre and the positive diagonals only; the
@@ -87,6 +88,13 @@ struct Scal {
   double* gpart_gs;  // group partials of k_gs's norm (apart from the projection's)
   int ng;            // groups of the grouped reductions
   int m;
+  // split iteration: the basis sweep h' = U^T w runs concurrently with the
+  // coarse solve; h = sigma h' - C y with C's rows c_i = Z^T A_p^T v_i
+  int split;             // 0: off
+  double* hraw;          // [2(m+1)] reduced U^T w (0..m) and U^T u_j (m+1..2m+1)
+  const double* cmat;    // C, (m+1) rows of stride ldc, label order
+  long long ldc;
+  int dco;               // d (columns of C)
 };
 
 // volatile (L2) load of a flag or scalar another grid still running may write
@@ -117,6 +125,12 @@ inline bool& pdl_skip_next() {
   return f;
 }
 
+// set before a launch: an L2 access-policy window (persisting set-aside) for that launch
+inline const cudaAccessPolicyWindow*& access_window_next() {
+  static thread_local const cudaAccessPolicyWindow* w = nullptr;
+  return w;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, Args... args) {
@@ -125,12 +139,22 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (!pdl_skip_next()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (access_window_next() != nullptr) {
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow = *access_window_next();
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_skip_next() ? 0 : 1;
+  cfg.numAttrs = na;
   pdl_skip_next() = false;
+  access_window_next() = nullptr;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) launch_error() = e;
   return e;
@@ -183,7 +207,7 @@ __device__ __forceinline__ void tl_mark_warp(unsigned kind, unsigned phase) {
 #define DK_TL_SETTER(fn)
 #endif
 enum TlKind { TL_STENCIL = 1, TL_RESTRICT = 2, TL_TG1 = 3, TL_TG2 = 4, TL_PROJECT = 5, TL_GS = 6,
-              TL_TG1W = 7, TL_TG2W = 8 };
+              TL_TG1W = 7, TL_TG2W = 8, TL_DOTS = 9 };
 
 // ---- small device helpers -------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
@@ -211,6 +235,12 @@ __device__ __forceinline__ unsigned long long l2_evict_first() {
 __device__ __forceinline__ unsigned long long l2_evict_last() {
   unsigned long long p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// no priority change: the launch's access-policy window (persisting set-aside) applies
+__device__ __forceinline__ unsigned long long l2_evict_unchanged() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ double2 ld2_stream(const double* ptr, unsigned long long pol) {
@@ -286,6 +316,31 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsign
 
 __device__ __forceinline__ void st2(double* p, double2 v) {
   *reinterpret_cast<double2*>(p) = v;
+}
+// per-iteration vectors (w, u) with an explicit L2 priority (DK_VEC_EF builds: evict-first)
+__device__ __forceinline__ void st2_vec(double* p, double2 v) {
+#ifdef DK_VEC_EF
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x),
+               "d"(v.y), "l"(pol)
+               : "memory");
+#else
+  st2(p, v);
+#endif
+}
+__device__ __forceinline__ double2 ld2_vec(const double* p) {
+#ifdef DK_VEC_EF
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldcg(reinterpret_cast<const double2*>(p));
+#endif
 }
 
 // Every block calls this after writing its partials; returns true in exactly one block

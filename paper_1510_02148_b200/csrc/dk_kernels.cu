@@ -328,8 +328,8 @@ __device__ __forceinline__ void sym7_load(Sym7Pair& q, const Dia& A, const doubl
   q.uxm = ld2_stream(A.co[5] + i - nx, pol);
   q.uz = ld2_stream(A.co[6] + i, pol);
   q.uzm = ld2_stream(A.co[6] + i - nz, pol);
-  q.vm = ld2(v + i - nz);
-  q.vp = ld2(v + i + nz);
+  q.vm = ld2_vec(v + i - nz);
+  q.vp = ld2_vec(v + i + nz);
   if (PRE) {
     q.im = ld2_stream(A.inv + i - nz, pol);
     q.ip = ld2_stream(A.inv + i + nz, pol);
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
   const unsigned long long pol = l2_evict_first();
   for (int e = threadIdx.x; e < (kTile + 2 * H) / 2; e += kThreads) {
     const long long i = base - H + 2 * e;
-    double2 x = ld2(v + i);
+    double2 x = ld2_vec(v + i);
     if (has_scale) {
       x.x = __dmul_rn(x.x, sc);
       x.y = __dmul_rn(x.y, sc);
@@ -436,9 +436,120 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
   if (WRITE)
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      st2(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
+      st2_vec(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
   if (RESTRICT)
     stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  DK_TL(TL_STENCIL, 3);
+  if (wait != nullptr) pdl_wait();
+  DK_TL(TL_STENCIL, 4);
+}
+
+// The 7-point sums of a cell pair (i, i+1) in ascending-offset order (sym7_apply's), with the
+// in-plane inputs from P(o) (o relative to cell i) and the z-plane inputs given.
+template <class F>
+__device__ __forceinline__ double2 sym7_pair(const Sym7Pair& q, F P, long long nx, double zm0,
+                                             double zm1, double zp0, double zp1) {
+  double r0 = __dmul_rn(q.uzm.x, zm0);
+  r0 = __dadd_rn(r0, __dmul_rn(q.uxm.x, P(-nx)));
+  r0 = __dadd_rn(r0, __dmul_rn(q.u1m.y, P(-1)));
+  r0 = __dadd_rn(r0, __dmul_rn(q.c.x, P(0)));
+  r0 = __dadd_rn(r0, __dmul_rn(q.u1.x, P(1)));
+  r0 = __dadd_rn(r0, __dmul_rn(q.ux.x, P(nx)));
+  r0 = __dadd_rn(r0, __dmul_rn(q.uz.x, zp0));
+  double r1 = __dmul_rn(q.uzm.y, zm1);
+  r1 = __dadd_rn(r1, __dmul_rn(q.uxm.y, P(1 - nx)));
+  r1 = __dadd_rn(r1, __dmul_rn(q.u1.x, P(0)));
+  r1 = __dadd_rn(r1, __dmul_rn(q.c.y, P(1)));
+  r1 = __dadd_rn(r1, __dmul_rn(q.u1.y, P(2)));
+  r1 = __dadd_rn(r1, __dmul_rn(q.ux.y, P(1 + nx)));
+  r1 = __dadd_rn(r1, __dmul_rn(q.uz.y, zp1));
+  return make_double2(r0, r1);
+}
+
+// Split-iteration stencil: w = A M^-1 (sigma v) exactly as k_stencil_sym7
+// (same products, same order: bitwise equal), its run sums, and the run sums of
+// a = A_p^T (sigma v) = A (sigma v) (times M^-1 for A_p = A M^-1; A symmetric), from which
+// k_restrict_final forms the row c_j = Z^T A_p^T v_j of C.  sigma v and M^-1 are staged
+// separately (the products are formed on use); the staging area is reused for the two
+// segmented restrictions.
+template <bool PRE>
+__global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7_split(
+    Dia A, const double* __restrict__ v, const double* __restrict__ scale,
+    double* __restrict__ out, const int* __restrict__ lab, const int* __restrict__ tile_run_off,
+    const int* __restrict__ run_slot, double* __restrict__ run_part,
+    double* __restrict__ run_part2, int am, const int* __restrict__ gate, int H,
+    const unsigned* wait, const double* gsig, int ng) {
+  DK_TL(TL_STENCIL, 0);
+  if (wait != nullptr) {
+    const long long b0 = (long long)blockIdx.x * kTile;
+    const int t = threadIdx.x;
+    if (t < 4) l2_prefetch(A.co[3 + t] + b0, kTile * 8);
+    if (PRE && t == 4) l2_prefetch(A.inv + b0, kTile * 8);
+    if (t == 5) l2_prefetch(lab + b0, kTile * 4);
+    if (!early_start(wait, gate, (unsigned)ng)) return;
+  } else {
+    pdl_wait();
+    if (gate != nullptr && *gate == 0) return;
+  }
+  DK_TL(TL_STENCIL, 1);
+  pdl_trigger();
+  extern __shared__ __align__(16) double sp[];  // [s1: sigma v | s2: M^-1], each H|kTile|H
+  __shared__ double wsum[kWarps];
+  const int L = kTile + 2 * H;
+  double* s1 = sp;
+  double* s2 = sp + L;
+  const long long base = (long long)blockIdx.x * kTile;
+  const long long nx = A.off[5], nz = A.off[6];
+  const bool has_scale = scale != nullptr;
+  const double sc = !has_scale ? 1.0 : wait != nullptr ? early_sigma(gsig, ng) : __ldcg(scale);
+  const unsigned long long pol = l2_evict_first();
+  for (int e = threadIdx.x; e < L / 2; e += kThreads) {
+    const long long i = base - H + 2 * e;
+    double2 x = ld2(v + i);
+    if (has_scale) {
+      x.x = __dmul_rn(x.x, sc);
+      x.y = __dmul_rn(x.y, sc);
+    }
+    reinterpret_cast<double2*>(s1)[e] = x;
+    if (PRE) reinterpret_cast<double2*>(s2)[e] = ld2_stream(A.inv + i, pol);
+  }
+  int2 lb[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) lb[k] = ldi2_stream(lab + base + 2 * threadIdx.x + 512 * k, pol);
+  __syncthreads();
+  double rr[8], aa[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = H + 2 * threadIdx.x + 512 * k;
+    Sym7Pair q;
+    sym7_load<PRE>(q, A, v, base + 2 * threadIdx.x + 512 * k, nx, nz, pol);
+    const double vm0 = has_scale ? __dmul_rn(q.vm.x, sc) : q.vm.x;
+    const double vm1 = has_scale ? __dmul_rn(q.vm.y, sc) : q.vm.y;
+    const double vp0 = has_scale ? __dmul_rn(q.vp.x, sc) : q.vp.x;
+    const double vp1 = has_scale ? __dmul_rn(q.vp.y, sc) : q.vp.y;
+    const double2 r = sym7_pair(
+        q, [&](long long o) { return PRE ? __dmul_rn(s1[c + o], s2[c + o]) : s1[c + o]; }, nx,
+        PRE ? __dmul_rn(vm0, q.im.x) : vm0, PRE ? __dmul_rn(vm1, q.im.y) : vm1,
+        PRE ? __dmul_rn(vp0, q.ip.x) : vp0, PRE ? __dmul_rn(vp1, q.ip.y) : vp1);
+    double2 a = sym7_pair(q, [&](long long o) { return s1[c + o]; }, nx, vm0, vm1, vp0, vp1);
+    if (PRE && am) {
+      a.x = __dmul_rn(a.x, s2[c]);
+      a.y = __dmul_rn(a.y, s2[c + 1]);
+    }
+    rr[2 * k] = r.x;
+    rr[2 * k + 1] = r.y;
+    aa[2 * k] = a.x;
+    aa[2 * k + 1] = a.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    st2(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
+  __syncthreads();  // the staging area becomes the restriction scratch
+  double* sw = sp;
+  int* sl = reinterpret_cast<int*>(sp + kTilePad);
+  stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  __syncthreads();
+  stencil_restrict_tail(aa, lb, sw, sl, wsum, tile_run_off, run_slot, run_part2);
   DK_TL(TL_STENCIL, 3);
   if (wait != nullptr) pdl_wait();
   DK_TL(TL_STENCIL, 4);
@@ -455,6 +566,30 @@ static int sym7_halo(const Dia& A) {
   for (int q = 3; q < 7; ++q)
     if (A.csh[q] != 0) return 0;
   return (int)((nx + 2 + 31) / 32 * 32);
+}
+
+bool sym7_supported(const Dia& A) { return sym7_halo(A) > 0; }
+
+void launch_stencil_split(bool pre, bool am, const Dia& A, long long n_pad, const double* v,
+                          const double* scale, double* out, const RunMap& rm, double* run_part2,
+                          const int* gate, cudaStream_t s, const unsigned* wait,
+                          const double* gsig, int ng) {
+  const int H = sym7_halo(A);
+  const unsigned grid = (unsigned)(n_pad / kTile);
+  size_t smem = (size_t)2 * (kTile + 2 * H) * sizeof(double);
+  const size_t scratch = (size_t)kTilePad * (sizeof(double) + sizeof(int));
+  if (smem < scratch) smem = scratch;
+  if (pre) {
+    smem_optin((const void*)k_stencil_sym7_split<true>, smem);
+    launch_pdl(k_stencil_sym7_split<true>, dim3(grid), dim3(kThreads), smem, s, A, v, scale, out,
+               rm.lab, rm.tile_run_off, rm.run_slot, rm.run_part, run_part2, am ? 1 : 0, gate,
+               H, wait, gsig, ng);
+  } else {
+    smem_optin((const void*)k_stencil_sym7_split<false>, smem);
+    launch_pdl(k_stencil_sym7_split<false>, dim3(grid), dim3(kThreads), smem, s, A, v, scale,
+               out, rm.lab, rm.tile_run_off, rm.run_slot, rm.run_part, run_part2, am ? 1 : 0,
+               gate, H, wait, gsig, ng);
+  }
 }
 
 template <bool PRE, bool R, bool W>
@@ -538,7 +673,9 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
                                                              int nlong, int short_blocks,
                                                              double* __restrict__ s,
                                                              const int* __restrict__ s_pos,
-                                                             const int* __restrict__ gate) {
+                                                             const int* __restrict__ gate,
+                                                             const double* __restrict__ rp2,
+                                                             double* __restrict__ out2) {
   DK_TL(TL_RESTRICT, 0);
   pdl_trigger();  // the tile GEMV's prologue (tile prefetch) overlaps this grid
   pdl_wait();
@@ -558,6 +695,15 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
     for (int k = 0; k < kShortRuns; ++k)
       if (k < len) acc += v[k];
     s[s_pos ? s_pos[L] : L] = acc;
+    if (out2 != nullptr) {
+#pragma unroll
+      for (int k = 0; k < kShortRuns; ++k) v[k] = k < len ? __ldcg(rp2 + lo + k) : 0.0;
+      double a2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < kShortRuns; ++k)
+        if (k < len) a2 += v[k];
+      out2[L] = a2;
+    }
     DK_TL(TL_RESTRICT, 4);
     return;
   }
@@ -566,7 +712,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
   const int lane = threadIdx.x & 31;
   if (wl >= nlong) return;
   const int L = long_ids[wl];
-  double acc = 0.0;
+  double acc = 0.0, a2 = 0.0;
   const int lo = ptr[L], hi = ptr[L + 1];
   for (int k0 = lo + lane; k0 < hi; k0 += 32 * kLongBatch) {
     double v[kLongBatch];
@@ -576,19 +722,32 @@ __global__ void __launch_bounds__(kThreads) k_restrict_final(const double* __res
 #pragma unroll
     for (int i = 0; i < kLongBatch; ++i)
       if (k0 + 32 * i < hi) acc += v[i];
+    if (out2 != nullptr) {
+#pragma unroll
+      for (int i = 0; i < kLongBatch; ++i)
+        v[i] = k0 + 32 * i < hi ? __ldcg(rp2 + k0 + 32 * i) : 0.0;
+#pragma unroll
+      for (int i = 0; i < kLongBatch; ++i)
+        if (k0 + 32 * i < hi) a2 += v[i];
+    }
   }
   acc = warp_sum(acc);
   if (lane == 0) s[s_pos ? s_pos[L] : L] = acc;
+  if (out2 != nullptr) {
+    a2 = warp_sum(a2);
+    if (lane == 0) out2[L] = a2;
+  }
   DK_TL(TL_RESTRICT, 4);
 }
 
-void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s) {
+void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s,
+                           const double* run_part2, double* out2) {
   if (rm.d <= 0) return;
   const int short_blocks = (rm.d + kThreads - 1) / kThreads;
   const unsigned grid =
       (unsigned)(short_blocks + ((long long)rm.nlong * 32 + kThreads - 1) / kThreads);
   launch_pdl(k_restrict_final, dim3(grid), dim3(kThreads), 0, s, rm.run_part, rm.lab_run_ptr,
-             rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, rm.s_pos, gate);
+             rm.d, rm.long_ids, rm.nlong, short_blocks, s_out, rm.s_pos, gate, run_part2, out2);
 }
 
 // ======================================================================================
@@ -850,6 +1009,14 @@ __device__ __forceinline__ double reduce8(double (&v)[8], int lane) {
 // red[0..2 nvec]: h[nvec], |corr|[nvec] and, for nvec <= kStageGram, G[nvec][nvec] (larger
 // cycles read G from global memory).
 constexpr int kStageGram = 96;
+// h_i of the split iteration: sigma_i (U^T w)_i - (C y)_i, the arithmetic k_gs's early start
+// repeats bitwise
+__device__ __forceinline__ double split_h(const Scal& sc, int i, double cy) {
+  return __dsub_rn(__dmul_rn(__ldcg(sc.hraw + i), __ldcg(sc.sigma + i)), cy);
+}
+
+// SPLIT: red[0..nvec) = C y, red[nvec] = ||w||^2, U^T w and U^T u_j in sc.hraw
+template <bool SPLIT = false>
 __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
   State* st = sc.st;
   const int m = sc.m;
@@ -860,11 +1027,13 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
   double* sh_c = sh_h + nvec;
   double* sh_g = sh_c + nvec;
   for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    const double h = red[v] * sc.sigma[v];  // h_i = V_i . w  (krylov.py:164-165)
+    // h_i = V_i . w  (krylov.py:164-165)
+    const double h = SPLIT ? split_h(sc, v, red[v]) : red[v] * sc.sigma[v];
     Hc[v] = h;
     sh_h[v] = h;
     sc.coef[v] = h * sc.sigma[v];
-    const double g = red[nvec + v] * sc.sigma[v] * sj;  // V_i . V_j
+    // V_i . V_j
+    const double g = (SPLIT ? sc.hraw[sc.m + 1 + v] : red[nvec + v]) * sc.sigma[v] * sj;
     sc.Gm[(size_t)j * (m + 1) + v] = g;
     if (stage) {
       sh_g[v * nvec + (nvec - 1)] = g;
@@ -887,7 +1056,7 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    st->wnorm0 = sqrt(red[2 * nvec]);  // krylov.py:162
+    st->wnorm0 = sqrt(red[SPLIT ? nvec : 2 * nvec]);  // krylov.py:162
     double mx = 0.0;
     for (int i = 0; i < nvec; ++i) mx = fmax(mx, sh_c[i]);
     if (mx > 1e-8 * fmax(st->wnorm0, 1e-300)) {  // krylov.py:168
@@ -907,22 +1076,32 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
                                                       long long vstride, int nvec, long long n_pad,
                                                       double* __restrict__ part, int G, Scal sc,
                                                       int j, const int* __restrict__ gate) {
-  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 0);
+  constexpr bool DOTS = MODE == PJ_ITER || MODE == PJ_REDOTS || MODE == PJ_DOTS;  // V sweep
+  constexpr bool GRAM = MODE == PJ_ITER || MODE == PJ_DOTS;  // also V^T v_j
+  constexpr bool NORM = MODE == PJ_ITER || MODE == PJ_RESTART || MODE == PJ_FIX;
+  constexpr bool CTRL = MODE == PJ_ITER || MODE == PJ_FIX;  // the iteration's control block
+  if (CTRL) DK_TL(TL_PROJECT, 0);
+  if (MODE == PJ_DOTS) DK_TL(TL_DOTS, 0);
   pdl_wait();
-  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 1);
+  if (CTRL) DK_TL(TL_PROJECT, 1);
+  if (MODE == PJ_DOTS) DK_TL(TL_DOTS, 1);
   // the stencil of this iteration has completed: re-arm its early-start flag
-  if (MODE == PJ_ITER && sc.post != nullptr && j >= 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (CTRL && sc.post != nullptr && j >= 1 && blockIdx.x == 0 && threadIdx.x == 0) {
     sc.post[j - 1] = 0u;            // consumed by this iteration's stencil
     sc.post[sc.m + 1 + j - 1] = 0u;  // consumed by the previous k_gs (done: the stencil waited)
   }
   if (*gate == 0) return;
   extern __shared__ double red[];  // [nq][kWarps]
-  __shared__ __align__(16) double s_w[(MODE == PJ_ITER || MODE == PJ_REDOTS) ? kChunk : 2];
-  __shared__ __align__(16) double s_vj[MODE == PJ_ITER ? kChunk : 2];
+  __shared__ __align__(16) double s_w[DOTS ? kChunk : 2];
+  __shared__ __align__(16) double s_vj[GRAM ? kChunk : 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // quantities: ITER: h[nvec], g[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec]
-  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
-  const int nslot = (MODE == PJ_ITER) ? 2 * nvec : 0;
+  // quantities: ITER: h[nvec], g[nvec], |w|^2 ; RESTART: |w|^2 ; REDOTS: corr[nvec] ;
+  // DOTS: h'[nvec], g[nvec] ; FIX: (C y)[nvec], |w|^2
+  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1
+                 : (MODE == PJ_DOTS) ? 2 * nvec
+                 : (MODE == PJ_REDOTS) ? nvec
+                 : (MODE == PJ_FIX) ? nvec + 1 : 1;
+  const int nslot = (MODE == PJ_ITER) ? 2 * nvec : (MODE == PJ_FIX) ? nvec : 0;
   for (int q = threadIdx.x; q < nq * kWarps; q += blockDim.x) red[q] = 0.0;
   __syncthreads();
   const long long nchunks = n_pad / kChunk;
@@ -936,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const long long i = cb + 512 * k;
-      xin[k] = (MODE == PJ_REDOTS) ? ld2cg(w_in + i) : ld2(w_in + i);
+      xin[k] = (MODE == PJ_REDOTS) ? ld2cg(w_in + i) : ld2_vec(w_in + i);
     }
     if (DEFL == DK_LABELS) {
       const unsigned long long cpol = l2_evict_first();
@@ -975,28 +1154,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
       }
       w[2 * k] = x.x;
       w[2 * k + 1] = x.y;
-      if (MODE != PJ_REDOTS && (DEFL != DK_NONE || w_out != w_in)) st2(w_out + i, x);
+      if (MODE != PJ_REDOTS && (DEFL != DK_NONE || w_out != w_in)) st2_vec(w_out + i, x);
     }
-    if (MODE == PJ_ITER && ch == blockIdx.x) DK_TL(TL_PROJECT, 2);
-    if (MODE == PJ_ITER || MODE == PJ_RESTART) {
+    if (CTRL && ch == blockIdx.x) DK_TL(TL_PROJECT, 2);
+    if (NORM) {
       double nrm = 0.0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) nrm = fma(w[e], w[e], nrm);
       nrm = warp_sum(nrm);
       if (lane == 0) red[nslot * kWarps + warp] += nrm;
     }
-    if (MODE == PJ_ITER || MODE == PJ_REDOTS) {
+    if (DOTS) {
       // Stage w (and v_j) of the chunk in shared memory; the warps then stream the basis as
       // (vector, quarter-chunk) items: 8 x 16 B loads in flight per lane and one warp
       // reduction per 4 KB of V, instead of one per 128 B.  Item (v, q) goes to warp
       // (4v + q) % 8 and its partial to that warp's slot: fixed order, deterministic.  Each
-      // V_i load serves both dots, V_i . w and the Gram entry V_i . v_j.
+      // V_i load serves both dots, V_i . w and the Gram entry V_i . v_j.  (Register-resident
+      // quarters of w and v_j instead of the staging spill at 64 registers: measured slower.)
       double2* sw2 = reinterpret_cast<double2*>(s_w);
       double2* sv2 = reinterpret_cast<double2*>(s_vj);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         sw2[threadIdx.x + 256 * k] = make_double2(w[2 * k], w[2 * k + 1]);
-        if (MODE == PJ_ITER) sv2[threadIdx.x + 256 * k] = ld2(Vj + cb + 512 * k);
+        if (GRAM) sv2[threadIdx.x + 256 * k] = ld2_vec(Vj + cb + 512 * k);
       }
       __syncthreads();
       const long long c0 = ch * kChunk;
@@ -1014,23 +1194,35 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
           const double2 ww = sw2[e];
           ah = fma(p[i].x, ww.x, ah);
           ah = fma(p[i].y, ww.y, ah);
-          if (MODE == PJ_ITER) {
+          if (GRAM) {
             const double2 gg = sv2[e];
             ag = fma(p[i].x, gg.x, ag);
             ag = fma(p[i].y, gg.y, ag);
           }
         }
         ah = warp_sum(ah);
-        if (MODE == PJ_ITER) ag = warp_sum(ag);
+        if (GRAM) ag = warp_sum(ag);
         if (lane == 0) {
           red[v * kWarps + warp] += ah;
-          if (MODE == PJ_ITER) red[(nvec + v) * kWarps + warp] += ag;
+          if (GRAM) red[(nvec + v) * kWarps + warp] += ag;
         }
       }
       __syncthreads();  // the next chunk reuses s_w / s_vj
     }
   }
-  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 3);
+  if (MODE == PJ_FIX) {
+    // this block's slice of the coarse columns: (C y)_i over [c0, c1), serial in k
+    const long long c0 = (long long)blockIdx.x * sc.dco / gridDim.x;
+    const long long c1 = (long long)(blockIdx.x + 1) * sc.dco / gridDim.x;
+    if ((int)threadIdx.x < nvec) {
+      const double* Cr = sc.cmat + (long long)threadIdx.x * sc.ldc;
+      double acc = 0.0;
+      for (long long k = c0; k < c1; ++k) acc = fma(__ldcg(Cr + k), __ldcg(yc + k), acc);
+      red[threadIdx.x * kWarps] += acc;
+    }
+  }
+  if (CTRL) DK_TL(TL_PROJECT, 3);
+  if (MODE == PJ_DOTS) DK_TL(TL_DOTS, 3);
   pdl_trigger();
   if (MODE == PJ_PLAIN) return;
   __syncthreads();
@@ -1040,9 +1232,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
     part[(size_t)q * G + blockIdx.x] = s;
   }
   if (!reduce_grouped(part, nq, G, sc.gticket, sc.gpart, red,
-                      (MODE == PJ_ITER && sc.post != nullptr) ? sc.post + (sc.m + 1) + j
-                                                              : nullptr)) {
-    if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 4);
+                      (CTRL && sc.post != nullptr) ? sc.post + (sc.m + 1) + j : nullptr)) {
+    if (CTRL) DK_TL(TL_PROJECT, 4);
+    if (MODE == PJ_DOTS) DK_TL(TL_DOTS, 4);
+    return;
+  }
+  if (MODE == PJ_DOTS) {  // U^T w and U^T u_j for the split iteration's control block
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      sc.hraw[v] = red[v];
+      sc.hraw[sc.m + 1 + v] = red[nvec + v];
+    }
+    DK_TL(TL_DOTS, 5);
     return;
   }
   State* st = sc.st;
@@ -1069,24 +1269,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
     return;
   }
   (void)st;
-  iter_finish(sc, j, nvec, red);
-  if (MODE == PJ_ITER) DK_TL(TL_PROJECT, 5);
+  iter_finish<MODE == PJ_FIX>(sc, j, nvec, red);
+  if (CTRL) DK_TL(TL_PROJECT, 5);
 }
 
 template <int MODE, int DEFL, bool AM>
 static void project_t(const Dia& A, const Prolong& lab, const double* yc, const double* w_in,
                       double* w_out, const double* V, long long vstride, int nvec,
                       long long n_pad, double* part, int G, const Scal& sc, int j,
-                      const int* gate, cudaStream_t s) {
-  const int nq = (MODE == PJ_ITER) ? 2 * nvec + 1 : (MODE == PJ_REDOTS ? nvec : 1);
+                      const int* gate, cudaStream_t s, bool pdl = true) {
+  const int nq = (MODE == PJ_ITER || MODE == PJ_DOTS) ? 2 * nvec + 1
+                 : (MODE == PJ_REDOTS) ? nvec : (MODE == PJ_FIX) ? nvec + 1 : 1;
   int slots = nq * kWarps > 3 * (sc.m + 1) ? nq * kWarps : 3 * (sc.m + 1);
-  // PJ_ITER re-orthogonalisation test scratch (iter_finish)
+  // PJ_ITER / PJ_FIX re-orthogonalisation test scratch (iter_finish)
   const int tail = 4 * nvec + 1 + (nvec <= kStageGram ? nvec * nvec : 0);
-  if (MODE == PJ_ITER && tail > slots) slots = tail;
+  if ((MODE == PJ_ITER || MODE == PJ_FIX) && tail > slots) slots = tail;
   if (nq + 260 > slots) slots = nq + 260;  // reduce_grouped scratch
   const size_t smem = (size_t)slots * sizeof(double);
   // one per instantiation and device: dynamic + 32 KB static > 48 KB default
   smem_optin((const void*)k_project<MODE, DEFL, AM>, 160 * 1024);
+  if (!pdl) pdl_skip_next() = true;
   launch_pdl(k_project<MODE, DEFL, AM>, dim3(G), dim3(kThreads), smem, s, A, lab, yc, w_in,
              w_out, V, vstride, nvec, n_pad, part, G, sc, j, gate);
 }
@@ -1113,7 +1315,21 @@ static void project_m(int defl, bool am, const Dia& A, const Prolong& lab, const
 void launch_project(int mode, int defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
-                    const int* gate, cudaStream_t s) {
+                    const int* gate, cudaStream_t s, bool pdl) {
+  if (mode == PJ_DOTS) {
+    project_t<PJ_DOTS, DK_NONE, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G,
+                                       sc, j, gate, s, pdl);
+    return;
+  }
+  if (mode == PJ_FIX) {
+    if (am)
+      project_t<PJ_FIX, DK_LABELS, true>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part,
+                                         G, sc, j, gate, s, pdl);
+    else
+      project_t<PJ_FIX, DK_LABELS, false>(A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part,
+                                          G, sc, j, gate, s, pdl);
+    return;
+  }
   if (mode == PJ_ITER)
     project_m<PJ_ITER>(defl, am, A, lab, yc, w_in, w_out, V, vstride, nvec, n_pad, part, G, sc, j,
                        gate, s);
@@ -1332,7 +1548,9 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     __syncthreads();
     for (int q = threadIdx.x; q < nvec; q += blockDim.x) {
       const double sv = __ldcg(sc.sigma + q);
-      cf[q] = (grouped_total(gp, q, sc.ng, false) * sv) * sv;
+      const double t = grouped_total(gp, q, sc.ng, false);
+      // iter_finish's h_i (split: sigma_i h'_i - (C y)_i), times sigma_i
+      cf[q] = (sc.split ? split_h(sc, q, t) : t * sv) * sv;
     }
     __syncthreads();
   } else {
@@ -1347,7 +1565,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     double u[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const double2 x = REORTH ? ld2cg(w_in + cb + 512 * k) : ld2(w_in + cb + 512 * k);
+      const double2 x = REORTH ? ld2cg(w_in + cb + 512 * k) : ld2_vec(w_in + cb + 512 * k);
       u[2 * k] = x.x;
       u[2 * k + 1] = x.y;
     }
@@ -1365,7 +1583,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
     double nrm = 0.0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      st2(u_out + cb + 512 * k, make_double2(u[2 * k], u[2 * k + 1]));
+      st2_vec(u_out + cb + 512 * k, make_double2(u[2 * k], u[2 * k + 1]));
       nrm = fma(u[2 * k], u[2 * k], nrm);
       nrm = fma(u[2 * k + 1], u[2 * k + 1], nrm);
     }

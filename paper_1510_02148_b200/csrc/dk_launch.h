@@ -48,8 +48,18 @@ void launch_stencil(int mode, bool pre, bool write, const Dia& A, long long n_pa
                     const double* scale, const double* b, double* out, const RunMap* rm,
                     const int* gate, cudaStream_t s, const unsigned* wait = nullptr,
                     const double* gsig = nullptr, int ng = 0);
-// s[s_pos[L]] (s[L] without s_pos) = sum of run partials of label L, fixed order.
-void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s);
+// Split-iteration stencil (symmetric 7-point operators only; sym7_supported): as
+// launch_stencil(ST_APPLY, ..., write, rm) and also the run sums of a = A_p^T v (A v, times
+// M^-1 when am) into run_part2.  Returns false when the operator is not supported.
+bool sym7_supported(const Dia& A);
+void launch_stencil_split(bool pre, bool am, const Dia& A, long long n_pad, const double* v,
+                          const double* scale, double* out, const RunMap& rm, double* run_part2,
+                          const int* gate, cudaStream_t s, const unsigned* wait,
+                          const double* gsig, int ng);
+// s[s_pos[L]] (s[L] without s_pos) = sum of run partials of label L, fixed order; with
+// run_part2, also out2[L] = the sums of run_part2 (label order).
+void launch_restrict_final(const RunMap& rm, double* s_out, const int* gate, cudaStream_t s,
+                           const double* run_part2 = nullptr, double* out2 = nullptr);
 // y = M x, M d x d row-major with leading dimension ld.
 void launch_gemv(const double* M, int d, int ld, const double* x, double* y, const int* gate,
                  cudaStream_t s);
@@ -71,14 +81,17 @@ void launch_prolong_setup(bool am, const Dia& A, const int* lab, long long n_pad
                           int2* flab, double2* fco, unsigned char* mask,
                           unsigned long long* nmasked, cudaStream_t s);
 
-enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3 };
+enum ProjectMode { PJ_ITER = 0, PJ_RESTART = 1, PJ_PLAIN = 2, PJ_REDOTS = 3,
+                   // split iteration: DOTS = h' = U^T w and the Gram column (no prolongation,
+                   // no control); FIX = w -= A_p Z y, ||w||^2, C y slices, then the H column
+                   PJ_DOTS = 4, PJ_FIX = 5 };
 // w_out = w_in - A_p Z y (defl) ; ITER: dots h = V^T w, ||w_out||^2
 // -> H col j + re-orthogonalisation test; RESTART: ||w_out||^2 -> restart test;
 // REDOTS: corr = V^T u for the second Gram-Schmidt pass.  G = grid width (fixed per op).
 void launch_project(int mode, int defl, bool am, const Dia& A, const Prolong& lab, const double* yc,
                     const double* w_in, double* w_out, const double* V, long long vstride,
                     int nvec, long long n_pad, double* part, int G, const Scal& sc, int j,
-                    const int* gate, cudaStream_t s);
+                    const int* gate, cudaStream_t s, bool pdl = true);
 // dense deflation basis (rows of stride zs): s_k = Z_k . v for k < nz; y[k * ystride] = s_k,
 // or y = Einv s (nz x nz, ld) when Einv != nullptr.  ticket: a zeroed device counter.
 void launch_zdots(const double* v, const double* Z, long long zs, int nz, long long n_pad,
@@ -189,6 +202,10 @@ struct TileGemv {
   long long nt = 0;
   int nw = 0;                  // warps holding tiles (min(kTgGrid * warps per CTA, nt))
   int nrows = 0;
+  // L2 persisting window over the tile store (win_bytes == 0: none; the tiles then load with
+  // an evict-last hint)
+  void* win_base = nullptr;
+  size_t win_bytes = 0;
 };
 struct TileGemvHost {
   long long nt = 0;

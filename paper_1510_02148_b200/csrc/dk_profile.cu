@@ -190,9 +190,9 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   const long long Wn = g.nw;
   const long long w = (long long)blockIdx.x * KW + wl;
   const long long t0 = w < Wn ? w * g.nt / Wn : g.nt, t1 = w < Wn ? (w + 1) * g.nt / Wn : g.nt;
-  // W is re-read by both passes of every iteration: evict-last keeps it L2-resident across
-  // the basis sweeps (evict-first) in between
-  const unsigned long long pol = l2_evict_last();
+  // W is re-read by both passes of every iteration: kept L2-resident across the basis sweeps
+  // (evict-first) in between by the persisting window of the launch, else by evict-last
+  const unsigned long long pol = g.win_bytes ? l2_evict_unchanged() : l2_evict_last();
   auto tile_ptr = [&](long long t) {
     const long long q = TRANS ? (long long)__ldg(g.tid + t) : t;
     return g.T + q * (kPT * kPT);
@@ -716,8 +716,8 @@ int tgemv_cfg() {
   static int c = -1;
   if (c < 0) {
     const char* e = getenv("DK_TG_CFG");
-    c = e ? atoi(e) : 0;
-    if (c < 0 || c > 5) c = 0;
+    c = e ? atoi(e) : 2;
+    if (c < 0 || c > 5) c = 2;
   }
   return c;
 }
@@ -731,6 +731,15 @@ static void launch_tg(const TileGemv& g, const double* x, double* y, const int* 
                       const int* gate, cudaStream_t s) {
   const size_t smem = (size_t)KW * KS * kPTileBytes;
   const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
+  cudaAccessPolicyWindow win{};
+  if (g.win_bytes) {
+    win.base_ptr = g.win_base;
+    win.num_bytes = g.win_bytes;
+    win.hitRatio = 1.0f;
+    win.hitProp = cudaAccessPropertyPersisting;
+    win.missProp = cudaAccessPropertyStreaming;
+    access_window_next() = &win;
+  }
   if (g.trans) {
     smem_optin((const void*)k_tgemv<KW, KS, true>, smem);
     launch_pdl(k_tgemv<KW, KS, true>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d,
@@ -746,11 +755,11 @@ void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scat
                   const int* gate, cudaStream_t s) {
   switch (tgemv_cfg()) {
     case 1: launch_tg<16, 1>(g, x, y, scatter, d, gate, s); break;
-    case 2: launch_tg<8, 3>(g, x, y, scatter, d, gate, s); break;
     case 3: launch_tg<4, 6>(g, x, y, scatter, d, gate, s); break;
     case 4: launch_tg<8, 2>(g, x, y, scatter, d, gate, s); break;
     case 5: launch_tg<6, 2>(g, x, y, scatter, d, gate, s); break;
-    default: launch_tg<12, 2>(g, x, y, scatter, d, gate, s); break;
+    case 0: launch_tg<12, 2>(g, x, y, scatter, d, gate, s); break;
+    default: launch_tg<8, 3>(g, x, y, scatter, d, gate, s); break;
   }
 }
 

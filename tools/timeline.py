@@ -21,7 +21,8 @@ import torch  # noqa: E402
 import paper_1510_02148_b200 as dk  # noqa: E402
 from paper_1510_02148_b200 import _lib, configs  # noqa: E402
 
-KIND = {1: "stencil", 2: "restrict", 3: "tgemv1", 4: "tgemv2", 5: "project", 6: "gs"}
+KIND = {1: "stencil", 2: "restrict", 3: "tgemv1", 4: "tgemv2", 5: "project", 6: "gs",
+        9: "dots"}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("config", type=int)
