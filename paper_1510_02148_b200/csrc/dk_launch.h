@@ -206,12 +206,15 @@ struct TileGemv {
   // an evict-last hint)
   void* win_base = nullptr;
   size_t win_bytes = 0;
+  const int* split_rows = nullptr;  // output blocks split across warps (NOSPIN finish)
+  int nsplit = 0;
 };
 struct TileGemvHost {
   long long nt = 0;
   int nw = 0;
   std::vector<int> trow, tcol, rfirst, rslot, rnp;
   std::vector<int> tid;  // empty: tiles stored in stream order
+  std::vector<int> split_rows;
   int nslots = 1;
 };
 // E's off-diagonal pattern (CSR, host)

@@ -175,7 +175,10 @@ __device__ __forceinline__ double butterfly_sum32(double (&v)[32], int lane) {
   return v[0];
 }
 
-template <int KW, int KS, bool TRANS>
+// NOSPIN (DK_NO_SPIN, or a grid that cannot be co-resident): no warp waits for another —
+// every piece of a split block goes to its slot and k_tg_finish sums them after the grid
+// (same order, bitwise equal).
+template <int KW, int KS, bool TRANS, bool NOSPIN>
 __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* __restrict__ x,
                                                       double* __restrict__ y,
                                                       const int* __restrict__ scatter, int d,
@@ -284,7 +287,10 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
       // fence or ticket is needed; the finisher re-arms the slots.  Sum in warp order.
       const int q = (int)(w - g.rfirst[R]);
       double* slots = g.part + (long long)g.rslot[R] * kPT + lane;
-      if (q != 0) {
+      if (NOSPIN) {
+        slots[(long long)q * kPT] = racc;
+        write = false;
+      } else if (q != 0) {
         slots[(long long)q * kPT] = racc;
         write = false;
       } else {
@@ -612,6 +618,9 @@ static int build_stream(const std::vector<int>& ti, const std::vector<int>& tj, 
     if (wb > wa) slots += (int)(wb - wa + 1);
   }
   h.nslots = std::max(slots, 1);
+  h.split_rows.clear();
+  for (int R = 0; R < nrows; ++R)
+    if (h.rnp[R] > 1) h.split_rows.push_back(R);
   return 0;
 }
 
@@ -679,6 +688,10 @@ int upload_stream(const double* W, int d, int ld, bool pack, const TileGemvHost&
   if (!h.tid.empty()) up(&tid, h.tid);
   g.tid = tid;
   g.trans = !h.tid.empty();
+  int* srows = nullptr;
+  if (!h.split_rows.empty()) up(&srows, h.split_rows);
+  g.split_rows = srows;
+  g.nsplit = (int)h.split_rows.size();
   up(&trow, h.trow);
   up(&tcol, h.tcol);
   up(&rfirst, h.rfirst);
@@ -703,10 +716,11 @@ int upload_stream(const double* W, int d, int ld, bool pack, const TileGemvHost&
 
 void free_stream(TileGemv& g, cudaStream_t s) {
   void* bufs[] = {(void*)g.trow, (void*)g.tcol, (void*)g.rfirst, (void*)g.rslot, (void*)g.rnp,
-                  (void*)g.part, (void*)g.tid};
+                  (void*)g.part, (void*)g.tid, (void*)g.split_rows};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);
-  g.trow = g.tcol = g.rfirst = g.rslot = g.rnp = g.tid = nullptr;
+  g.trow = g.tcol = g.rfirst = g.rslot = g.rnp = g.tid = g.split_rows = nullptr;
+  g.nsplit = 0;
   g.part = nullptr;
 }
 
@@ -726,6 +740,71 @@ int tgemv_warps_per_cta() { return kTgCfg[tgemv_cfg()][0]; }
 // SMs of the current device (the tile streams are split over tg_grid() CTAs)
 int tg_grid() { return num_sms(); }
 
+// the split blocks of a NOSPIN pass: one warp per block, pieces summed in warp order (the
+// finisher's arithmetic), slots re-armed
+__global__ void __launch_bounds__(256) k_tg_finish(TileGemv g, double* __restrict__ y,
+                                                   const int* __restrict__ scatter, int d,
+                                                   const int* __restrict__ gate) {
+  pdl_wait();
+  if (gate != nullptr && *gate == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (k >= g.nsplit) return;
+  const int R = g.split_rows[k];
+  const int np = g.rnp[R];
+  double* slots = g.part + (long long)g.rslot[R] * kPT + lane;
+  double out = 0.0 + slots[0];
+  slots[0] = sentinel_f64();
+  for (int q = 1; q < np; ++q) {
+    out += slots[(long long)q * kPT];
+    slots[(long long)q * kPT] = sentinel_f64();
+  }
+  const int row = R * kPT + lane;
+  if (row < d) y[scatter ? scatter[row] : row] = out;
+}
+
+// the whole grid (one CTA per SM at this shared-memory size) must be co-resident for the
+// finisher warps' waits; otherwise, or with DK_NO_SPIN, the NOSPIN pass + k_tg_finish
+template <int KW, int KS, bool TRANS>
+static bool tg_spin_ok(unsigned grid, size_t smem) {
+  static int per_sm[kMaxDevices];
+  static bool init[kMaxDevices];
+  static const bool env = getenv("DK_NO_SPIN") != nullptr;
+  if (env) return false;
+  const int dev = current_device();
+  if (!init[dev]) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tgemv<KW, KS, TRANS, false>, KW * 32,
+                                                      smem) != cudaSuccess) {
+      cudaGetLastError();
+      b = 0;
+    }
+    per_sm[dev] = b;
+    init[dev] = true;
+  }
+  return (long long)per_sm[dev] * num_sms() >= (long long)grid;
+}
+
+template <int KW, int KS, bool TRANS>
+static void launch_tg_t(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
+                        const int* gate, cudaStream_t s, unsigned grid, size_t smem,
+                        const cudaAccessPolicyWindow* win) {
+  const bool spin = tg_spin_ok<KW, KS, TRANS>(grid, smem);
+  if (win) access_window_next() = win;
+  if (spin) {
+    smem_optin((const void*)k_tgemv<KW, KS, TRANS, false>, smem);
+    launch_pdl(k_tgemv<KW, KS, TRANS, false>, dim3(grid), dim3(KW * 32), smem, s, g, x, y,
+               scatter, d, gate);
+    return;
+  }
+  smem_optin((const void*)k_tgemv<KW, KS, TRANS, true>, smem);
+  launch_pdl(k_tgemv<KW, KS, TRANS, true>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter,
+             d, gate);
+  if (g.nsplit > 0)
+    launch_pdl(k_tg_finish, dim3((unsigned)((g.nsplit * 32 + 255) / 256)), dim3(256), 0, s, g, y,
+               scatter, d, gate);
+}
+
 template <int KW, int KS>
 static void launch_tg(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
                       const int* gate, cudaStream_t s) {
@@ -738,17 +817,12 @@ static void launch_tg(const TileGemv& g, const double* x, double* y, const int* 
     win.hitRatio = 1.0f;
     win.hitProp = cudaAccessPropertyPersisting;
     win.missProp = cudaAccessPropertyStreaming;
-    access_window_next() = &win;
   }
-  if (g.trans) {
-    smem_optin((const void*)k_tgemv<KW, KS, true>, smem);
-    launch_pdl(k_tgemv<KW, KS, true>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d,
-               gate);
-  } else {
-    smem_optin((const void*)k_tgemv<KW, KS, false>, smem);
-    launch_pdl(k_tgemv<KW, KS, false>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter, d,
-               gate);
-  }
+  const cudaAccessPolicyWindow* wp = g.win_bytes ? &win : nullptr;
+  if (g.trans)
+    launch_tg_t<KW, KS, true>(g, x, y, scatter, d, gate, s, grid, smem, wp);
+  else
+    launch_tg_t<KW, KS, false>(g, x, y, scatter, d, gate, s, grid, smem, wp);
 }
 
 void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,

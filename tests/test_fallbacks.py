@@ -1,0 +1,59 @@
+"""The non-spinning fallbacks reproduce the default device path bit for bit (GPU).
+
+Grids whose blocks wait on other blocks of the same grid (the tile GEMV's split-block
+finishers, k_gs's fused second Gram-Schmidt pass) and the early starts across grids each have
+a non-waiting fallback, chosen automatically when the grid cannot be co-resident and forced by
+environment switches (read once per process, so each variant runs in a subprocess):
+  DK_NO_SPIN     tile GEMV pieces all go to slots, k_tg_finish sums them after the grid
+  DK_NO_GS_FUSE  the second Gram-Schmidt pass as separate launches
+  DK_NO_EARLY    no early start of the stencil / k_gs on published partials
+Config 3 uses the nested-dissection tile streams (the spinning finisher) and its x is
+compared bitwise; config 1 checks the small-d coarse paths.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import hashlib, json, sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_1510_02148_b200 as dk
+from paper_1510_02148_b200 import configs
+case = configs.make_case({cfg})
+A, b = case.problem()
+M = dk.Preconditioner.jacobi(A)
+basis = dk.partition_to_basis(case.partition())
+rep = dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=case.max_iters)
+print(json.dumps({{"iters": rep.iterations, "relres": rep.final_relres,
+                  "x": hashlib.sha256(np.ascontiguousarray(rep.x).tobytes()).hexdigest(),
+                  "hist": hashlib.sha256(np.asarray(rep.residual_history).tobytes()).hexdigest()}}))
+"""
+
+
+def _run(cfg, env_extra):
+    env = {k: v for k, v in os.environ.items() if not k.startswith("DK_")}
+    env.update(env_extra)
+    out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=str(ROOT), cfg=cfg)],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_fallbacks_bitwise(gpu, cfg):
+    ref = _run(cfg, {})
+    for extra in ({"DK_NO_SPIN": "1"},
+                  {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"}):
+        got = _run(cfg, extra)
+        assert got == ref, (extra, got, ref)

@@ -22,6 +22,9 @@ basis = dk.partition_to_basis(case.partition())
 ctx = dk.build_context(A, M, basis, b)
 print("coarse kind", ctx.coarse_kind(), "d", basis.d)
 E, Einv = ctx.coarse_matrix(inverse=True)
+import os
+os.makedirs("gpurun_out", exist_ok=True)
+np.save("gpurun_out/config4_E_dev.npy", E)
 dg = np.abs(np.diag(E))
 D = 1.0 / np.sqrt(dg)
 Es = D[:, None] * E * D[None, :]
@@ -41,6 +44,8 @@ for trial in range(3):
           f"{np.linalg.norm(E @ ye - s) / np.linalg.norm(s):.3e}")
 g = np.load(sys.argv[1]) if len(sys.argv) > 1 else None
 rep = dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=200)
+np.savez("gpurun_out/config4_dev_x.npz", x_sketch=O.sketch(rep.x), x_norm=np.linalg.norm(rep.x),
+         x_sample=rep.x[::97], history=rep.residual_history)
 for name in ("tests/golden/config4_oracle.npz",) + ((sys.argv[1],) if g is not None else ()):
     gg = np.load(name)
     est = np.linalg.norm(O.sketch(rep.x) - gg["x_sketch"]) / np.sqrt(len(gg["x_sketch"]))
