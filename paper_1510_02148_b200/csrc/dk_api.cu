@@ -1321,7 +1321,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
       cudaEventCreate(&f1);
       cudaEventRecord(f0, s);
       DKD(cudaMemsetAsync(c->Einv, 0, ebytes, s));
-      err = nd_tree_inverse(Ework, d, c->ld, tree, c->Einv, &min_sq, s);
+      err = nd_tree_inverse(Ework, d, c->ld, tree, c->Einv, &min_sq, s, &gptr, &gcol, &iperm);
       cudaEventRecord(f1, s);
       cudaEventSynchronize(f1);
       cudaEventElapsedTime(&c->ms[1], f0, f1);

@@ -681,8 +681,33 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
 // |D|^2) instead of the O(d^3) of the dense factorisation.  Leaves (no descendants) are
 // factorised and inverted in one batched launch.  E~ is overwritten by the Schur complements
 // on the separator diagonal blocks; W must be zero on entry.
+// L_SD = E_SD W_D^T with E_SD sparse (the label graph: a few neighbours per separator row):
+// X[r][jj] = sum over the row's descendant neighbours k (ascending) of E~[s0 + r][k] W[t0 + jj][k]
+// (W is zero right of its diagonal and across children).  One block per row of W_D (read
+// once, L1-resident), fixed order per output.
+__global__ void __launch_bounds__(128) k_lsd_sparse(const double* __restrict__ E,
+                                                    const double* __restrict__ W, int ld, int s0,
+                                                    int ns, int t0, int nd,
+                                                    const int* __restrict__ rp,
+                                                    const int* __restrict__ ck,
+                                                    double* __restrict__ X, int ldx) {
+  for (int jj = blockIdx.x; jj < nd; jj += gridDim.x) {
+    const double* Wr = W + (long long)(t0 + jj) * ld;
+    for (int r = threadIdx.x; r < ns; r += blockDim.x) {
+      const double* Er = E + (long long)(s0 + r) * ld;
+      double acc = 0.0;
+      for (int i = rp[r]; i < rp[r + 1]; ++i) {
+        const int k = ck[i];
+        acc = fma(__ldg(Er + k), __ldg(Wr + k), acc);
+      }
+      X[(long long)r * ldx + jj] = acc;
+    }
+  }
+}
+
 int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tree, double* W,
-                    double* min_diag_sq, cudaStream_t s) {
+                    double* min_diag_sq, cudaStream_t s, const std::vector<int>* gptr,
+                    const std::vector<int>* gcol, const std::vector<int>* iperm) {
   smem_optin((const void*)k_chol_diag, kDiagSmem);
   auto at = [&](double* X, int r, int c) { return X + (long long)r * ld + c; };
   // leaves: batched diagonal factorisation + inversion
@@ -712,6 +737,56 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
     cudaMallocAsync(&X, (size_t)xmax * sizeof(double), s);
     cudaMallocAsync(&T, (size_t)xmax * sizeof(double), s);
   }
+  // separator-to-descendant couplings of every node (permuted columns, ascending), from E's
+  // pattern: L_SD by the sparse product instead of a dense GEMM (DK_DENSE_LSD: the GEMM)
+  std::vector<int> node_rp_off(tree.size(), -1), all_rp, all_ck;
+  if (gptr && gcol && iperm && !getenv("DK_DENSE_LSD")) {
+    std::vector<int> inv_perm(d);  // position -> label
+    for (int L = 0; L < d; ++L) inv_perm[(*iperm)[L]] = L;
+    for (size_t t = 0; t < tree.size(); ++t) {
+      const auto& n = tree[t];
+      const int ns = n.s1 - n.s0, nd = n.s0 - n.t0;
+      if (ns <= 0 || nd <= 0) continue;
+      node_rp_off[t] = (int)all_rp.size();
+      const int base = (int)all_ck.size();
+      std::vector<int> row;
+      for (int r = 0; r < ns; ++r) {
+        all_rp.push_back((int)all_ck.size() - base);
+        const int L = inv_perm[n.s0 + r];
+        row.clear();
+        for (int e = (*gptr)[L]; e < (*gptr)[L + 1]; ++e) {
+          const int p = (*iperm)[(*gcol)[e]];
+          if (p >= n.t0 && p < n.s0) row.push_back(p);
+        }
+        std::sort(row.begin(), row.end());
+        all_ck.insert(all_ck.end(), row.begin(), row.end());
+      }
+      all_rp.push_back((int)all_ck.size() - base);
+    }
+  }
+  // rp entries are relative to each node's first column index: keep per node (rp offset,
+  // ck offset) pairs
+  std::vector<int2> node_off(tree.size(), make_int2(-1, -1));
+  {
+    size_t rpo = 0, cko = 0;
+    for (size_t t = 0; t < tree.size(); ++t) {
+      if (node_rp_off[t] < 0) continue;
+      const auto& n = tree[t];
+      const int ns = n.s1 - n.s0;
+      node_off[t] = make_int2((int)rpo, (int)cko);
+      cko += (size_t)all_rp[rpo + ns];
+      rpo += (size_t)ns + 1;
+    }
+  }
+  int *d_rp = nullptr, *d_ck = nullptr;
+  if (!all_rp.empty()) {
+    cudaMallocAsync(&d_rp, all_rp.size() * sizeof(int), s);
+    cudaMemcpyAsync(d_rp, all_rp.data(), all_rp.size() * sizeof(int), cudaMemcpyHostToDevice, s);
+    cudaMallocAsync(&d_ck, std::max<size_t>(all_ck.size(), 1) * sizeof(int), s);
+    if (!all_ck.empty())
+      cudaMemcpyAsync(d_ck, all_ck.data(), all_ck.size() * sizeof(int), cudaMemcpyHostToDevice,
+                      s);
+  }
   double host_min = INFINITY;
   int slot = (int)jobs.size();
   const bool trace = getenv("DK_TRACE_TREE") != nullptr;
@@ -722,17 +797,24 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
     cudaEventSynchronize(tev[0]);
   }
   auto t_start = std::chrono::steady_clock::now();
-  for (const auto& n : tree) {
+  for (size_t t = 0; t < tree.size(); ++t) {
+    const auto& n = tree[t];
     const int ns = n.s1 - n.s0, nd = n.s0 - n.t0;
     if (ns <= 0 || (nd == 0 && ns <= DB)) continue;
     if (trace) cudaEventRecord(tev[1], s);
     if (nd > 0) {
       const int ldx = nd;
-      // L_SD = E_SD W_D^T, child by child (W_C lower: op(B)[k][j] = 0 for k > j)
-      for (int k : n.kids) {
-        const int a = tree[k].t0, nc = tree[k].s1 - tree[k].t0;
-        gemm_mma(false, true, at(E, n.s0, a), ld, at(W, a, a), ld, X + (a - n.t0), ldx, ns, nc,
-                 nc, 1.0, 0.0, 0, INT_MIN, s, 0);
+      if (node_off[t].x >= 0) {
+        // L_SD = E_SD W_D^T, E_SD sparse
+        k_lsd_sparse<<<(unsigned)std::min(nd, 16 * num_sms()), 128, 0, s>>>(
+            E, W, ld, n.s0, ns, n.t0, nd, d_rp + node_off[t].x, d_ck + node_off[t].y, X, ldx);
+      } else {
+        // L_SD = E_SD W_D^T, child by child (W_C lower: op(B)[k][j] = 0 for k > j)
+        for (int k : n.kids) {
+          const int a = tree[k].t0, nc = tree[k].s1 - tree[k].t0;
+          gemm_mma(false, true, at(E, n.s0, a), ld, at(W, a, a), ld, X + (a - n.t0), ldx, ns,
+                   nc, nc, 1.0, 0.0, 0, INT_MIN, s, 0);
+        }
       }
       // S = E_S - L_SD L_SD^T (lower tiles)
       gemm_mma(false, true, X, ldx, X, ldx, at(E, n.s0, n.s0), ld, ns, ns, nd, -1.0, 1.0, 1,
@@ -784,6 +866,8 @@ int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tre
   const cudaError_t e = cudaStreamSynchronize(s);
   cudaFreeAsync(dpmin, s);
   if (djobs) cudaFreeAsync(djobs, s);
+  if (d_rp) cudaFreeAsync(d_rp, s);
+  if (d_ck) cudaFreeAsync(d_ck, s);
   if (X) cudaFreeAsync(X, s);
   if (T) cudaFreeAsync(T, s);
   double mn = host_min;

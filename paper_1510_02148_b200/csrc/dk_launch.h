@@ -182,8 +182,12 @@ int spd_inverse(double* L, int d, int ld, double* W, double* min_diag_sq, float*
 struct NDTreeNode;
 // W = L^-1 of an SPD E~ in nested-dissection order, node by node along the tree (W zeroed
 // on entry; E~'s separator blocks are overwritten).  *min_diag_sq as for spd_inverse.
+// With E's pattern (host CSR in label order) and iperm (label -> position), L_SD = E_SD W_D^T
+// is the sparse product instead of dense GEMMs.
 int nd_tree_inverse(double* E, int d, int ld, const std::vector<NDTreeNode>& tree, double* W,
-                    double* min_diag_sq, cudaStream_t s);
+                    double* min_diag_sq, cudaStream_t s, const std::vector<int>* gptr = nullptr,
+                    const std::vector<int>* gcol = nullptr,
+                    const std::vector<int>* iperm = nullptr);
 // X = W^T W (full, d x d) for lower-triangular W
 void lauum_into(const double* W, int d, int ld, double* X, cudaStream_t s);
 
