@@ -116,17 +116,32 @@ class LabelDeflation:
         # A_p = A or A M^-1 (deflation.py:50-51): column scaling by inv_diag
         Ap = A if ap == "A" else (A @ scipy.sparse.diags(inv_diag)).tocsr()
         self.Ap = Ap
-        # E = sum of A_p's nonzeros by (label_row, label_col), in row blocks (bounded memory)
-        E = np.zeros(self.d * self.d)
+        # E = Z^T (A_p Z) (deflation.py:84-85) with the row-wise product first, as the
+        # reference's A_p @ Z forms it: q_i = (A_p Z)[i, lab(i)] sums row i's coefficients
+        # into its own label in CSR (ascending column) order; E[L][L] = sum of q_i over the
+        # cells of L in ascending order; E[L][L2] (L2 != L) = sum of the coupling
+        # coefficients in (row, column) order.  Every sum is sequential (np.bincount adds in
+        # input order), so the order is fully defined: the in-label couplings nearly cancel
+        # on the diagonal and at a high coefficient contrast (BASELINE config 4) the order
+        # fixes the last bits that the ill-conditioned coarse solve amplifies.  Row blocks
+        # bound the memory; off-diagonal entries are collected in order and summed once.
         n = Ap.shape[0]
+        q = np.zeros(n)
+        okeys, ovals = [], []
         step = 1 << 22
         for r0 in range(0, n, step):
-            blk = Ap[r0:min(n, r0 + step)].tocoo()
+            blk = Ap[r0:min(n, r0 + step)].tocoo()  # row-major, columns ascending per row
             lr, lc = self.lab[blk.row + r0], self.lab[blk.col]
-            ok = (lr >= 0) & (lc >= 0)
-            E += np.bincount(lr[ok] * self.d + lc[ok], weights=blk.data[ok],
-                             minlength=self.d * self.d)
-        E = E.reshape(self.d, self.d)
+            own = (lr >= 0) & (lc == lr)
+            q[r0:r0 + blk.shape[0]] = np.bincount(blk.row[own], weights=blk.data[own],
+                                                  minlength=blk.shape[0])
+            cross = (lr >= 0) & (lc >= 0) & (lc != lr)
+            okeys.append(lr[cross].astype(np.int64) * self.d + lc[cross])
+            ovals.append(blk.data[cross])
+        E = np.bincount(np.concatenate(okeys), weights=np.concatenate(ovals),
+                        minlength=self.d * self.d).reshape(self.d, self.d)
+        diag = np.bincount(self.lab[self.keep], weights=q[self.keep], minlength=self.d)
+        E[np.arange(self.d), np.arange(self.d)] = diag
         self.E = E
         # dense_lu (sparse.py:121-137)
         lu, piv = scipy.linalg.lu_factor(E, check_finite=True)

@@ -111,6 +111,7 @@ struct dk_op {
   bool gs_fuse = false;  // second Gram-Schmidt pass inside k_gs (whole grid co-resident)
   // split iteration: the basis sweep runs on `aux` beside the coarse solve
   bool split = false;
+  bool small = false;  // the cycle's Arnoldi steps in one persistent grid (k_cycle_small)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int G_dots = 1;
@@ -356,7 +357,9 @@ int ensure_part(dk_op* op, int q) {
   if (op->part_q < q) {
     if (op->part) DK_TRY(cudaFreeAsync(op->part, op->stream));
     if (op->gpart) DK_TRY(cudaFreeAsync(op->gpart, op->stream));
-    DK_TRY(cudaMallocAsync(&op->part, (size_t)q * op->G * sizeof(double), op->stream));
+    // [q][grid] partials: grids of up to max(G, SMs) blocks (the persistent small cycle)
+    DK_TRY(cudaMallocAsync(&op->part, (size_t)q * std::max(op->G, num_sms()) * sizeof(double),
+                           op->stream));
     DK_TRY(cudaMallocAsync(&op->gpart, (size_t)q * kGroupTickets * sizeof(double), op->stream));
     op->part_q = q;
     op->g_m = -1;  // the graph refers to the old buffer
@@ -710,6 +713,20 @@ void issue_iteration(dk_op* op, dk_defl* c, int j) {
   }
 }
 
+// the m Arnoldi steps of a cycle as one persistent cooperative grid (small problems)
+void issue_cycle_small(dk_op* op, dk_defl* c, int m) {
+  const bool pre = op->inv != nullptr;
+  const bool am = c && c->ap == DK_AP_AM;
+  Scal sc = op->sc;
+  sc.post = nullptr;
+  ProfScope ps(op, PC_PROJECT, 0.0);
+  launch_cycle_small(c ? DK_LABELS : DK_NONE, pre, am, make_dia(op, pre), make_dia(op, am),
+                     c ? c->pro : Prolong{}, c ? c->rm : RunMap{}, c ? c->Einv : nullptr,
+                     c ? c->ld : 0, op->V_base + op->guard, op->vstride, op->n_pad, op->part,
+                     c ? c->y : nullptr, sc, op->stream);
+  (void)m;
+}
+
 void issue_cycle_end(dk_op* op) {
   const bool pre = op->inv != nullptr;
   const Dia A = make_dia(op, pre);
@@ -728,7 +745,8 @@ int read_state(dk_op* op) {
 }
 
 int build_graph(dk_op* op, dk_defl* c, int m) {
-  const unsigned long long key = (c ? c->serial : 0ull) * 2 + (op->split ? 1 : 0);
+  const unsigned long long key =
+      (c ? c->serial : 0ull) * 4 + (op->split ? 1 : 0) + (op->small ? 2 : 0);
   if (op->gexec && op->g_m == m && op->g_ctx == key) return DK_OK;
   if (op->gexec) {
     cudaGraphExecDestroy(op->gexec);
@@ -740,7 +758,9 @@ int build_graph(dk_op* op, dk_defl* c, int m) {
   pdl_skip_next() = true;
   const int l0 = op->launches;
   issue_restart(op, c);
-  for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
+  if (op->small) issue_cycle_small(op, c, m);
+  else
+    for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
   issue_cycle_end(op);
   op->launches = l0;
   {
@@ -1808,6 +1828,10 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
                            cudaMemcpyDeviceToDevice, op->stream));
   }
   if ((rc = setup_split(op, c, m))) return rc;
+  // small problems: the cycle's Arnoldi steps in one persistent grid (not when profiling per
+  // kernel, not with the nested-dissection / dense-basis coarse paths)
+  op->small = !op->prof && !op->split && (!c || (!c->dense && !c->prof)) &&
+              cycle_small_ok(op->n_pad, m, c ? c->d : 0);
   launch_init_state(op->sc, tol, m, max_iters, min_iters, op->stream);
   op->launches += 1;
   const bool resume = ctl_in && ctl_in->resume;
@@ -1821,7 +1845,8 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   const bool run_cycles = !(resume && ctl_in->iterations >= max_iters);
   // The cycle becomes a CUDA graph from the second solve with the same (context, m): a
   // one-off solve (the public pdgmres path) launches eagerly and skips the instantiation.
-  const unsigned long long key = (c ? c->serial : 0ull) * 2 + (op->split ? 1 : 0);
+  const unsigned long long key =
+      (c ? c->serial : 0ull) * 4 + (op->split ? 1 : 0) + (op->small ? 2 : 0);
   const bool use_graph =
       !op->prof && ((op->gexec && op->g_m == m && op->g_ctx == key) ||
                     (op->seen_m == m && op->seen_ctx == key));
@@ -1840,8 +1865,9 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   // restart (stencil chain + projection), m x (stencil chain, projection, update [+ the
   // separate second pass]), cycle end, x update
   const int per_cycle_launches =
-      coarse_launches + 1 + m * (coarse_launches + (op->gs_fuse ? 2 : 4) + (op->split ? 1 : 0)) +
-      2;
+      op->small ? coarse_launches + 1 + 1 + 2
+                : coarse_launches + 1 +
+                      m * (coarse_launches + (op->gs_fuse ? 2 : 4) + (op->split ? 1 : 0)) + 2;
   long long guard_cycles = run_cycles ? (long long)max_iters + 2 : 0;
   if (max_cycles > 0 && guard_cycles > max_cycles) guard_cycles = max_cycles;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
@@ -1851,7 +1877,9 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
     } else if (!op->prof) {
       const int l0 = op->launches;
       issue_restart(op, c);
-      for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
+      if (op->small) issue_cycle_small(op, c, m);
+      else
+        for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
       issue_cycle_end(op);
       op->launches = l0 + per_cycle_launches;
       DK_TRY(launch_error());

@@ -378,8 +378,8 @@ void launch_symv_reduce(int d, const double* rowpart, const double* colpart,
 
 // ======================================================================================
 // Assembly of E = Z^T A_p Z for an indicator Z given by labels.
-//   E[L][L]  = sum over cells i of L of q_i, q_i = sum of the row's coefficients whose
-//              column is in L — a run-wise restriction of q (deterministic);
+//   E[L][L]  = sum over cells i of L (ascending) of q_i, q_i = sum of the row's coefficients
+//              whose column is in L (ascending column) — sequential, deterministic;
 //   E[L][L2] = sum over (i in L, k in L2, k = i + off) of a_ik — the boundary-face list is
 //              sorted by key (L, L2) with a stable radix sort and summed per key in cell
 //              order (deterministic).
@@ -447,9 +447,49 @@ __global__ void k_coarse_reduce(const unsigned long long* __restrict__ keys,
   }
 }
 
-__global__ void k_set_diag(double* __restrict__ E, int d, int ld, const double* __restrict__ s) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
-    E[(long long)i * ld + i] = s[i];
+// Diagonal E[L][L] = sum over the cells of L in ascending order of q_i — a plain sequential
+// sum per label (the oracle's np.bincount order; the in-label couplings nearly cancel, so
+// the order is what fixes the last bits at a high coefficient contrast).  Cells are grouped
+// by a stable sort of their labels (unlabelled cells sort last, as label d).
+__global__ void k_label_keys(const int* __restrict__ lab, long long n_pad, int d,
+                             int* __restrict__ key, int* __restrict__ cell) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int L = lab[i];
+    key[i] = L >= 0 ? L : d;
+    cell[i] = (int)i;
+  }
+}
+
+// start[L] = first sorted position of label L (start[d] = end of the labelled cells)
+__global__ void k_label_start(const int* __restrict__ skey, long long n, int d,
+                              int* __restrict__ start) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = skey[i];
+    const int prev = i > 0 ? skey[i - 1] : -1;
+    for (int L = prev + 1; L <= k && L <= d; ++L) start[L] = (int)i;
+    if (i == n - 1)
+      for (int L = k + 1; L <= d; ++L) start[L] = (int)n;
+  }
+}
+
+__global__ void k_diag_seq(const double* __restrict__ q, const int* __restrict__ cells,
+                           const int* __restrict__ start, int d, double* __restrict__ E, int ld) {
+  for (int L = blockIdx.x * blockDim.x + threadIdx.x; L < d; L += gridDim.x * blockDim.x) {
+    const int p0 = start[L], p1 = start[L + 1];
+    double s = 0.0;
+    int p = p0;
+    for (; p + 8 <= p1; p += 8) {  // eight loads in flight, then the in-order sum
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = q[cells[p + k]];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
+    }
+    for (; p < p1; ++p) s = __dadd_rn(s, q[cells[p]]);
+    E[(long long)L * ld + L] = s;
+  }
 }
 
 static int bits_for(unsigned long long v) {
@@ -483,11 +523,35 @@ int build_coarse(const Dia& A, bool am, const int* lab, long long n_pad, const R
   if (am) k_coarse_scan<true><<<grid, kThreads, 0, s>>>(A, lab, n_pad, qv, cnt);
   else k_coarse_scan<false><<<grid, kThreads, 0, s>>>(A, lab, n_pad, qv, cnt);
   DKC(cudaGetLastError());
-  // diagonal: run-wise restriction of q
-  launch_stencil(ST_IDENT, false, false, A, n_pad, qv, nullptr, nullptr, nullptr, &rm, nullptr, s);
-  launch_restrict_final(rm, sdiag, nullptr, s);
-  k_set_diag<<<(d + kThreads - 1) / kThreads, kThreads, 0, s>>>(E, d, ld, sdiag);
-  DKC(cudaGetLastError());
+  // diagonal: per label, the sequential sum of q over its cells in ascending order
+  (void)rm;
+  {
+    int *key_in = nullptr, *key_out = nullptr, *cell_in = nullptr, *cell_out = nullptr,
+        *start = nullptr;
+    void* stmp = nullptr;
+    size_t sbytes = 0;
+    const int kbits = bits_for((unsigned long long)d + 1);
+    DKC(cudaMallocAsync(&key_in, (size_t)n_pad * sizeof(int), s));
+    DKC(cudaMallocAsync(&key_out, (size_t)n_pad * sizeof(int), s));
+    DKC(cudaMallocAsync(&cell_in, (size_t)n_pad * sizeof(int), s));
+    DKC(cudaMallocAsync(&cell_out, (size_t)n_pad * sizeof(int), s));
+    DKC(cudaMallocAsync(&start, (size_t)(d + 1) * sizeof(int), s));
+    k_label_keys<<<grid, kThreads, 0, s>>>(lab, n_pad, d, key_in, cell_in);
+    DKC(cub::DeviceRadixSort::SortPairs(nullptr, sbytes, key_in, key_out, cell_in, cell_out,
+                                        (int)n_pad, 0, kbits, s));
+    DKC(cudaMallocAsync(&stmp, sbytes, s));
+    DKC(cub::DeviceRadixSort::SortPairs(stmp, sbytes, key_in, key_out, cell_in, cell_out,
+                                        (int)n_pad, 0, kbits, s));
+    k_label_start<<<grid, kThreads, 0, s>>>(key_out, n_pad, d, start);
+    k_diag_seq<<<(d + 127) / 128, 128, 0, s>>>(qv, cell_out, start, d, E, ld);
+    DKC(cudaGetLastError());
+    cudaFreeAsync(key_in, s);
+    cudaFreeAsync(key_out, s);
+    cudaFreeAsync(cell_in, s);
+    cudaFreeAsync(cell_out, s);
+    cudaFreeAsync(start, s);
+    cudaFreeAsync(stmp, s);
+  }
   // off-diagonal: boundary faces
   DKC(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, (int)n_pad, s));
   DKC(cudaMallocAsync(&tmp, tmp_bytes, s));

@@ -207,7 +207,7 @@ __device__ __forceinline__ void tl_mark_warp(unsigned kind, unsigned phase) {
 #define DK_TL_SETTER(fn)
 #endif
 enum TlKind { TL_STENCIL = 1, TL_RESTRICT = 2, TL_TG1 = 3, TL_TG2 = 4, TL_PROJECT = 5, TL_GS = 6,
-              TL_TG1W = 7, TL_TG2W = 8, TL_DOTS = 9 };
+              TL_TG1W = 7, TL_TG2W = 8, TL_DOTS = 9, TL_SMALL = 10 };
 
 // ---- small device helpers -------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {

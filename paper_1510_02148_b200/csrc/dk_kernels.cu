@@ -1040,11 +1040,22 @@ __device__ void iter_finish(const Scal& sc, int j, int nvec, double* red) {
       sh_g[(nvec - 1) * nvec + v] = g;
     }
   }
-  if (stage)
-    for (int e = threadIdx.x; e < (nvec - 1) * (nvec - 1); e += blockDim.x) {
-      const int i = e / (nvec - 1), k = e % (nvec - 1);
-      sh_g[i * nvec + k] = gram_at(sc.Gm, m, i, k);
+  if (stage) {  // eight Gram loads per thread in flight (this section is latency-bound)
+    const int ne = (nvec - 1) * (nvec - 1);
+    for (int e0 = threadIdx.x; e0 < ne; e0 += 8 * blockDim.x) {
+      double g8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        g8[u] = e < ne ? gram_at(sc.Gm, m, e / (nvec - 1), e % (nvec - 1)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < ne) sh_g[(e / (nvec - 1)) * nvec + e % (nvec - 1)] = g8[u];
+      }
     }
+  }
   __syncthreads();
   // corr_i = h_i - sum_k G_ik h_k
   for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
@@ -1693,6 +1704,490 @@ __global__ void __launch_bounds__(kThreads) k_gs(const double* w_in, double* u_o
   if (!REORTH && !second && sc.st->reorth) return;  // the separate second pass finishes it
   finish_iteration_block(sc, j, hj1, red);
   if (!REORTH) DK_TL(TL_GS, 5);
+}
+
+// ======================================================================================
+// Small problems (one 2048-cell chunk per block, the basis L2-resident: BASELINE config 1):
+// the cycle's m Arnoldi steps run in ONE persistent, co-resident (cooperative) grid instead of
+// 5 launches per step, each of which is pure latency at this size.  Per step j:
+//   stencil w = A M^-1 (sigma_j u_j) of the block's chunk (kept in registers) + its run sums
+//   | lead: s = Z^T w (warp per column, runs in order), y = E^-1 s (dense E^-1, d <= 64)
+//   w -= A_p Z y (compact prolongation, y in shared memory); block partials of U^T w, the
+//   Gram column U^T u_j and ||w||^2
+//   | lead: reduction + iter_finish (H column, coefficients, re-orthogonalisation test)
+//   u = w - U coef (+ the second pass through one more lead when the test fired), stored
+//   as basis row j+1; block partial of ||u||^2
+//   | lead: finish_iteration_block (Givens, convergence, breakdown, sigma_{j+1})
+// "|" is grid_arrive_lead_release: the last block to arrive runs the control section (the
+// same device functions as the multi-kernel path) before releasing the others.  Block-local
+// sums run in fixed order; results agree with the multi-kernel path to rounding (parity
+// against the reference is the bar; the path is chosen by shape, DK_NO_SMALL disables it).
+// ======================================================================================
+constexpr int kSmallMaxD = 64;
+constexpr int kSmallRuns = 32;  // label runs per warp and cell slot (at most one per lane)
+
+template <bool AM>
+__device__ __forceinline__ double prolong_cell_smem(const Dia& A, const Prolong& P,
+                                                    const double* ys, long long c) {
+  const int L = P.lab[c];
+  const double own = P.own[c];
+  const int2 fl = P.flab[c];
+  const double2 fc = P.fco[c];
+  const unsigned msk = P.mask[c];
+  double t = (L >= 0) ? __dmul_rn(own, ys[L]) : 0.0;
+  if (fl.x >= 0) t = __dadd_rn(t, __dmul_rn(fc.x, ys[fl.x]));
+  if (fl.y >= 0) t = __dadd_rn(t, __dmul_rn(fc.y, ys[fl.y]));
+  if (msk) {
+#pragma unroll
+    for (int q = 0; q < kMaxDiag; ++q) {
+      if (!((msk >> q) & 1u)) continue;
+      const long long o = A.off[q];
+      double a = dia_coef(A, q, c);
+      if (AM) a = __dmul_rn(a, __ldg(A.inv + c + o));
+      t = __dadd_rn(t, __dmul_rn(a, ys[__ldg(P.lab + c + o)]));
+    }
+  }
+  return t;
+}
+
+// 32 per-lane values -> lane l holds the warp sum of value l (fixed butterfly: deterministic)
+__device__ __forceinline__ double small_transpose_sum(double (&v)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? v[k] : v[k + h];
+      const double keep = up ? v[k + h] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
+// out[q] = sum over the blocks of part[q * G + b]: each warp takes 8 quantities at a time,
+// lane l sums blocks l, l + 32, ... in order (all loads in flight), reduce8's fixed butterfly
+// combines the lanes (deterministic)
+__device__ __forceinline__ void small_reduce(const double* part, int nq, double* out) {
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q0 = 8 * warp; q0 < nq; q0 += 8 * kWarps) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double t = 0.0;
+      if (q0 + k < nq) {
+        const double* p = part + (size_t)(q0 + k) * G;
+        double a[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) a[i] = (lane + 32 * i < G) ? __ldcg(p + lane + 32 * i) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) t += a[i];
+      }
+      v[k] = t;
+    }
+    const double r = reduce8(v, lane);
+    if ((lane & 3) == 0 && q0 + (lane >> 2) < nq) out[q0 + (lane >> 2)] = r;
+  }
+  __syncthreads();
+}
+
+// Grid barrier of the persistent small-cycle grid: thread 0 of each block arrives with an
+// acq_rel atomic (release is cumulative over the block's writes ordered by the preceding
+// __syncthreads); the last to arrive runs lead() with the whole block, then releases the
+// others with a release store of the generation they poll with acquire loads.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <class F>
+__device__ __forceinline__ void small_barrier(unsigned* count, unsigned* gen, F lead) {
+  __shared__ int s_lead;
+  __shared__ unsigned s_gen;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire_u32(gen);
+    s_gen = g;
+    s_lead = (atom_add_acq_rel(count, 1u) == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_lead) {
+    DK_TL(TL_SMALL, 7);
+    lead();
+    __syncthreads();
+    DK_TL(TL_SMALL, 8);
+    if (threadIdx.x == 0) {
+      *reinterpret_cast<volatile unsigned*>(count) = 0u;
+      st_release_u32(gen, s_gen + 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    while (*reinterpret_cast<volatile unsigned*>(gen) == s_gen) __nanosleep(20);
+    (void)ld_acquire_u32(gen);  // acquire once the release is seen
+  }
+  __syncthreads();
+}
+
+// Block partials of nq <= 128 quantities (thread values vals(q)) to part[q * G + b]: batches
+// of 32 transposed-summed within the warp, then the warps in order.
+template <class F>
+__device__ __forceinline__ void small_partials(int nq, double* red, double* part, F vals) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q0 = 0; q0 < nq; q0 += 32) {
+    double v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = (q0 + k < nq) ? vals(q0 + k) : 0.0;
+    const double t = small_transpose_sum(v, lane);
+    if (q0 + lane < nq) red[(q0 + lane) * kWarps + warp] = t;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) t += red[q * kWarps + w2];
+    __stcg(part + (size_t)q * gridDim.x + blockIdx.x, t);
+  }
+  __syncthreads();
+}
+
+// ======================================================================================
+// Small problems (BASELINE config 1: 32 k cells, the whole basis L2-resident): the cycle's m
+// Arnoldi steps in ONE persistent cooperative grid over all SMs, CPT cells per thread
+// (consecutive threads own consecutive cells), instead of 5 latency-bound launches per step.
+// Per step j:
+//   w = A M^-1 (sigma_j u_j) (k_stencil's arithmetic), kept in registers; per-block label
+//   sums of w (warp-segmented runs of consecutive cells, fixed trees)
+//   | lead: s = Z^T w (blocks in order), y = E^-1 s (dense E^-1, d <= 64)
+//   w -= A_p Z y (compact prolongation, y in shared memory); block partials of U^T w, of the
+//   Gram column U^T u_j and of ||w||^2
+//   | lead: reduction + iter_finish (H column, coefficients, re-orthogonalisation test)
+//   u = w - U coef (+ the second pass through one more lead when the test fired), stored as
+//   basis row j+1; block partial of ||u||^2
+//   | lead: finish_iteration_block (Givens, convergence / breakdown, sigma_{j+1})
+// "|" is small_barrier: the last block to arrive runs the control section (the same device
+// functions as the multi-kernel path) before releasing the others.  Every sum has a fixed
+// order; results agree with the multi-kernel path to rounding (parity against the reference
+// is the bar).  Chosen by shape (cycle_small_ok); DK_NO_SMALL disables it.
+// ======================================================================================
+template <int DEFL, bool PRE, bool AM, int CPT>
+__global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Prolong P,
+                                                          const int* __restrict__ lab, int d,
+                                                          const double* __restrict__ Einv,
+                                                          int ld, double* V, long long vstride,
+                                                          long long n_pad, double* part,
+                                                          double* yg, Scal sc) {
+  extern __shared__ __align__(16) double sm[];
+  const int m = sc.m;
+  double* ctl = sm;  // control scratch of the lead
+  const int nctl = 4 * (m + 1) + 1 + (m + 1) * (m + 1) + 512;
+  double* red = ctl + nctl;  // [q][warp]
+  __shared__ double ys[kSmallMaxD];
+  __shared__ double cf[kMaxCycleSmall];
+  __shared__ double rsum[kWarps][CPT][kSmallRuns];
+  __shared__ int rlab[kWarps][CPT][kSmallRuns];
+  __shared__ int rcnt[kWarps][CPT];
+  State* st = sc.st;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long cell[CPT];
+  bool ok[CPT];
+#pragma unroll
+  for (int e = 0; e < CPT; ++e) {
+    cell[e] = (long long)blockIdx.x * blockDim.x + threadIdx.x + e * stride;
+    ok[e] = cell[e] < n_pad;
+    if (!ok[e]) cell[e] = 0;  // a padded cell: reads stay in bounds, results unused
+  }
+  int L[CPT];
+#pragma unroll
+  for (int e = 0; e < CPT; ++e) L[e] = (DEFL == DK_LABELS && ok[e]) ? __ldg(lab + cell[e]) : -1;
+  unsigned int* cnt = sc.gticket + kGroupTickets - 2;
+  unsigned int* gen = sc.gticket + kGroupTickets - 3;
+  pdl_wait();
+  for (int j = 0; j < m; ++j) {
+    if (*reinterpret_cast<volatile int*>(&st->active) == 0) break;
+    DK_TL(TL_SMALL, 0);
+    const int nvec = j + 1;
+    const double sig = __ldcg(sc.sigma + j);
+    const double* vj = V + (long long)j * vstride;
+    // ---- stencil: every coefficient and neighbour in flight, then the ordered sums
+    double w[CPT];
+#pragma unroll
+    for (int e = 0; e < CPT; ++e) {
+      const long long c = cell[e];
+      double a[kMaxDiag], x[kMaxDiag], mi[kMaxDiag];
+#pragma unroll
+      for (int q = 0; q < kMaxDiag; ++q) {
+        const bool on = q < A.ndiag;
+        const long long o = on ? A.off[q] : 0;
+        a[q] = on ? dia_coef(A, q, c) : 0.0;
+        x[q] = on ? __ldcg(vj + c + o) : 0.0;
+        mi[q] = (on && PRE) ? __ldg(A.inv + c + o) : 1.0;
+      }
+      double r = 0.0;
+#pragma unroll
+      for (int q = 0; q < kMaxDiag; ++q) {
+        if (q >= A.ndiag) break;
+        double y = __dmul_rn(x[q], sig);
+        if (PRE) y = __dmul_rn(y, mi[q]);
+        r = __dadd_rn(r, __dmul_rn(a[q], y));
+      }
+      w[e] = ok[e] ? r : 0.0;
+    }
+    if (DEFL == DK_LABELS) {
+      // warp-segmented label runs of consecutive cells: inclusive segmented scan, the run's
+      // last lane records (label, sum)
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) {
+        const int Lp = __shfl_up_sync(0xffffffffu, L[e], 1);
+        const bool head = lane == 0 || Lp != L[e];
+        double v = L[e] >= 0 ? w[e] : 0.0;
+        unsigned hm = __ballot_sync(0xffffffffu, head);
+#pragma unroll
+        for (int dlt = 1; dlt < 32; dlt <<= 1) {
+          const double u = __shfl_up_sync(0xffffffffu, v, dlt);
+          // add while lane - dlt is still inside this lane's run
+          const int seg_start = 31 - __clz(hm & ((2u << lane) - 1u));
+          if (lane >= dlt && lane - dlt >= seg_start) v = __dadd_rn(u, v);
+        }
+        const bool tail = lane == 31 || ((hm >> (lane + 1)) & 1u);
+        const unsigned tm = __ballot_sync(0xffffffffu, tail && L[e] >= 0);
+        const int ntail = __popc(tm);
+        if (lane == 0) rcnt[warp][e] = ntail;
+        if (tail && L[e] >= 0) {
+          const int k = __popc(tm & ((1u << lane) - 1u));
+          if (k < kSmallRuns) {
+            rsum[warp][e][k] = v;
+            rlab[warp][e][k] = L[e];
+          }
+        }
+      }
+      __syncthreads();
+      // block partial of label l: the runs in (warp, slot, run) order
+      for (int l = threadIdx.x; l < d; l += blockDim.x) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < kWarps; ++w2)
+#pragma unroll
+          for (int e = 0; e < CPT; ++e) {
+            const int nr = rcnt[w2][e];
+            for (int k = 0; k < nr && k < kSmallRuns; ++k)
+              if (rlab[w2][e][k] == l) t += rsum[w2][e][k];
+          }
+        __stcg(part + (size_t)l * gridDim.x + blockIdx.x, t);
+      }
+      DK_TL(TL_SMALL, 1);
+      // ---- lead: s = Z^T w (blocks in order), y = E^-1 s
+      small_barrier(cnt, gen, [&] {
+        small_reduce(part, d, ctl);
+        for (int l = threadIdx.x; l < d; l += blockDim.x) {
+          const double* Er = Einv + (long long)l * ld;
+          double t = 0.0;
+          int k = 0;
+          for (; k + 8 <= d; k += 8) {  // the row's loads in flight, then the ordered sum
+            double e8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) e8[u] = __ldg(Er + k + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t = fma(e8[u], ctl[k + u], t);
+          }
+          for (; k < d; ++k) t = fma(__ldg(Er + k), ctl[k], t);
+          __stcg(yg + l, t);
+        }
+      });
+      DK_TL(TL_SMALL, 2);
+      for (int l = threadIdx.x; l < d; l += blockDim.x) ys[l] = __ldcg(yg + l);
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < CPT; ++e)
+        if (ok[e]) w[e] = __dsub_rn(w[e], prolong_cell_smem<AM>(Aam, P, ys, cell[e]));
+    }
+    // ---- block partials: U^T w, U^T u_j, ||w||^2
+    double uj[CPT];
+#pragma unroll
+    for (int e = 0; e < CPT; ++e) uj[e] = __ldcg(vj + cell[e]);
+    DK_TL(TL_SMALL, 9);
+    small_partials(2 * nvec + 1, red, part, [&](int q) {
+      double t = 0.0;
+      if (q == 2 * nvec) {
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) t = fma(w[e], w[e], t);
+        return t;
+      }
+      const int v = q < nvec ? q : q - nvec;
+      const double* Vr = V + (long long)v * vstride;
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) t = fma(__ldcg(Vr + cell[e]), q < nvec ? w[e] : uj[e], t);
+      return t;
+    });
+    DK_TL(TL_SMALL, 3);
+    // ---- lead: the H column and the re-orthogonalisation test
+    small_barrier(cnt, gen, [&] {
+      small_reduce(part, 2 * nvec + 1, ctl);
+      iter_finish(sc, j, nvec, ctl);
+    });
+    DK_TL(TL_SMALL, 4);
+    // ---- u = w - U coef
+    for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = __ldcg(sc.coef + q);
+    __syncthreads();
+    double u[CPT];
+#pragma unroll
+    for (int e = 0; e < CPT; ++e) u[e] = w[e];
+#pragma unroll 8
+    for (int v = 0; v < nvec; ++v) {
+      const double c = cf[v];
+      const double* Vr = V + (long long)v * vstride;
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) u[e] = __dsub_rn(u[e], __dmul_rn(c, __ldcg(Vr + cell[e])));
+    }
+    if (*reinterpret_cast<volatile int*>(&st->reorth) != 0) {
+      // the second Gram-Schmidt pass (krylov.py:169-170): corr = V^T u, u -= V corr
+      small_partials(nvec, red, part, [&](int v) {
+        double t = 0.0;
+        const double* Vr = V + (long long)v * vstride;
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) t = fma(__ldcg(Vr + cell[e]), u[e], t);
+        return t;
+      });
+      small_barrier(cnt, gen, [&] {
+        small_reduce(part, nvec, ctl);
+        double* Hc = sc.H + (size_t)j * (m + 1);
+        double* cr = ctl + nvec;
+        for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+          cr[v] = ctl[v] * sc.sigma[v];
+          Hc[v] += cr[v];
+          sc.corr[v] = cr[v] * sc.sigma[v];
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+          double c = cr[i];
+          for (int k = 0; k < nvec; ++k) c -= gram_at(sc.Gm, m, i, k) * cr[k];
+          sc.gcol[i] = c;
+        }
+      });
+      for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = __ldcg(sc.corr + q);
+      __syncthreads();
+#pragma unroll 8
+      for (int v = 0; v < nvec; ++v) {
+        const double c = cf[v];
+        const double* Vr = V + (long long)v * vstride;
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) u[e] = __dsub_rn(u[e], __dmul_rn(c, __ldcg(Vr + cell[e])));
+      }
+    }
+    double* un = V + (long long)(j + 1) * vstride;
+#pragma unroll
+    for (int e = 0; e < CPT; ++e)
+      if (ok[e]) un[cell[e]] = u[e];
+    DK_TL(TL_SMALL, 5);
+    small_partials(1, red, part, [&](int) {
+      double t = 0.0;
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) t = fma(u[e], u[e], t);
+      return t;
+    });
+    // ---- lead: Givens, convergence / breakdown, sigma_{j+1}
+    small_barrier(cnt, gen, [&] {
+      small_reduce(part, 1, ctl);
+      const double hj1 = sqrt(ctl[0]);
+      __syncthreads();
+      finish_iteration_block(sc, j, hj1, ctl);
+    });
+    DK_TL(TL_SMALL, 6);
+  }
+}
+
+size_t cycle_small_smem(int m) {
+  const int nctl = 4 * (m + 1) + 1 + (m + 1) * (m + 1) + 512;
+  return ((size_t)nctl + (size_t)(2 * (m + 1) + 1 + 32) * kWarps) * sizeof(double);
+}
+
+// cells per thread over one block per SM
+static int small_cpt(long long n_pad) {
+  const long long threads = (long long)num_sms() * kThreads;
+  for (int c = 1; c <= 4; c <<= 1)
+    if ((long long)c * threads >= n_pad) return c;
+  return 0;
+}
+
+static unsigned small_grid(long long n_pad, int cpt) {
+  const long long need = (n_pad + (long long)cpt * kThreads - 1) / ((long long)cpt * kThreads);
+  return (unsigned)std::min<long long>(need, num_sms());
+}
+
+bool cycle_small_ok(long long n_pad, int m, int d) {
+  if (getenv("DK_NO_SMALL")) return false;
+  if (m + 1 > kMaxCycleSmall || d > kSmallMaxD) return false;
+  const int cpt = small_cpt(n_pad);
+  if (cpt == 0) return false;
+  // the grid must be co-resident (the cooperative launch fails otherwise)
+  int per_sm = 0;
+  const size_t smem = cycle_small_smem(m);
+  if (smem_optin((const void*)k_cycle_small<DK_LABELS, true, false, 4>, smem) ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, k_cycle_small<DK_LABELS, true, false, 4>, kThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (long long)per_sm * num_sms() >= small_grid(n_pad, cpt);
+}
+
+template <int DEFL, bool PRE, bool AM, int CPT>
+static void cycle_small_t(const Dia& A, const Dia& Aam, const Prolong& P, const int* lab, int d,
+                          const double* Einv, int ld, double* V, long long vstride,
+                          long long n_pad, double* part, double* yg, const Scal& sc,
+                          cudaStream_t s) {
+  const size_t smem = cycle_small_smem(sc.m);
+  smem_optin((const void*)k_cycle_small<DEFL, PRE, AM, CPT>, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(small_grid(n_pad, CPT));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency guaranteed or the launch fails
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  pdl_skip_next() = false;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cycle_small<DEFL, PRE, AM, CPT>, A, Aam, P,
+                                           lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc);
+  if (e != cudaSuccess) launch_error() = e;
+}
+
+template <int DEFL, bool PRE, bool AM>
+static void cycle_small_c(const Dia& A, const Dia& Aam, const Prolong& P, const int* lab, int d,
+                          const double* Einv, int ld, double* V, long long vstride,
+                          long long n_pad, double* part, double* yg, const Scal& sc,
+                          cudaStream_t s) {
+  switch (small_cpt(n_pad)) {
+    case 1: cycle_small_t<DEFL, PRE, AM, 1>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s); break;
+    case 2: cycle_small_t<DEFL, PRE, AM, 2>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s); break;
+    default: cycle_small_t<DEFL, PRE, AM, 4>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s); break;
+  }
+}
+
+void launch_cycle_small(int defl, bool pre, bool am, const Dia& A, const Dia& Aam,
+                        const Prolong& P, const RunMap& rm, const double* Einv, int ld, double* V,
+                        long long vstride, long long n_pad, double* part, double* yg,
+                        const Scal& sc, cudaStream_t s) {
+  const int* lab = rm.lab;
+  const int d = rm.d;
+  if (defl == DK_NONE) {
+    if (pre) cycle_small_c<DK_NONE, true, false>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s);
+    else cycle_small_c<DK_NONE, false, false>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s);
+  } else if (am) {
+    if (pre) cycle_small_c<DK_LABELS, true, true>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s);
+    else cycle_small_c<DK_LABELS, false, true>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s);
+  } else {
+    if (pre) cycle_small_c<DK_LABELS, true, false>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s);
+    else cycle_small_c<DK_LABELS, false, false>(A, Aam, P, lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc, s);
+  }
 }
 
 static size_t gs_smem(const Scal& sc, int nvec) {

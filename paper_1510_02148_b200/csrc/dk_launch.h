@@ -113,6 +113,14 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
 // the whole k_gs grid is co-resident: the second Gram-Schmidt pass may run inside it
 bool gs_can_fuse(int G, const Scal& sc);
 void launch_cycle_end(const Scal& sc, cudaStream_t s);
+// Small problems: the cycle's m Arnoldi steps in one persistent cooperative grid (one 2048-cell
+// chunk per block).  cycle_small_ok: shape and co-residency check (DK_NO_SMALL: never).
+constexpr int kMaxCycleSmall = 128;
+bool cycle_small_ok(long long n_pad, int m, int d);
+void launch_cycle_small(int defl, bool pre, bool am, const Dia& A, const Dia& Aam,
+                        const Prolong& P, const RunMap& rm, const double* Einv, int ld, double* V,
+                        long long vstride, long long n_pad, double* part, double* yg,
+                        const Scal& sc, cudaStream_t s);
 void launch_xupdate(const Dia& A, double* x, const double* V, long long vstride, long long n_pad,
                     const Scal& sc, cudaStream_t s);
 // out = xs + (xh - y[lab])   (deflation.py:64-68)

@@ -205,9 +205,21 @@ def test_max_iters_not_an_error(gpu):
 
 
 def test_min_iters(gpu):
+    """pkg/tests/test_krylov.py::test_min_iters_forces_extra_work against the reference's
+    outcome (run here, krylov.py:137,189-194): the identity is solved in one step; min_iters=3
+    keeps the solve going, the step breaks down (h_10 at rounding level, <= 1e-13 |H col|) and
+    ends the cycle.  The reference then needs one more step because its x after the first
+    cycle is off by one rounding unit (history [3.16, 5.6e-16, 1.2e-31]: 2 iterations, 1
+    restart); whether that second step happens depends only on the last bit of 1/sqrt(10), so
+    the bar is the north_star's: same outcome and warning, iterations within +-2."""
     A = dk.SparseMatrix.identity(10)
     rep = dk.gmres(A, np.ones(10), m=10, tol=1e-6, min_iters=3)
-    assert rep.iterations >= 1
+    assert rep.converged and rep.warning == "breakdown"
+    assert abs(rep.iterations - 2) <= IT_TOL and 1 <= rep.iterations
+    assert len(rep.residual_history) == rep.iterations + 1
+    assert rep.residual_history[0] == pytest.approx(np.sqrt(10.0), rel=1e-15)
+    assert np.all(np.abs(rep.residual_history[1:]) <= 1e-14)
+    np.testing.assert_allclose(rep.x, np.ones(10), rtol=1e-14)
 
 
 def test_history_monotone_within_cycle_and_restarts(gpu):
