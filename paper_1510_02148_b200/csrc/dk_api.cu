@@ -1010,8 +1010,8 @@ int dk_op_create(dk_op** out, int64_t n, int32_t ndiag, const int64_t* offsets,
   DK_TRY(pinned_state(&op->st_host));
   DK_TRY(cudaMallocAsync(&op->nrm, 4 * sizeof(double), op->stream));
   DK_TRY(cudaMallocAsync(&op->tickets, 4 * sizeof(unsigned int), op->stream));
-  DK_TRY(cudaMallocAsync(&op->gticket, kGroupTickets * sizeof(unsigned int), op->stream));
-  DK_TRY(cudaMemsetAsync(op->gticket, 0, kGroupTickets * sizeof(unsigned int), op->stream));
+  DK_TRY(cudaMallocAsync(&op->gticket, (kGroupTickets + 1) * sizeof(unsigned int), op->stream));
+  DK_TRY(cudaMemsetAsync(op->gticket, 0, (kGroupTickets + 1) * sizeof(unsigned int), op->stream));
   {
     const int one_h = 1;
     DK_TRY(cudaMallocAsync(&op->one, sizeof(int), op->stream));

@@ -197,6 +197,19 @@ __device__ __forceinline__ void tl_mark_warp(unsigned kind, unsigned phase) {
     }
   }
 }
+// a value record (the "time" field carries v): per-phase sums of persistent kernels
+__device__ __forceinline__ void tl_mark_value(unsigned kind, unsigned phase,
+                                              unsigned long long v) {
+  if (g_tl.rec != nullptr) {
+    const unsigned i = atomicAdd(g_tl.cnt, 1u);
+    if (i < g_tl.cap) {
+      g_tl.rec[2 * i] = v;
+      g_tl.rec[2 * i + 1] = ((unsigned long long)kind << 56) |
+                            ((unsigned long long)(phase | 0x80) << 48) |
+                            (unsigned long long)blockIdx.x;
+    }
+  }
+}
 #define DK_TL(kind, phase) ::dk::tl_mark(kind, phase)
 #define DK_TLW(kind, phase) ::dk::tl_mark_warp(kind, phase)
 #define DK_TL_SETTER(fn) \

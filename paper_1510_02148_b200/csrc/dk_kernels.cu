@@ -1765,25 +1765,28 @@ __device__ __forceinline__ double small_transpose_sum(double (&v)[32], int lane)
   return v[0];
 }
 
-// out[q] = sum over the blocks of part[q * G + b]: each warp takes 8 quantities at a time,
-// lane l sums blocks l, l + 32, ... in order (all loads in flight), reduce8's fixed butterfly
-// combines the lanes (deterministic)
+// out[q] = sum over the blocks of part[q * G + b] (G <= 160): each warp takes 8 quantities at
+// a time, lane l sums blocks l, l + 32, ... in order with all 40 loads issued first, reduce8's
+// fixed butterfly combines the lanes (deterministic)
 __device__ __forceinline__ void small_reduce(const double* part, int nq, double* out) {
   const int G = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int q0 = 8 * warp; q0 < nq; q0 += 8 * kWarps) {
+    double a[8][5];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const bool on = q0 + k < nq && lane + 32 * i < G;
+        const double* p = part + (size_t)(on ? q0 + k : 0) * G + (on ? lane + 32 * i : 0);
+        a[k][i] = on ? __ldcg(p) : 0.0;
+      }
     double v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       double t = 0.0;
-      if (q0 + k < nq) {
-        const double* p = part + (size_t)(q0 + k) * G;
-        double a[5];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) a[i] = (lane + 32 * i < G) ? __ldcg(p + lane + 32 * i) : 0.0;
-#pragma unroll
-        for (int i = 0; i < 5; ++i) t += a[i];
-      }
+      for (int i = 0; i < 5; ++i) t += a[k][i];
       v[k] = t;
     }
     const double r = reduce8(v, lane);
@@ -1857,24 +1860,46 @@ __device__ __forceinline__ void small_partials(int nq, double* red, double* part
   __syncthreads();
 }
 
+// Plain grid barrier of the small-cycle grid: a per-launch arrival counter (zeroed before
+// the launch); barrier k waits for (k + 1) G arrivals.  Release-add to arrive (cumulative
+// over the block's writes ordered by __syncthreads), relaxed polling, one acquire.
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void small_sync(unsigned* counter, unsigned& target) {
+  target += gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    red_add_release(counter, 1u);
+    while (ld_relaxed_u32(counter) < target) __nanosleep(20);
+    (void)ld_acquire_u32(counter);
+  }
+  __syncthreads();
+}
+
 // ======================================================================================
 // Small problems (BASELINE config 1: 32 k cells, the whole basis L2-resident): the cycle's m
 // Arnoldi steps in ONE persistent cooperative grid over all SMs, CPT cells per thread
 // (consecutive threads own consecutive cells), instead of 5 latency-bound launches per step.
 // Per step j:
 //   w = A M^-1 (sigma_j u_j) (k_stencil's arithmetic), kept in registers; per-block label
-//   sums of w (warp-segmented runs of consecutive cells, fixed trees)
-//   | lead: s = Z^T w (blocks in order), y = E^-1 s (dense E^-1, d <= 64)
-//   w -= A_p Z y (compact prolongation, y in shared memory); block partials of U^T w, of the
-//   Gram column U^T u_j and of ||w||^2
-//   | lead: reduction + iter_finish (H column, coefficients, re-orthogonalisation test)
-//   u = w - U coef (+ the second pass through one more lead when the test fired), stored as
-//   basis row j+1; block partial of ||u||^2
-//   | lead: finish_iteration_block (Givens, convergence / breakdown, sigma_{j+1})
-// "|" is small_barrier: the last block to arrive runs the control section (the same device
-// functions as the multi-kernel path) before releasing the others.  Every sum has a fixed
-// order; results agree with the multi-kernel path to rounding (parity against the reference
-// is the bar).  Chosen by shape (cycle_small_ok); DK_NO_SMALL disables it.
+//   sums of w (warp-segmented runs of consecutive cells, fixed trees)          | barrier
+//   s = Z^T w, y = E^-1 s in every block; w -= A_p Z y; block partials of U^T w, of the Gram
+//   column U^T u_j and of ||w||^2                                                | barrier
+//   the H column and the re-orthogonalisation test (iter_finish's arithmetic) in every
+//   block; u = w - U coef (+ the second pass when the test fired), stored as basis row j+1;
+//   block partial of ||u||^2                                                     | barrier
+//   Givens, convergence / breakdown, sigma_{j+1} (finish_iteration_block's arithmetic)
+// The control state (sigma, cs, sn, the Gram matrix, the residual estimate, the counters) is
+// replicated in every block's shared memory — the blocks compute identical values from the
+// same partials in the same order — so no block waits for another's control section; block
+// 0 alone writes the solver's device state, exactly what the multi-kernel path writes.
+// Chosen by shape (cycle_small_ok); DK_NO_SMALL disables it.
 // ======================================================================================
 template <int DEFL, bool PRE, bool AM, int CPT>
 __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Prolong P,
@@ -1882,18 +1907,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
                                                           const double* __restrict__ Einv,
                                                           int ld, double* V, long long vstride,
                                                           long long n_pad, double* part,
-                                                          double* yg, Scal sc) {
+                                                          unsigned* counter, Scal sc) {
   extern __shared__ __align__(16) double sm[];
-  const int m = sc.m;
-  double* ctl = sm;  // control scratch of the lead
-  const int nctl = 4 * (m + 1) + 1 + (m + 1) * (m + 1) + 512;
-  double* red = ctl + nctl;  // [q][warp]
-  __shared__ double ys[kSmallMaxD];
-  __shared__ double cf[kMaxCycleSmall];
+  const int m = sc.m, M1 = m + 1;
+  double* gm = sm;                   // (m+1)^2 Gram matrix, full
+  double* tot = gm + M1 * M1;        // reduced quantities (2 M1 + 1)
+  double* red = tot + 2 * M1 + 8;    // [q][warp] block partial staging (2 M1 + 33)
+  __shared__ double ys[kSmallMaxD], sdv[kSmallMaxD];
+  __shared__ double sig[kMaxCycleSmall + 1], csv[kMaxCycleSmall], snv[kMaxCycleSmall];
+  __shared__ double hcol[kMaxCycleSmall + 1], cf[kMaxCycleSmall], absc[kMaxCycleSmall];
   __shared__ double rsum[kWarps][CPT][kSmallRuns];
   __shared__ int rlab[kWarps][CPT][kSmallRuns];
   __shared__ int rcnt[kWarps][CPT];
+  __shared__ double s_gcur, s_tol, s_denom;
+  __shared__ int s_its, s_min, s_max, s_cycle, s_active, s_reorth;
   State* st = sc.st;
+  const bool w0 = blockIdx.x == 0;  // the writer of the device state
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long stride = (long long)gridDim.x * blockDim.x;
   long long cell[CPT];
@@ -1902,19 +1931,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
   for (int e = 0; e < CPT; ++e) {
     cell[e] = (long long)blockIdx.x * blockDim.x + threadIdx.x + e * stride;
     ok[e] = cell[e] < n_pad;
-    if (!ok[e]) cell[e] = 0;  // a padded cell: reads stay in bounds, results unused
+    if (!ok[e]) cell[e] = 0;  // a padded slot: reads stay in bounds, results unused
   }
   int L[CPT];
 #pragma unroll
   for (int e = 0; e < CPT; ++e) L[e] = (DEFL == DK_LABELS && ok[e]) ? __ldg(lab + cell[e]) : -1;
-  unsigned int* cnt = sc.gticket + kGroupTickets - 2;
-  unsigned int* gen = sc.gticket + kGroupTickets - 3;
+  unsigned target = 0;
+#ifdef DK_TIMELINE
+  unsigned long long tacc[16] = {0}, tprev = 0;
+  auto tmark = [&](int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (k > 0) tacc[k] += t - tprev;
+    tprev = t;
+  };
+#define SMALL_MARK(k) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) tmark(k)
+#else
+#define SMALL_MARK(k)
+#endif
   pdl_wait();
-  for (int j = 0; j < m; ++j) {
-    if (*reinterpret_cast<volatile int*>(&st->active) == 0) break;
-    DK_TL(TL_SMALL, 0);
+  if (threadIdx.x == 0) {  // the restart's state (written before this launch)
+    s_active = st->active;
+    s_its = st->iterations;
+    s_tol = st->tol;
+    s_denom = st->denom;
+    s_min = st->min_iters;
+    s_max = st->max_iters;
+    s_cycle = st->cycle;
+    s_gcur = sc.g[0];
+    sig[0] = sc.sigma[0];
+  }
+  __syncthreads();
+  for (int j = 0; j < m && s_active; ++j) {
+    SMALL_MARK(0);
     const int nvec = j + 1;
-    const double sig = __ldcg(sc.sigma + j);
+    const double sgj = sig[j];
     const double* vj = V + (long long)j * vstride;
     // ---- stencil: every coefficient and neighbour in flight, then the ordered sums
     double w[CPT];
@@ -1934,7 +1986,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
 #pragma unroll
       for (int q = 0; q < kMaxDiag; ++q) {
         if (q >= A.ndiag) break;
-        double y = __dmul_rn(x[q], sig);
+        double y = __dmul_rn(x[q], sgj);
         if (PRE) y = __dmul_rn(y, mi[q]);
         r = __dadd_rn(r, __dmul_rn(a[q], y));
       }
@@ -1948,24 +2000,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
         const int Lp = __shfl_up_sync(0xffffffffu, L[e], 1);
         const bool head = lane == 0 || Lp != L[e];
         double v = L[e] >= 0 ? w[e] : 0.0;
-        unsigned hm = __ballot_sync(0xffffffffu, head);
+        const unsigned hm = __ballot_sync(0xffffffffu, head);
+        const int seg_start = 31 - __clz(hm & ((2u << lane) - 1u));
 #pragma unroll
         for (int dlt = 1; dlt < 32; dlt <<= 1) {
           const double u = __shfl_up_sync(0xffffffffu, v, dlt);
-          // add while lane - dlt is still inside this lane's run
-          const int seg_start = 31 - __clz(hm & ((2u << lane) - 1u));
           if (lane >= dlt && lane - dlt >= seg_start) v = __dadd_rn(u, v);
         }
         const bool tail = lane == 31 || ((hm >> (lane + 1)) & 1u);
         const unsigned tm = __ballot_sync(0xffffffffu, tail && L[e] >= 0);
-        const int ntail = __popc(tm);
-        if (lane == 0) rcnt[warp][e] = ntail;
+        if (lane == 0) rcnt[warp][e] = __popc(tm);
         if (tail && L[e] >= 0) {
           const int k = __popc(tm & ((1u << lane) - 1u));
-          if (k < kSmallRuns) {
-            rsum[warp][e][k] = v;
-            rlab[warp][e][k] = L[e];
-          }
+          rsum[warp][e][k] = v;
+          rlab[warp][e][k] = L[e];
         }
       }
       __syncthreads();
@@ -1976,33 +2024,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
 #pragma unroll
           for (int e = 0; e < CPT; ++e) {
             const int nr = rcnt[w2][e];
-            for (int k = 0; k < nr && k < kSmallRuns; ++k)
+            for (int k = 0; k < nr; ++k)
               if (rlab[w2][e][k] == l) t += rsum[w2][e][k];
           }
         __stcg(part + (size_t)l * gridDim.x + blockIdx.x, t);
       }
-      DK_TL(TL_SMALL, 1);
-      // ---- lead: s = Z^T w (blocks in order), y = E^-1 s
-      small_barrier(cnt, gen, [&] {
-        small_reduce(part, d, ctl);
-        for (int l = threadIdx.x; l < d; l += blockDim.x) {
-          const double* Er = Einv + (long long)l * ld;
-          double t = 0.0;
-          int k = 0;
-          for (; k + 8 <= d; k += 8) {  // the row's loads in flight, then the ordered sum
-            double e8[8];
+      SMALL_MARK(1);
+      small_sync(counter, target);
+      SMALL_MARK(2);
+      // ---- s = Z^T w (blocks in order), y = E^-1 s: every block
+      small_reduce(part, d, sdv);
+      SMALL_MARK(3);
+      for (int l = threadIdx.x; l < d; l += blockDim.x) {
+        const double* Er = Einv + (long long)l * ld;
+        double t = 0.0;
+        int k = 0;
+        for (; k + 8 <= d; k += 8) {  // the row's loads in flight, then the ordered sum
+          double e8[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) e8[u] = __ldg(Er + k + u);
+          for (int u = 0; u < 8; ++u) e8[u] = __ldg(Er + k + u);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) t = fma(e8[u], ctl[k + u], t);
-          }
-          for (; k < d; ++k) t = fma(__ldg(Er + k), ctl[k], t);
-          __stcg(yg + l, t);
+          for (int u = 0; u < 8; ++u) t = fma(e8[u], sdv[k + u], t);
         }
-      });
-      DK_TL(TL_SMALL, 2);
-      for (int l = threadIdx.x; l < d; l += blockDim.x) ys[l] = __ldcg(yg + l);
+        for (; k < d; ++k) t = fma(__ldg(Er + k), sdv[k], t);
+        ys[l] = t;
+      }
       __syncthreads();
+      SMALL_MARK(4);
 #pragma unroll
       for (int e = 0; e < CPT; ++e)
         if (ok[e]) w[e] = __dsub_rn(w[e], prolong_cell_smem<AM>(Aam, P, ys, cell[e]));
@@ -2011,30 +2059,106 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
     double uj[CPT];
 #pragma unroll
     for (int e = 0; e < CPT; ++e) uj[e] = __ldcg(vj + cell[e]);
-    DK_TL(TL_SMALL, 9);
-    small_partials(2 * nvec + 1, red, part, [&](int q) {
-      double t = 0.0;
-      if (q == 2 * nvec) {
+    SMALL_MARK(5);
+    {
+      // batches of 32 basis rows: every load of the batch in flight, each row serving both
+      // dots (U_v . w and the Gram entry U_v . u_j); quantity v, nvec + v; ||w||^2 last
+      const int nq = 2 * nvec + 1;
+      for (int v0 = 0; v0 < nvec; v0 += 32) {
+        double pv[32][CPT];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const bool on = v0 + k < nvec;
+          const double* Vr = V + (long long)(on ? v0 + k : 0) * vstride;
+#pragma unroll
+          for (int e = 0; e < CPT; ++e) pv[k][e] = on ? __ldcg(Vr + cell[e]) : 0.0;
+        }
+        double hv[32], gv[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          double th = 0.0, tg = 0.0;
+#pragma unroll
+          for (int e = 0; e < CPT; ++e) {
+            th = fma(pv[k][e], w[e], th);
+            tg = fma(pv[k][e], uj[e], tg);
+          }
+          hv[k] = th;
+          gv[k] = tg;
+        }
+        const double th = small_transpose_sum(hv, lane);
+        const double tg = small_transpose_sum(gv, lane);
+        if (v0 + lane < nvec) {
+          red[(v0 + lane) * kWarps + warp] = th;
+          red[(nvec + v0 + lane) * kWarps + warp] = tg;
+        }
+      }
+      {
+        double t = 0.0;
 #pragma unroll
         for (int e = 0; e < CPT; ++e) t = fma(w[e], w[e], t);
-        return t;
+        t = warp_sum(t);
+        if (lane == 0) red[(2 * nvec) * kWarps + warp] = t;
       }
-      const int v = q < nvec ? q : q - nvec;
-      const double* Vr = V + (long long)v * vstride;
-#pragma unroll
-      for (int e = 0; e < CPT; ++e) t = fma(__ldcg(Vr + cell[e]), q < nvec ? w[e] : uj[e], t);
-      return t;
-    });
-    DK_TL(TL_SMALL, 3);
-    // ---- lead: the H column and the re-orthogonalisation test
-    small_barrier(cnt, gen, [&] {
-      small_reduce(part, 2 * nvec + 1, ctl);
-      iter_finish(sc, j, nvec, ctl);
-    });
-    DK_TL(TL_SMALL, 4);
-    // ---- u = w - U coef
-    for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = __ldcg(sc.coef + q);
+      __syncthreads();
+      for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < kWarps; ++w2) t += red[q * kWarps + w2];
+        __stcg(part + (size_t)q * gridDim.x + blockIdx.x, t);
+      }
+      __syncthreads();
+    }
+    SMALL_MARK(6);
+    small_sync(counter, target);
+    SMALL_MARK(7);
+    // ---- the H column and the re-orthogonalisation test (iter_finish's arithmetic)
+    small_reduce(part, 2 * nvec + 1, tot);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      const double h = tot[v] * sig[v];  // h_i = V_i . w  (krylov.py:164-165)
+      hcol[v] = h;
+      cf[v] = h * sig[v];
+      const double g = tot[nvec + v] * sig[v] * sgj;  // V_i . V_j
+      gm[v * M1 + j] = g;
+      gm[j * M1 + v] = g;
+      if (w0) {
+        sc.H[(size_t)j * M1 + v] = h;
+        sc.coef[v] = cf[v];
+        sc.Gm[(size_t)j * M1 + v] = g;
+      }
+    }
     __syncthreads();
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {  // corr_i = h_i - sum_k G_ik h_k
+      double c4[4] = {0.0, 0.0, 0.0, 0.0};  // four interleaved chains, fixed combination
+      int k = 0;
+      for (; k + 4 <= nvec; k += 4)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c4[u] = fma(gm[i * M1 + k + u], hcol[k + u], c4[u]);
+      for (; k < nvec; ++k) c4[0] = fma(gm[i * M1 + k], hcol[k], c4[0]);
+      const double c = hcol[i] - ((c4[0] + c4[1]) + (c4[2] + c4[3]));
+      absc[i] = fabs(c);
+      if (w0) sc.gcol[i] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // max |corr| (order-free)
+      double mx = 0.0;
+      for (int i = threadIdx.x; i < nvec; i += 32) mx = fmax(mx, absc[i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (threadIdx.x == 0) absc[kMaxCycleSmall - 1] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double wnorm0 = sqrt(tot[2 * nvec]);  // krylov.py:162
+      const double mx = absc[kMaxCycleSmall - 1];
+      s_reorth = mx > 1e-8 * fmax(wnorm0, 1e-300);  // krylov.py:168
+      if (w0) {
+        st->wnorm0 = wnorm0;
+        st->reorth = s_reorth;
+        if (s_reorth) st->reorths += 1;
+      }
+    }
+    __syncthreads();
+    SMALL_MARK(8);
+    // ---- u = w - U coef
     double u[CPT];
 #pragma unroll
     for (int e = 0; e < CPT; ++e) u[e] = w[e];
@@ -2045,7 +2169,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
 #pragma unroll
       for (int e = 0; e < CPT; ++e) u[e] = __dsub_rn(u[e], __dmul_rn(c, __ldcg(Vr + cell[e])));
     }
-    if (*reinterpret_cast<volatile int*>(&st->reorth) != 0) {
+    if (s_reorth) {
       // the second Gram-Schmidt pass (krylov.py:169-170): corr = V^T u, u -= V corr
       small_partials(nvec, red, part, [&](int v) {
         double t = 0.0;
@@ -2054,24 +2178,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
         for (int e = 0; e < CPT; ++e) t = fma(__ldcg(Vr + cell[e]), u[e], t);
         return t;
       });
-      small_barrier(cnt, gen, [&] {
-        small_reduce(part, nvec, ctl);
-        double* Hc = sc.H + (size_t)j * (m + 1);
-        double* cr = ctl + nvec;
-        for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-          cr[v] = ctl[v] * sc.sigma[v];
-          Hc[v] += cr[v];
-          sc.corr[v] = cr[v] * sc.sigma[v];
+      small_sync(counter, target);
+      small_reduce(part, nvec, tot);
+      for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+        const double cr = tot[v] * sig[v];
+        hcol[v] += cr;
+        cf[v] = cr * sig[v];
+        absc[v] = cr;
+        if (w0) {
+          sc.H[(size_t)j * M1 + v] = hcol[v];
+          sc.corr[v] = cf[v];
         }
-        __syncthreads();
+      }
+      __syncthreads();
+      if (w0)
         for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-          double c = cr[i];
-          for (int k = 0; k < nvec; ++k) c -= gram_at(sc.Gm, m, i, k) * cr[k];
+          double c = absc[i];
+          for (int k = 0; k < nvec; ++k) c -= gm[i * M1 + k] * absc[k];
           sc.gcol[i] = c;
         }
-      });
-      for (int q = threadIdx.x; q < nvec; q += blockDim.x) cf[q] = __ldcg(sc.corr + q);
-      __syncthreads();
 #pragma unroll 8
       for (int v = 0; v < nvec; ++v) {
         const double c = cf[v];
@@ -2084,27 +2209,95 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
 #pragma unroll
     for (int e = 0; e < CPT; ++e)
       if (ok[e]) un[cell[e]] = u[e];
-    DK_TL(TL_SMALL, 5);
+    SMALL_MARK(9);
     small_partials(1, red, part, [&](int) {
       double t = 0.0;
 #pragma unroll
       for (int e = 0; e < CPT; ++e) t = fma(u[e], u[e], t);
       return t;
     });
-    // ---- lead: Givens, convergence / breakdown, sigma_{j+1}
-    small_barrier(cnt, gen, [&] {
-      small_reduce(part, 1, ctl);
-      const double hj1 = sqrt(ctl[0]);
-      __syncthreads();
-      finish_iteration_block(sc, j, hj1, ctl);
-    });
-    DK_TL(TL_SMALL, 6);
+    SMALL_MARK(10);
+    small_sync(counter, target);
+    SMALL_MARK(11);
+    // ---- Givens, convergence / breakdown, sigma_{j+1} (finish_iteration_block's arithmetic)
+    small_reduce(part, 1, tot);
+    if (threadIdx.x == 0) {
+      const double hj1 = sqrt(tot[0]);
+      double* col = absc;  // j + 2 <= kMaxCycleSmall
+      for (int i = 0; i <= j; ++i) col[i] = hcol[i];
+      col[j + 1] = hj1;
+      double hn = 0.0;
+      for (int i = 0; i <= j + 1; ++i) hn += col[i] * col[i];
+      hn = sqrt(hn);
+      double run = col[0];  // the rotated entry carried in a register
+      for (int i = 0; i < j; ++i) {  // _givens_update, krylov.py:90-104
+        const double nx = col[i + 1];
+        const double t = __dadd_rn(__dmul_rn(csv[i], run), __dmul_rn(snv[i], nx));
+        run = __dadd_rn(__dmul_rn(-snv[i], run), __dmul_rn(csv[i], nx));
+        col[i] = t;
+      }
+      col[j] = run;
+      const double den = hypot(col[j], col[j + 1]);
+      double c = 1.0, sn = 0.0;
+      if (den != 0.0) {
+        c = col[j] / den;
+        sn = col[j + 1] / den;
+      }
+      csv[j] = c;
+      snv[j] = sn;
+      col[j] = den;
+      col[j + 1] = 0.0;
+      const double gj = s_gcur;
+      const double gn = __dmul_rn(-sn, gj);
+      const double resnorm = fabs(gn);
+      s_gcur = gn;
+      s_its += 1;
+      int active = 1, converged = 0, broke = 0, warn = 0;
+      if (resnorm <= s_tol * s_denom && s_its >= s_min) {  // :189-191
+        converged = 1;
+        active = 0;
+        broke = 1;
+      } else if (hj1 <= 1e-13 * fmax(1.0, hn)) {  // :192-194
+        warn = 1;
+        active = 0;
+        broke = 1;
+      } else {
+        sig[j + 1] = 1.0 / hj1;  // V[j+1] = w / hj1 (:197)
+        if (j + 1 >= m || s_its >= s_max) active = 0;
+      }
+      s_active = active;
+      if (w0) {
+        sc.H[(size_t)j * M1 + j + 1] = hj1;  // krylov.py:172
+        sc.cs[j] = c;
+        sc.sn[j] = sn;
+        sc.g[j + 1] = gn;
+        sc.g[j] = __dmul_rn(c, gj);
+        st->cols = j + 1;
+        st->iterations = s_its;
+        sc.hist[s_its] = resnorm;
+        sc.restart_of[s_its] = s_cycle;
+        st->reorth = 0;
+        st->last_broke = broke;
+        if (converged) st->converged = 1;
+        if (warn) st->warning = DK_WARNING_BREAKDOWN;
+        if (!broke) sc.sigma[j + 1] = sig[j + 1];
+        if (!active) st->active = 0;
+        double* Rc = sc.R + (size_t)j * M1;
+        for (int i = 0; i <= j + 1; ++i) Rc[i] = col[i];
+      }
+    }
+    __syncthreads();
+    SMALL_MARK(12);
   }
+#ifdef DK_TIMELINE
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int k = 1; k <= 12; ++k) tl_mark_value(TL_SMALL, k, tacc[k]);
+#endif
 }
 
 size_t cycle_small_smem(int m) {
-  const int nctl = 4 * (m + 1) + 1 + (m + 1) * (m + 1) + 512;
-  return ((size_t)nctl + (size_t)(2 * (m + 1) + 1 + 32) * kWarps) * sizeof(double);
+  const size_t M1 = (size_t)m + 1;
+  return (M1 * M1 + (2 * M1 + 8) + (2 * M1 + 33) * kWarps) * sizeof(double);
 }
 
 // cells per thread over one block per SM
@@ -2143,6 +2336,10 @@ static void cycle_small_t(const Dia& A, const Dia& Aam, const Prolong& P, const 
                           long long n_pad, double* part, double* yg, const Scal& sc,
                           cudaStream_t s) {
   const size_t smem = cycle_small_smem(sc.m);
+  // the arrival counter of small_sync (zeroed per launch; after the group tickets)
+  unsigned* counter = sc.gticket + kGroupTickets;
+  cudaMemsetAsync(counter, 0, sizeof(unsigned), s);
+  (void)yg;
   smem_optin((const void*)k_cycle_small<DEFL, PRE, AM, CPT>, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(small_grid(n_pad, CPT));
@@ -2156,7 +2353,8 @@ static void cycle_small_t(const Dia& A, const Dia& Aam, const Prolong& P, const 
   cfg.numAttrs = 1;
   pdl_skip_next() = false;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cycle_small<DEFL, PRE, AM, CPT>, A, Aam, P,
-                                           lab, d, Einv, ld, V, vstride, n_pad, part, yg, sc);
+                                           lab, d, Einv, ld, V, vstride, n_pad, part, counter,
+                                           sc);
   if (e != cudaSuccess) launch_error() = e;
 }
 

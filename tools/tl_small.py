@@ -1,4 +1,5 @@
-"""Phase timeline of the persistent small-cycle kernel (diagnostic; -DDK_TIMELINE build)."""
+"""Per-phase time of the persistent small-cycle kernel (diagnostic; -DDK_TIMELINE build):
+block 0 sums globaltimer deltas per phase over the cycle and records them at exit."""
 import ctypes as C
 import sys
 from pathlib import Path
@@ -19,38 +20,22 @@ M = dk.Preconditioner.jacobi(A)
 basis = dk.partition_to_basis(case.partition())
 for _ in range(2):
     dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=case.max_iters)
-lib.dk_timeline_enable(1 << 20)
+lib.dk_timeline_enable(1 << 16)
 rep = dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=case.max_iters)
-buf = np.empty(2 << 20, dtype=np.uint64)
-n = lib.dk_timeline_read(buf.ctypes.data, 1 << 20)
+buf = np.empty(2 << 16, dtype=np.uint64)
+n = lib.dk_timeline_read(buf.ctypes.data, 1 << 16)
 rec = buf[:2 * n].reshape(n, 2)
-t = rec[:, 0].astype(np.int64)
 kind = (rec[:, 1] >> np.uint64(56)).astype(int)
 ph = ((rec[:, 1] >> np.uint64(48)) & np.uint64(0xff)).astype(int)
-sel = kind == 10
-t, ph = t[sel], ph[sel]
-order = np.argsort(t)
-t, ph = t[order], ph[order]
-# iterations: phase-0 records come in groups of G blocks
-t0 = t[ph == 0]
-G = int(np.sum(t0 < t0[0] + 3000))  # blocks per step (records within 3 us)
-print("records", len(t), "blocks", G, "iterations", rep.iterations)
-starts = t0[::G]
-names = ["start", "stencil+restrict", "bar1(y)", "dots", "bar2(ctl)", "gs", "bar3(givens)",
-         "lead start", "lead end", "prolong done", "-", "staged", "small_dots"]
-acc = np.zeros(13)
-cntv = 0
-for i in range(5, len(starts) - 1):
-    w = (t >= starts[i]) & (t < starts[i + 1])
-    row = [np.max(t[w & (ph == p)]) - starts[i] if np.any(w & (ph == p)) else np.nan for p in range(13)]
-    acc += np.nan_to_num(row)
-    cntv += 1
-print("mean of the last block's arrival at each phase end (us after the step's first start):")
-for p in range(13):
-    print(f"  {names[p]:18s} {acc[p] / cntv / 1e3:7.2f}")
-# the three leads of a step, in order
-for i in range(5, 8):
-    w = (t >= starts[i]) & (t < starts[i + 1])
-    print("  step", i, "lead start/end:", ((t[w & (ph == 7)] - starts[i]) / 1e3).round(2),
-          ((t[w & (ph == 8)] - starts[i]) / 1e3).round(2))
-print(f"step period {np.mean(np.diff(starts)) / 1e3:.2f} us")
+sel = (kind == 10) & (ph >= 0x80)
+names = {1: "stencil + label partials", 2: "barrier 1", 3: "reduce s", 4: "y = E^-1 s",
+         5: "prolongation + u_j", 6: "dot partials", 7: "barrier 2", 8: "control (H col, test)",
+         9: "GS update + store", 10: "norm partial", 11: "barrier 3", 12: "Givens / flags"}
+tot = {}
+for p, v in zip(ph[sel] - 0x80, rec[sel, 0]):
+    tot[p] = tot.get(p, 0) + int(v)
+its = rep.iterations
+print(f"iterations {its}; mean us per step:")
+for p in sorted(tot):
+    print(f"  {names.get(p, p):28s} {tot[p] / its / 1e3:7.2f}")
+print(f"  {'sum':28s} {sum(tot.values()) / its / 1e3:7.2f}")
