@@ -1920,7 +1920,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
   __shared__ int rlab[kWarps][CPT][kSmallRuns];
   __shared__ int rcnt[kWarps][CPT];
   __shared__ double s_gcur, s_tol, s_denom;
-  __shared__ int s_its, s_min, s_max, s_cycle, s_active, s_reorth;
+  __shared__ int s_its, s_min, s_max, s_cycle, s_active, s_reorth, s_broke, s_final;
+  __shared__ double s_hn;
   State* st = sc.st;
   const bool w0 = blockIdx.x == 0;  // the writer of the device state
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1962,6 +1963,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
     s_gcur = sc.g[0];
     sig[0] = sc.sigma[0];
   }
+  if (threadIdx.x == 0) s_final = s_active;
   __syncthreads();
   for (int j = 0; j < m && s_active; ++j) {
     SMALL_MARK(0);
@@ -2017,6 +2019,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
         }
       }
       __syncthreads();
+      if (!s_final) break;  // the previous step's convergence test (speculative stencil)
       // block partial of label l: the runs in (warp, slot, run) order
       for (int l = threadIdx.x; l < d; l += blockDim.x) {
         double t = 0.0;
@@ -2054,6 +2057,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
 #pragma unroll
       for (int e = 0; e < CPT; ++e)
         if (ok[e]) w[e] = __dsub_rn(w[e], prolong_cell_smem<AM>(Aam, P, ys, cell[e]));
+    }
+    if (DEFL != DK_LABELS) {
+      __syncthreads();
+      if (!s_final) break;  // the previous step's convergence test (speculative stencil)
     }
     // ---- block partials: U^T w, U^T u_j, ||w||^2
     double uj[CPT];
@@ -2219,19 +2226,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
     SMALL_MARK(10);
     small_sync(counter, target);
     SMALL_MARK(11);
-    // ---- Givens, convergence / breakdown, sigma_{j+1} (finish_iteration_block's arithmetic)
+    // ---- Givens, convergence / breakdown, sigma_{j+1} (finish_iteration_block's arithmetic).
+    // The breakdown test and sigma_{j+1} come first; the block then starts the next step's
+    // stencil while thread 0 finishes the rotations and the convergence test, which the next
+    // step checks before its first global write (the same decision in every block).
     small_reduce(part, 1, tot);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // |H column| for the breakdown test (warp 0)
       const double hj1 = sqrt(tot[0]);
-      double* col = absc;  // j + 2 <= kMaxCycleSmall
-      for (int i = 0; i <= j; ++i) col[i] = hcol[i];
-      col[j + 1] = hj1;
       double hn = 0.0;
-      for (int i = 0; i <= j + 1; ++i) hn += col[i] * col[i];
-      hn = sqrt(hn);
-      double run = col[0];  // the rotated entry carried in a register
+      for (int i = threadIdx.x; i <= j; i += 32) hn = fma(hcol[i], hcol[i], hn);
+      hn = warp_sum(hn);
+      if (threadIdx.x == 0) {
+        hn = sqrt(fma(hj1, hj1, hn));
+        s_hn = hn;
+        absc[j + 1] = hj1;
+        s_broke = hj1 <= 1e-13 * fmax(1.0, hn);  // :192-194 (convergence is tested first)
+        if (!s_broke) sig[j + 1] = 1.0 / hj1;     // V[j+1] = w / hj1 (:197)
+        s_active = !s_broke && j + 1 < m && s_its + 1 < s_max;  // provisional
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double hj1 = absc[j + 1];
+      double* col = absc;  // the rotated column (j + 2 <= kMaxCycleSmall)
+      double run = hcol[0];  // the rotated entry carried in a register
       for (int i = 0; i < j; ++i) {  // _givens_update, krylov.py:90-104
-        const double nx = col[i + 1];
+        const double nx = hcol[i + 1];
         const double t = __dadd_rn(__dmul_rn(csv[i], run), __dmul_rn(snv[i], nx));
         run = __dadd_rn(__dmul_rn(-snv[i], run), __dmul_rn(csv[i], nx));
         col[i] = t;
@@ -2257,15 +2277,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
         converged = 1;
         active = 0;
         broke = 1;
-      } else if (hj1 <= 1e-13 * fmax(1.0, hn)) {  // :192-194
+      } else if (s_broke) {  // :192-194
         warn = 1;
         active = 0;
         broke = 1;
-      } else {
-        sig[j + 1] = 1.0 / hj1;  // V[j+1] = w / hj1 (:197)
-        if (j + 1 >= m || s_its >= s_max) active = 0;
+      } else if (j + 1 >= m || s_its >= s_max) {
+        active = 0;
       }
-      s_active = active;
       if (w0) {
         sc.H[(size_t)j * M1 + j + 1] = hj1;  // krylov.py:172
         sc.cs[j] = c;
@@ -2282,11 +2300,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
         if (warn) st->warning = DK_WARNING_BREAKDOWN;
         if (!broke) sc.sigma[j + 1] = sig[j + 1];
         if (!active) st->active = 0;
-        double* Rc = sc.R + (size_t)j * M1;
-        for (int i = 0; i <= j + 1; ++i) Rc[i] = col[i];
       }
+      s_final = active;
     }
-    __syncthreads();
+    if (w0 && threadIdx.x < 32) {  // the rotated column (warp 0, after its lane 0 formed it)
+      __syncwarp();
+      double* Rc = sc.R + (size_t)j * M1;
+      for (int i = threadIdx.x; i <= j + 1; i += 32) Rc[i] = absc[i];
+    }
     SMALL_MARK(12);
   }
 #ifdef DK_TIMELINE
