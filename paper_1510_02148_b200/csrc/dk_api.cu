@@ -1861,7 +1861,12 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   cudaEventCreate(&e1);
   cudaEventRecord(e0, op->stream);
   // stencil (+ restrict + E^-1 s; dense: one multi-dot)
-  const int coarse_launches = c ? (c->dense ? 2 : (c->sym || c->prof) ? 4 : 3) : 1;
+  const int coarse_launches =
+      !c ? 1
+         : c->dense ? 2
+         : c->prof  ? 2 + tgemv_launches(c->tg1) + tgemv_launches(c->tg2)
+         : c->sym   ? 4
+                    : 3;
   // restart (stencil chain + projection), m x (stencil chain, projection, update [+ the
   // separate second pass]), cycle end, x update
   const int per_cycle_launches =

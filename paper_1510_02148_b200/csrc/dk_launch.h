@@ -262,6 +262,8 @@ void free_stream(TileGemv& g, cudaStream_t s);
 // y[scatter ? scatter[i] : i] = (sum over the stream's tiles) for rows i < d
 void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,
                   const int* gate, cudaStream_t s);
+// kernels one launch_tgemv issues (1: spinning finisher; 2: NOSPIN pass + k_tg_finish)
+int tgemv_launches(const TileGemv& g);
 // f[r] = first nonzero column of row r (<= r) of a d x d matrix (device)
 void launch_row_first_nz(const double* X, int d, int ld, int* f, cudaStream_t s);
 

@@ -774,7 +774,9 @@ static bool tg_spin_ok(unsigned grid, size_t smem) {
   const int dev = current_device();
   if (!init[dev]) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tgemv<KW, KS, TRANS, false>, KW * 32,
+    // the occupancy query needs the shared-memory opt-in first (0 blocks otherwise)
+    if (smem_optin((const void*)k_tgemv<KW, KS, TRANS, false>, smem) != 0 ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tgemv<KW, KS, TRANS, false>, KW * 32,
                                                       smem) != cudaSuccess) {
       cudaGetLastError();
       b = 0;
@@ -823,6 +825,26 @@ static void launch_tg(const TileGemv& g, const double* x, double* y, const int* 
     launch_tg_t<KW, KS, true>(g, x, y, scatter, d, gate, s, grid, smem, wp);
   else
     launch_tg_t<KW, KS, false>(g, x, y, scatter, d, gate, s, grid, smem, wp);
+}
+
+// kernels one launch_tgemv issues: 1 (spinning finisher) or 2 (NOSPIN pass + k_tg_finish)
+template <int KW, int KS>
+static int tg_launches_t(const TileGemv& g) {
+  const size_t smem = (size_t)KW * KS * kPTileBytes;
+  const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
+  const bool spin = g.trans ? tg_spin_ok<KW, KS, true>(grid, smem)
+                            : tg_spin_ok<KW, KS, false>(grid, smem);
+  return spin || g.nsplit == 0 ? 1 : 2;
+}
+int tgemv_launches(const TileGemv& g) {
+  switch (tgemv_cfg()) {
+    case 0: return tg_launches_t<12, 2>(g);
+    case 1: return tg_launches_t<16, 1>(g);
+    case 3: return tg_launches_t<4, 6>(g);
+    case 4: return tg_launches_t<8, 2>(g);
+    case 5: return tg_launches_t<6, 2>(g);
+    default: return tg_launches_t<8, 3>(g);
+  }
 }
 
 void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scatter, int d,

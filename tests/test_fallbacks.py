@@ -36,6 +36,7 @@ M = dk.Preconditioner.jacobi(A)
 basis = dk.partition_to_basis(case.partition())
 rep = dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=case.max_iters)
 print(json.dumps({{"iters": rep.iterations, "relres": rep.final_relres,
+                  "launches": rep.kernel_launches,
                   "x": hashlib.sha256(np.ascontiguousarray(rep.x).tobytes()).hexdigest(),
                   "hist": hashlib.sha256(np.asarray(rep.residual_history).tobytes()).hexdigest()}}))
 """
@@ -53,7 +54,11 @@ def _run(cfg, env_extra):
 @pytest.mark.parametrize("cfg", [1, 3])
 def test_fallbacks_bitwise(gpu, cfg):
     ref = _run(cfg, {})
+    launches = ref.pop("launches")
     for extra in ({"DK_NO_SPIN": "1"},
                   {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"}):
         got = _run(cfg, extra)
+        got_launches = got.pop("launches")
         assert got == ref, (extra, got, ref)
+        if cfg == 3:  # the default path is the spinning one (one launch per tile pass)
+            assert got_launches > launches, (extra, got_launches, launches)
