@@ -1192,6 +1192,53 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
       __syncthreads();
       const long long c0 = ch * kChunk;
       const unsigned long long pol = l2_evict_first();
+#ifndef DK_K4_SINGLE
+      // two items per round (16 loads per lane in flight), each reduced as before
+      for (int it = warp; it < 4 * nvec; it += 2 * kWarps) {
+        const int it2 = it + kWarps;
+        const bool two = it2 < 4 * nvec;
+        const int v = it >> 2, qtr = it & 3, v2 = it2 >> 2;
+        const double* Vr = V + (long long)v * vstride + c0 + 512 * qtr + 2 * lane;
+        const double* Vr2 = V + (long long)(two ? v2 : v) * vstride + c0 + 512 * qtr + 2 * lane;
+        double2 p[8], p2[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p[i] = ld2_stream(Vr + 64 * i, pol);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          p2[i] = two ? ld2_stream(Vr2 + 64 * i, pol) : make_double2(0.0, 0.0);
+        double ah = 0.0, ag = 0.0, ah2 = 0.0, ag2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = 256 * qtr + lane + 32 * i;
+          const double2 ww = sw2[e];
+          ah = fma(p[i].x, ww.x, ah);
+          ah = fma(p[i].y, ww.y, ah);
+          ah2 = fma(p2[i].x, ww.x, ah2);
+          ah2 = fma(p2[i].y, ww.y, ah2);
+          if (GRAM) {
+            const double2 gg = sv2[e];
+            ag = fma(p[i].x, gg.x, ag);
+            ag = fma(p[i].y, gg.y, ag);
+            ag2 = fma(p2[i].x, gg.x, ag2);
+            ag2 = fma(p2[i].y, gg.y, ag2);
+          }
+        }
+        ah = warp_sum(ah);
+        ah2 = warp_sum(ah2);
+        if (GRAM) {
+          ag = warp_sum(ag);
+          ag2 = warp_sum(ag2);
+        }
+        if (lane == 0) {
+          red[v * kWarps + warp] += ah;
+          if (GRAM) red[(nvec + v) * kWarps + warp] += ag;
+          if (two) {
+            red[v2 * kWarps + warp] += ah2;
+            if (GRAM) red[(nvec + v2) * kWarps + warp] += ag2;
+          }
+        }
+      }
+#else
       for (int it = warp; it < 4 * nvec; it += kWarps) {
         const int v = it >> 2, qtr = it & 3;
         const double* Vr = V + (long long)v * vstride + c0 + 512 * qtr + 2 * lane;
@@ -1218,6 +1265,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_project(Dia A, Prolong P,
           if (GRAM) red[(nvec + v) * kWarps + warp] += ag;
         }
       }
+#endif
       __syncthreads();  // the next chunk reuses s_w / s_vj
     }
   }
