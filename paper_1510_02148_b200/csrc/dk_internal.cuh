@@ -125,6 +125,14 @@ inline bool& pdl_skip_next() {
   return f;
 }
 
+// set before a launch: the grid's blocks wait on one another, so it is launched cooperative
+// (all blocks co-resident or the launch fails — never a partly resident grid that spins
+// while another solve holds the SMs)
+inline bool& coop_next() {
+  static thread_local bool f = false;
+  return f;
+}
+
 // set before a launch: an L2 access-policy window (persisting set-aside) for that launch
 inline const cudaAccessPolicyWindow*& access_window_next() {
   static thread_local const cudaAccessPolicyWindow* w = nullptr;
@@ -139,8 +147,13 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
+  if (coop_next()) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   if (!pdl_skip_next()) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
@@ -155,6 +168,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.numAttrs = na;
   pdl_skip_next() = false;
   access_window_next() = nullptr;
+  coop_next() = false;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) launch_error() = e;
   return e;

@@ -2489,6 +2489,7 @@ void launch_gs(bool reorth, const double* w_in, double* u_out, const double* V, 
     launch_pdl(k_gs<true>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
                n_pad, part, G, sc, j, gate, 0, (const unsigned*)nullptr);
   else
+    if (fuse && !getenv("DK_NO_COOP")) coop_next() = true;  // the fused pass's grid barrier
     launch_pdl(k_gs<false>, dim3(G), dim3(kThreads), smem, s, w_in, u_out, V, vstride, nvec,
                n_pad, part, G, sc, j, gate, fuse ? 1 : 0,
                (const unsigned*)(fuse && sc.post != nullptr ? sc.post + (sc.m + 1) + j

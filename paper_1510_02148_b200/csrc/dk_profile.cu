@@ -795,6 +795,7 @@ static void launch_tg_t(const TileGemv& g, const double* x, double* y, const int
   if (win) access_window_next() = win;
   if (spin) {
     smem_optin((const void*)k_tgemv<KW, KS, TRANS, false>, smem);
+    if (!getenv("DK_NO_COOP")) coop_next() = true;  // finishers wait on other blocks
     launch_pdl(k_tgemv<KW, KS, TRANS, false>, dim3(grid), dim3(KW * 32), smem, s, g, x, y,
                scatter, d, gate);
     return;

@@ -7,6 +7,8 @@ environment switches (read once per process, so each variant runs in a subproces
   DK_NO_SPIN     tile GEMV pieces all go to slots, k_tg_finish sums them after the grid
   DK_NO_GS_FUSE  the second Gram-Schmidt pass as separate launches
   DK_NO_EARLY    no early start of the stencil / k_gs on published partials
+  DK_NO_COOP     the spinning grids launched without the cooperative attribute (by default
+                 they are cooperative: all blocks co-resident or the launch fails)
 Config 3 uses the nested-dissection tile streams (the spinning finisher) and its x is
 compared bitwise; config 1 checks the small-d coarse paths.
 """
@@ -56,9 +58,10 @@ def test_fallbacks_bitwise(gpu, cfg):
     ref = _run(cfg, {})
     launches = ref.pop("launches")
     for extra in ({"DK_NO_SPIN": "1"},
-                  {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"}):
+                  {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"},
+                  {"DK_NO_COOP": "1"}):
         got = _run(cfg, extra)
         got_launches = got.pop("launches")
         assert got == ref, (extra, got, ref)
-        if cfg == 3:  # the default path is the spinning one (one launch per tile pass)
+        if cfg == 3 and "DK_NO_SPIN" in extra:  # the default path spins (one launch a pass)
             assert got_launches > launches, (extra, got_launches, launches)
