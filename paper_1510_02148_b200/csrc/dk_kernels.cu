@@ -1987,7 +1987,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
   for (int e = 0; e < CPT; ++e) L[e] = (DEFL == DK_LABELS && ok[e]) ? __ldg(lab + cell[e]) : -1;
   unsigned target = 0;
 #ifdef DK_TIMELINE
-  unsigned long long tacc[16] = {0}, tprev = 0;
+  unsigned long long tacc[24] = {0}, tprev = 0;
   auto tmark = [&](int k) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -2167,6 +2167,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
     SMALL_MARK(7);
     // ---- the H column and the re-orthogonalisation test (iter_finish's arithmetic)
     small_reduce(part, 2 * nvec + 1, tot);
+    SMALL_MARK(13);
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
       const double h = tot[v] * sig[v];  // h_i = V_i . w  (krylov.py:164-165)
       hcol[v] = h;
@@ -2181,6 +2182,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
       }
     }
     __syncthreads();
+    SMALL_MARK(14);
     for (int i = threadIdx.x; i < nvec; i += blockDim.x) {  // corr_i = h_i - sum_k G_ik h_k
       double c4[4] = {0.0, 0.0, 0.0, 0.0};  // four interleaved chains, fixed combination
       int k = 0;
@@ -2193,6 +2195,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
       if (w0) sc.gcol[i] = c;
     }
     __syncthreads();
+    SMALL_MARK(15);
     if (threadIdx.x < 32) {  // max |corr| (order-free)
       double mx = 0.0;
       for (int i = threadIdx.x; i < nvec; i += 32) mx = fmax(mx, absc[i]);
@@ -2279,6 +2282,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
     // stencil while thread 0 finishes the rotations and the convergence test, which the next
     // step checks before its first global write (the same decision in every block).
     small_reduce(part, 1, tot);
+    SMALL_MARK(16);
     if (threadIdx.x < 32) {  // |H column| for the breakdown test (warp 0)
       const double hj1 = sqrt(tot[0]);
       double hn = 0.0;
@@ -2294,6 +2298,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
       }
     }
     __syncthreads();
+    SMALL_MARK(17);
     if (threadIdx.x == 0) {
       const double hj1 = absc[j + 1];
       double* col = absc;  // the rotated column (j + 2 <= kMaxCycleSmall)
@@ -2360,7 +2365,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cycle_small(Dia A, Dia Aam, Pro
   }
 #ifdef DK_TIMELINE
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int k = 1; k <= 12; ++k) tl_mark_value(TL_SMALL, k, tacc[k]);
+    for (int k = 1; k <= 20; ++k) tl_mark_value(TL_SMALL, k, tacc[k]);
 #endif
 }
 
@@ -2372,8 +2377,9 @@ size_t cycle_small_smem(int m) {
 // cells per thread over one block per SM
 static int small_cpt(long long n_pad) {
   const long long threads = (long long)num_sms() * kThreads;
+  static const int force = getenv("DK_SMALL_CPT") ? atoi(getenv("DK_SMALL_CPT")) : 0;
   for (int c = 1; c <= 4; c <<= 1)
-    if ((long long)c * threads >= n_pad) return c;
+    if ((long long)c * threads >= n_pad) return (force > c && force <= 4) ? force : c;
   return 0;
 }
 

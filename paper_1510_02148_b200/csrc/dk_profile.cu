@@ -725,13 +725,13 @@ void free_stream(TileGemv& g, cudaStream_t s) {
 }
 
 // (warps per CTA, stages per warp) of k_tgemv; DK_TG_CFG picks one (set-up and launch agree)
-static const int kTgCfg[][2] = {{12, 2}, {16, 1}, {8, 3}, {4, 6}, {8, 2}, {6, 2}};
+static const int kTgCfg[][2] = {{12, 2}, {16, 1}, {8, 3}, {4, 6}, {8, 2}, {6, 2}, {4, 3}, {4, 2}};
 int tgemv_cfg() {
   static int c = -1;
   if (c < 0) {
     const char* e = getenv("DK_TG_CFG");
     c = e ? atoi(e) : 2;
-    if (c < 0 || c > 5) c = 2;
+    if (c < 0 || c > 7) c = 2;
   }
   return c;
 }
@@ -844,6 +844,8 @@ int tgemv_launches(const TileGemv& g) {
     case 3: return tg_launches_t<4, 6>(g);
     case 4: return tg_launches_t<8, 2>(g);
     case 5: return tg_launches_t<6, 2>(g);
+    case 6: return tg_launches_t<4, 3>(g);
+    case 7: return tg_launches_t<4, 2>(g);
     default: return tg_launches_t<8, 3>(g);
   }
 }
@@ -855,6 +857,8 @@ void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scat
     case 3: launch_tg<4, 6>(g, x, y, scatter, d, gate, s); break;
     case 4: launch_tg<8, 2>(g, x, y, scatter, d, gate, s); break;
     case 5: launch_tg<6, 2>(g, x, y, scatter, d, gate, s); break;
+    case 6: launch_tg<4, 3>(g, x, y, scatter, d, gate, s); break;
+    case 7: launch_tg<4, 2>(g, x, y, scatter, d, gate, s); break;
     case 0: launch_tg<12, 2>(g, x, y, scatter, d, gate, s); break;
     default: launch_tg<8, 3>(g, x, y, scatter, d, gate, s); break;
   }

@@ -30,12 +30,14 @@ ph = ((rec[:, 1] >> np.uint64(48)) & np.uint64(0xff)).astype(int)
 sel = (kind == 10) & (ph >= 0x80)
 names = {1: "stencil + label partials", 2: "barrier 1", 3: "reduce s", 4: "y = E^-1 s",
          5: "prolongation + u_j", 6: "dot partials", 7: "barrier 2", 8: "control (H col, test)",
-         9: "GS update + store", 10: "norm partial", 11: "barrier 3", 12: "Givens / flags"}
+         9: "GS update + store", 10: "norm partial", 11: "barrier 3", 12: "Givens / flags",
+         13: "ctl: reduce", 14: "ctl: h / G column", 15: "ctl: corr", 16: "giv: reduce",
+         17: "giv: |H col|"}
 tot = {}
 for p, v in zip(ph[sel] - 0x80, rec[sel, 0]):
     tot[p] = tot.get(p, 0) + int(v)
 its = rep.iterations
 print(f"iterations {its}; mean us per step:")
 for p in sorted(tot):
-    print(f"  {names.get(p, p):28s} {tot[p] / its / 1e3:7.2f}")
+    print(f"  {str(names.get(p, p)):28s} {tot[p] / its / 1e3:7.2f}")
 print(f"  {'sum':28s} {sum(tot.values()) / its / 1e3:7.2f}")
