@@ -558,13 +558,19 @@ void coarse_solve(dk_op* op, dk_defl* c, int mode, bool pre, bool write, const d
   if (split_row != nullptr) split_fork(op, c, v);
   const double rbytes = (split_row ? 2.0 : 1.0) * (12.0 * (double)c->nlabelled + 8.0 * c->d);
   if (c->prof) {  // s~ = P Z^T w, then the two tile streams (t = W s~, y = P^T W^T t)
-    {
-      ProfScope ps(op, PC_RESTRICT, rbytes);
-      launch_restrict_final(c->rm, c->s, gate, op->stream, split_row ? c->run_part2 : nullptr,
-                            split_row);
+    if (split_row != nullptr) {
+      {
+        ProfScope ps(op, PC_RESTRICT, rbytes);
+        launch_restrict_final(c->rm, c->s, gate, op->stream, c->run_part2, split_row);
+      }
+      ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)(c->tg1.nt + c->tg2.nt));
+      launch_tgemv(c->tg1, c->s, c->tv, nullptr, c->d, gate, op->stream);
+      launch_tgemv(c->tg2, c->tv, c->y, c->perm, c->d, gate, op->stream);
+      return;
     }
-    ProfScope ps(op, PC_GEMV, 8.0 * 1024.0 * (double)(c->tg1.nt + c->tg2.nt));
-    launch_tgemv(c->tg1, c->s, c->tv, nullptr, c->d, gate, op->stream);
+    // pass 1 folds in the column sums (cooperative pass with a grid barrier)
+    ProfScope ps(op, PC_GEMV, rbytes + 8.0 * 1024.0 * (double)(c->tg1.nt + c->tg2.nt));
+    launch_tgemv_restrict(c->tg1, c->rm, c->s, c->tv, c->d, gate, op->stream);
     launch_tgemv(c->tg2, c->tv, c->y, c->perm, c->d, gate, op->stream);
     return;
   }
@@ -1864,7 +1870,9 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   const int coarse_launches =
       !c ? 1
          : c->dense ? 2
-         : c->prof  ? 2 + tgemv_launches(c->tg1) + tgemv_launches(c->tg2)
+         : c->prof  ? 1 + (op->split ? 1 + tgemv_launches(c->tg1)
+                                       : tgemv_restrict_launches(c->tg1)) +
+                          tgemv_launches(c->tg2)
          : c->sym   ? 4
                     : 3;
   // restart (stencil chain + projection), m x (stencil chain, projection, update [+ the

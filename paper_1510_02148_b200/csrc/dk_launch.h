@@ -220,6 +220,7 @@ struct TileGemv {
   size_t win_bytes = 0;
   const int* split_rows = nullptr;  // output blocks split across warps (NOSPIN finish)
   int nsplit = 0;
+  unsigned* bar = nullptr;  // [count, generation] of the in-kernel grid barrier (fused pass 1)
 };
 struct TileGemvHost {
   long long nt = 0;
@@ -264,6 +265,12 @@ void launch_tgemv(const TileGemv& g, const double* x, double* y, const int* scat
                   const int* gate, cudaStream_t s);
 // kernels one launch_tgemv issues (1: spinning finisher; 2: NOSPIN pass + k_tg_finish)
 int tgemv_launches(const TileGemv& g);
+// Pass 1 with the column sums s = Z^T w folded in (k_restrict_final's arithmetic, then a grid
+// barrier, inside the cooperative spinning pass); otherwise k_restrict_final + launch_tgemv.
+// s_out = s~ (rm.s_pos order), the pass's x.  Returns the kernels launched.
+int launch_tgemv_restrict(const TileGemv& g, const RunMap& rm, double* s_out, double* y,
+                          int d, const int* gate, cudaStream_t s);
+int tgemv_restrict_launches(const TileGemv& g);
 // f[r] = first nonzero column of row r (<= r) of a d x d matrix (device)
 void launch_row_first_nz(const double* X, int d, int ld, int* f, cudaStream_t s);
 

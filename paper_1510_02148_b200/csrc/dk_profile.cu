@@ -134,6 +134,7 @@ __global__ void k_tile_pack(const double* __restrict__ X, int d, int ld, const i
 // self-validating slots (sentinel until written; no fence, no ticket) and sums them in warp
 // order: deterministic.  With scatter, output row i goes to y[scatter[i]].
 constexpr int kXPre = 8;
+constexpr int kTgLongBatch = 16;  // = k_restrict_final's kLongBatch (bitwise-equal sums)
 
 // partial-row slots hold this bit pattern until written (a negative NaN with a full payload:
 // never the result of arithmetic, which yields the canonical NaN)
@@ -178,11 +179,75 @@ __device__ __forceinline__ double butterfly_sum32(double (&v)[32], int lane) {
 // NOSPIN (DK_NO_SPIN, or a grid that cannot be co-resident): no warp waits for another —
 // every piece of a split block goes to its slot and k_tg_finish sums them after the grid
 // (same order, bitwise equal).
-template <int KW, int KS, bool TRANS, bool NOSPIN>
+// grid barrier of the fused pass 1 (cooperative launch: all blocks resident): release-add
+// arrival, relaxed polling of the generation, acquire; the last arriver resets the count
+__device__ __forceinline__ void tg_grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* count = bar;
+    unsigned* gen = bar + 1;
+    unsigned g0;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(count)
+                 : "memory");
+    if (old == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned*>(count) = 0u;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g0 + 1u) : "memory");
+    } else {
+      while (*reinterpret_cast<volatile unsigned*>(gen) == g0) __nanosleep(20);
+      unsigned t;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(gen) : "memory");
+    }
+  }
+  __syncthreads();
+}
+
+// s~ = the column sums of the stencil's run partials, each block a slice of the short
+// columns (thread per column, all <= kShortRuns loads in flight, in-order sum) and every
+// grid-th long column (warp per column, kLongBatch loads per lane, xor tree): exactly
+// k_restrict_final's arithmetic
+__device__ __forceinline__ void tg_restrict(const RunMap& rm, double* __restrict__ s_out) {
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int d = rm.d;
+  const int per = (d + gridDim.x - 1) / gridDim.x;
+  const int L0 = blockIdx.x * per, L1 = min(d, L0 + per);
+  for (int L = L0 + threadIdx.x; L < L1; L += blockDim.x) {
+    const int lo = rm.lab_run_ptr[L], len = rm.lab_run_ptr[L + 1] - lo;
+    if (len > kShortRuns) continue;
+    double v[kShortRuns];
+#pragma unroll
+    for (int k = 0; k < kShortRuns; ++k) v[k] = k < len ? __ldcg(rm.run_part + lo + k) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < kShortRuns; ++k)
+      if (k < len) acc += v[k];
+    s_out[rm.s_pos ? rm.s_pos[L] : L] = acc;
+  }
+  for (int k = blockIdx.x * nwarp + wl; k < rm.nlong; k += gridDim.x * nwarp) {
+    const int L = rm.long_ids[k];
+    double acc = 0.0;
+    const int lo = rm.lab_run_ptr[L], hi = rm.lab_run_ptr[L + 1];
+    for (int k0 = lo + lane; k0 < hi; k0 += 32 * kTgLongBatch) {
+      double v[kTgLongBatch];
+#pragma unroll
+      for (int i = 0; i < kTgLongBatch; ++i)
+        v[i] = k0 + 32 * i < hi ? __ldcg(rm.run_part + k0 + 32 * i) : 0.0;
+#pragma unroll
+      for (int i = 0; i < kTgLongBatch; ++i)
+        if (k0 + 32 * i < hi) acc += v[i];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_out[rm.s_pos ? rm.s_pos[L] : L] = acc;
+  }
+}
+
+template <int KW, int KS, bool TRANS, bool NOSPIN, bool FUSE_R = false>
 __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* __restrict__ x,
                                                       double* __restrict__ y,
                                                       const int* __restrict__ scatter, int d,
-                                                      const int* __restrict__ gate) {
+                                                      const int* __restrict__ gate,
+                                                      RunMap rm, double* s_out) {
   DK_TL(TRANS ? TL_TG2 : TL_TG1, 0);
   DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 0);
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -218,6 +283,10 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   DK_TL(TRANS ? TL_TG2 : TL_TG1, 1);
   DK_TLW(TRANS ? TL_TG2W : TL_TG1W, 1);
   const bool off = gate != nullptr && *gate == 0;
+  if (FUSE_R && !off) {  // s~ first (every block), then the pass reads it as x
+    tg_restrict(rm, s_out);
+    tg_grid_barrier(g.bar);
+  }
   if (off || t0 >= t1) {  // drain the copies already in flight, then leave
     for (int s = 0; s < nfirst; ++s) mbar_wait_parity(&bars[wl][s], 0);
     return;
@@ -706,6 +775,8 @@ int upload_stream(const double* W, int d, int ld, bool pack, const TileGemvHost&
     e = cudaMallocAsync(&g.part, (size_t)h.nslots * kPT * sizeof(double), s);
   if (e == cudaSuccess)  // every slot starts as the sentinel (all bits set)
     e = cudaMemsetAsync(g.part, 0xff, (size_t)h.nslots * kPT * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&g.bar, 2 * sizeof(unsigned), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g.bar, 0, 2 * sizeof(unsigned), s);
   if (e != cudaSuccess) return (int)e;
   // the tile stream itself (big_alloc'd by the caller into g.T)
   if (pack)
@@ -716,10 +787,11 @@ int upload_stream(const double* W, int d, int ld, bool pack, const TileGemvHost&
 
 void free_stream(TileGemv& g, cudaStream_t s) {
   void* bufs[] = {(void*)g.trow, (void*)g.tcol, (void*)g.rfirst, (void*)g.rslot, (void*)g.rnp,
-                  (void*)g.part, (void*)g.tid, (void*)g.split_rows};
+                  (void*)g.part, (void*)g.tid, (void*)g.split_rows, (void*)g.bar};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);
   g.trow = g.tcol = g.rfirst = g.rslot = g.rnp = g.tid = g.split_rows = nullptr;
+  g.bar = nullptr;
   g.nsplit = 0;
   g.part = nullptr;
 }
@@ -797,12 +869,12 @@ static void launch_tg_t(const TileGemv& g, const double* x, double* y, const int
     smem_optin((const void*)k_tgemv<KW, KS, TRANS, false>, smem);
     if (!getenv("DK_NO_COOP")) coop_next() = true;  // finishers wait on other blocks
     launch_pdl(k_tgemv<KW, KS, TRANS, false>, dim3(grid), dim3(KW * 32), smem, s, g, x, y,
-               scatter, d, gate);
+               scatter, d, gate, RunMap{}, (double*)nullptr);
     return;
   }
   smem_optin((const void*)k_tgemv<KW, KS, TRANS, true>, smem);
   launch_pdl(k_tgemv<KW, KS, TRANS, true>, dim3(grid), dim3(KW * 32), smem, s, g, x, y, scatter,
-             d, gate);
+             d, gate, RunMap{}, (double*)nullptr);
   if (g.nsplit > 0)
     launch_pdl(k_tg_finish, dim3((unsigned)((g.nsplit * 32 + 255) / 256)), dim3(256), 0, s, g, y,
                scatter, d, gate);
@@ -826,6 +898,64 @@ static void launch_tg(const TileGemv& g, const double* x, double* y, const int* 
     launch_tg_t<KW, KS, true>(g, x, y, scatter, d, gate, s, grid, smem, wp);
   else
     launch_tg_t<KW, KS, false>(g, x, y, scatter, d, gate, s, grid, smem, wp);
+}
+
+template <int KW, int KS>
+static bool tg_fuse_ok(const TileGemv& g) {
+  const size_t smem = (size_t)KW * KS * kPTileBytes;
+  const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
+  // opt-in (DK_FUSE_RESTRICT=1): measured 1.9 % slower at config 3 than the separate
+  // column-sum kernel (148 blocks sum what 241 did, plus the barrier)
+  static const bool no_fuse = getenv("DK_FUSE_RESTRICT") == nullptr;
+  static const bool no_coop = getenv("DK_NO_COOP") != nullptr;
+  return !(no_fuse || no_coop || g.bar == nullptr || g.trans || g.win_bytes ||
+           !tg_spin_ok<KW, KS, false>(grid, smem));
+}
+
+template <int KW, int KS>
+static int launch_tg_restrict(const TileGemv& g, const RunMap& rm, double* s_out, double* y,
+                              int d, const int* gate, cudaStream_t s) {
+  const size_t smem = (size_t)KW * KS * kPTileBytes;
+  const unsigned grid = (unsigned)((g.nw + KW - 1) / KW);
+  if (!tg_fuse_ok<KW, KS>(g)) {
+    launch_restrict_final(rm, s_out, gate, s);
+    launch_tgemv(g, s_out, y, nullptr, d, gate, s);
+    return 1 + tgemv_launches(g);
+  }
+  smem_optin((const void*)k_tgemv<KW, KS, false, false, true>, smem);
+  coop_next() = true;  // the in-kernel grid barrier and the finishers need every block resident
+  launch_pdl(k_tgemv<KW, KS, false, false, true>, dim3(grid), dim3(KW * 32), smem, s, g,
+             (const double*)s_out, y, (const int*)nullptr, d, gate, rm, s_out);
+  return 1;
+}
+
+int tgemv_restrict_launches(const TileGemv& g) {
+  bool f;
+  switch (tgemv_cfg()) {
+    case 0: f = tg_fuse_ok<12, 2>(g); break;
+    case 1: f = tg_fuse_ok<16, 1>(g); break;
+    case 3: f = tg_fuse_ok<4, 6>(g); break;
+    case 4: f = tg_fuse_ok<8, 2>(g); break;
+    case 5: f = tg_fuse_ok<6, 2>(g); break;
+    case 6: f = tg_fuse_ok<4, 3>(g); break;
+    case 7: f = tg_fuse_ok<4, 2>(g); break;
+    default: f = tg_fuse_ok<8, 3>(g); break;
+  }
+  return f ? 1 : 1 + tgemv_launches(g);
+}
+
+int launch_tgemv_restrict(const TileGemv& g, const RunMap& rm, double* s_out, double* y,
+                          int d, const int* gate, cudaStream_t s) {
+  switch (tgemv_cfg()) {
+    case 0: return launch_tg_restrict<12, 2>(g, rm, s_out, y, d, gate, s);
+    case 1: return launch_tg_restrict<16, 1>(g, rm, s_out, y, d, gate, s);
+    case 3: return launch_tg_restrict<4, 6>(g, rm, s_out, y, d, gate, s);
+    case 4: return launch_tg_restrict<8, 2>(g, rm, s_out, y, d, gate, s);
+    case 5: return launch_tg_restrict<6, 2>(g, rm, s_out, y, d, gate, s);
+    case 6: return launch_tg_restrict<4, 3>(g, rm, s_out, y, d, gate, s);
+    case 7: return launch_tg_restrict<4, 2>(g, rm, s_out, y, d, gate, s);
+    default: return launch_tg_restrict<8, 3>(g, rm, s_out, y, d, gate, s);
+  }
 }
 
 // kernels one launch_tgemv issues: 1 (spinning finisher) or 2 (NOSPIN pass + k_tg_finish)

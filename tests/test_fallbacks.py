@@ -9,6 +9,8 @@ environment switches (read once per process, so each variant runs in a subproces
   DK_NO_EARLY    no early start of the stencil / k_gs on published partials
   DK_NO_COOP     the spinning grids launched without the cooperative attribute (by default
                  they are cooperative: all blocks co-resident or the launch fails)
+  DK_FUSE_RESTRICT     (opt-in variant) the column sums inside tile pass 1, behind a grid
+                       barrier of the cooperative pass
 Config 3 uses the nested-dissection tile streams (the spinning finisher) and its x is
 compared bitwise; config 1 checks the small-d coarse paths.
 """
@@ -59,9 +61,11 @@ def test_fallbacks_bitwise(gpu, cfg):
     launches = ref.pop("launches")
     for extra in ({"DK_NO_SPIN": "1"},
                   {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"},
-                  {"DK_NO_COOP": "1"}):
+                  {"DK_NO_COOP": "1"}, {"DK_FUSE_RESTRICT": "1"}):
         got = _run(cfg, extra)
         got_launches = got.pop("launches")
         assert got == ref, (extra, got, ref)
         if cfg == 3 and "DK_NO_SPIN" in extra:  # the default path spins (one launch a pass)
             assert got_launches > launches, (extra, got_launches, launches)
+        if cfg == 3 and "DK_FUSE_RESTRICT" in extra:  # one kernel fewer per coarse solve
+            assert got_launches < launches, (extra, got_launches, launches)
