@@ -1849,13 +1849,16 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
   const int max_cycles = ctl_in ? ctl_in->max_cycles : 0;
   // krylov.py:127: no cycle starts once max_iters is reached (the caller's earlier calls)
   const bool run_cycles = !(resume && ctl_in->iterations >= max_iters);
-  // The cycle becomes a CUDA graph from the second solve with the same (context, m): a
-  // one-off solve (the public pdgmres path) launches eagerly and skips the instantiation.
+  // The cycle is a CUDA graph.  A repeated solve with the same (context, m) builds it up
+  // front; a one-off solve (the public pdgmres path: a fresh context per call) launches its
+  // first cycle eagerly and captures + instantiates the graph on the host while the GPU runs
+  // that cycle, so the remaining cycles replay it (DK_NO_LATE_GRAPH: eager throughout).
   const unsigned long long key =
       (c ? c->serial : 0ull) * 4 + (op->split ? 1 : 0) + (op->small ? 2 : 0);
-  const bool use_graph =
+  bool use_graph =
       !op->prof && ((op->gexec && op->g_m == m && op->g_ctx == key) ||
                     (op->seen_m == m && op->seen_ctx == key));
+  static const bool late_graph_off = getenv("DK_NO_LATE_GRAPH") != nullptr;
   op->seen_m = m;
   op->seen_ctx = key;
   if (use_graph) {
@@ -1896,6 +1899,12 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
       issue_cycle_end(op);
       op->launches = l0 + per_cycle_launches;
       DK_TRY(launch_error());
+      if (cyc == 0 && guard_cycles > 1 && !late_graph_off) {
+        // the stream still holds this cycle's work; capture records only what follows
+        rc = build_graph(op, c, m);
+        if (rc) return rc;
+        use_graph = true;  // from the next cycle on
+      }
     } else {
       issue_restart(op, c);
       if ((rc = read_state(op))) return rc;

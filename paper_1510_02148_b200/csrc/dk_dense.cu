@@ -125,7 +125,8 @@ __device__ __forceinline__ void stage_operand(double* s, const double* g, int ld
 template <bool TA, bool TB, int NT, bool A8>
 __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
     k_dgemm_mma(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
-                int N, int K, double alpha, double beta, int tri, int kshift, int kstop) {
+                int N, int K, double alpha, double beta, int tri, int kshift, int kstop,
+                double* P) {
   constexpr int BN = 32 * NT, LDMA = GM + 4, LDMB = BN + 4;
   constexpr int OPA = op_doubles<GM>(), OPB = op_doubles<BN>();
   extern __shared__ __align__(128) double smem[];
@@ -139,7 +140,15 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
   }
   int kend = K;
   if (kstop != INT_MIN) kend = min(K, c0 + BN + kstop);  // op(B)[k][j] == 0 for k >= j + kstop
-  const int nk = (kend > kbeg) ? (kend - kbeg + GK - 1) / GK : 0;
+  int nk = (kend > kbeg) ? (kend - kbeg + GK - 1) / GK : 0;
+  if (P != nullptr) {  // split K: this CTA's share of the tile's K steps, raw partial sums
+    const int chunk = (nk + gridDim.z - 1) / gridDim.z;
+    const int it0 = min(nk, (int)blockIdx.z * chunk);
+    nk = min(nk, it0 + chunk) - it0;
+    kbeg += it0 * GK;
+    beta = 0.0;
+    alpha = 1.0;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 2) * 64, wn = (warp & 3) * (8 * NT);
@@ -221,6 +230,23 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
     }
   }
   cp_wait<0>();
+  if (P != nullptr) {  // partials of split z: [z][M][N]
+    double* Pz = P + (long long)blockIdx.z * M * N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = r0 + wm + i * 16 + g + 8 * h;
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int col = c0 + wn + j * 8 + 2 * t;
+          if (col < N) Pz[(long long)row * N + col] = acc[i][j][2 * h];
+          if (col + 1 < N) Pz[(long long)row * N + col + 1] = acc[i][j][2 * h + 1];
+        }
+      }
+    return;
+  }
   // epilogue: c0,c1 at (g, 2t..2t+1), c2,c3 at (g+8, 2t..2t+1) of each 16 x 8 tile
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -246,15 +272,59 @@ __global__ void __launch_bounds__(256, NT == 2 ? 2 : 1)
   }
 }
 
+// split-K epilogue: C = alpha (beta/alpha C + sum_z P[z]) over the tiles the GEMM writes, the
+// partials summed in split order (deterministic)
+__global__ void k_splitk_reduce(const double* __restrict__ P, int S, int M, int N, double* C,
+                                int ldc, double alpha, double beta, int tri, int BN) {
+  const long long total = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e / N), col = (int)(e % N);
+    const int r0 = (row / GM) * GM, c0 = (col / BN) * BN;
+    if (tri == 1 && c0 > r0 + GM - 1) continue;
+    if (tri == 2 && r0 > c0 + BN - 1) continue;
+    double v = beta != 0.0 ? (beta / alpha) * C[(long long)row * ldc + col] : 0.0;
+    for (int z = 0; z < S; ++z) v += P[z * total + e];
+    C[(long long)row * ldc + col] = alpha * v;
+  }
+}
+
+// K splits of a GEMM whose tile grid cannot fill the SMs (the nested-dissection tree's
+// separator products: a few hundred rows, K up to d): enough CTAs for two per SM, at least
+// 256 K per split (DK_NO_SPLITK: one CTA per tile)
+int splitk_count(int M, int N, int K, int BN) {
+  static const bool off = getenv("DK_NO_SPLITK") != nullptr;
+  if (off) return 1;
+  const long long tiles = (long long)((N + BN - 1) / BN) * ((M + GM - 1) / GM);
+  const long long want = 2ll * num_sms();
+  if (tiles >= want || K < 512) return 1;
+  long long S = (want + tiles - 1) / tiles;
+  S = std::min<long long>(S, K / 256);
+  S = std::min<long long>(S, 32);
+  return S < 2 ? 1 : (int)S;
+}
+
 template <bool TA, bool TB, int NT, bool A8>
 void launch_mma_a(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
                   int N, int K, double alpha, double beta, int tri, int kshift, int kstop,
                   cudaStream_t s) {
   smem_optin((const void*)k_dgemm_mma<TA, TB, NT, A8>, gemm_smem<NT>());
-  dim3 grid((N + 32 * NT - 1) / (32 * NT), (M + GM - 1) / GM);
+  const int S = splitk_count(M, N, K, 32 * NT);
+  double* P = nullptr;
+  if (S > 1 && cudaMallocAsync(&P, (size_t)S * M * N * sizeof(double), s) != cudaSuccess) {
+    cudaGetLastError();
+    P = nullptr;
+  }
+  dim3 grid((N + 32 * NT - 1) / (32 * NT), (M + GM - 1) / GM, P ? S : 1);
   k_dgemm_mma<TA, TB, NT, A8><<<grid, 256, gemm_smem<NT>(), s>>>(A, lda, B, ldb, C, ldc, M, N,
                                                                 K, alpha, beta, tri, kshift,
-                                                                kstop);
+                                                                kstop, P);
+  if (P) {
+    const long long total = (long long)M * N;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 8ll * num_sms());
+    k_splitk_reduce<<<blocks, 256, 0, s>>>(P, S, M, N, C, ldc, alpha, beta, tri, 32 * NT);
+    cudaFreeAsync(P, s);
+  }
 }
 
 // operands at odd column offsets or with odd strides take the 8-byte copy path
