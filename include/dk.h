@@ -167,6 +167,12 @@ int dk_gmres_ex(dk_op* op, dk_defl* ctx, const double* b, const double* x0, int3
                 int32_t max_iters, int32_t min_iters, double* x_out, double* hist,
                 int32_t* restart_of, double* hbar, double* gram, dk_solve_info* info,
                 const dk_cycle_ctl* ctl_in, dk_cycle_ctl* ctl_out);
+/* The restart loop of the last dk_gmres / dk_gmres_ex call (krylov.py:127 `while not converged
+ * and it < max_iters`): host_syncs = host synchronisations inside the cycle loop; device_loop
+ * = 1 when the cycles ran as the body of a CUDA conditional WHILE graph node, the device
+ * deciding each restart (one host read after the loop), 0 when the host read the state after
+ * every cycle (first cycle of a one-off solve, event-profiled solves, DK_NO_LOOP_GRAPH). */
+int dk_op_solve_stats(dk_op* op, int32_t* host_syncs, int32_t* device_loop);
 /* Copies basis vector i of the last cycle (normalised, length n) out; i <= last_cols. */
 int dk_last_basis_vector(dk_op* op, int32_t i, double* out);
 

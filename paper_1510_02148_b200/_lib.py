@@ -27,7 +27,7 @@ EXPORTS = (
     "dk_op_profile_read",
     "dk_defl_create", "dk_defl_destroy", "dk_defl_apply_p1", "dk_defl_apply_p2",
     "dk_defl_reconstruct", "dk_defl_x_star", "dk_defl_coarse", "dk_defl_setup_ms",
-    "dk_gmres", "dk_gmres_ex", "dk_last_basis_vector",
+    "dk_gmres", "dk_gmres_ex", "dk_last_basis_vector", "dk_op_solve_stats",
     "dk_levelset_labels_device", "dk_assemble_tpfa", "dk_defl_create_dense",
     "dk_defl_create_ritz", "dk_defl_coarse_kind", "dk_dense_lu", "dk_lu_solve",
 )
@@ -100,6 +100,7 @@ def _declare(lib):
         "dk_defl_create_ritz": (C.c_int, [C.POINTER(_P), _P, _P, C.c_int32, C.c_int32, C.c_int32,
                                           _P]),
         "dk_last_basis_vector": (C.c_int, [_P, C.c_int32, _P]),
+        "dk_op_solve_stats": (C.c_int, [_P, _P, _P]),
         "dk_levelset_labels_device": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _P, C.c_int32,
                                                 C.c_int32, C.c_int32, _P, _I64, _P]),
         "dk_dense_lu": (C.c_int, [C.c_int64, _P, _P, _P, _D]),

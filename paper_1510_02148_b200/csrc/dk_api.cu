@@ -133,6 +133,10 @@ struct dk_op {
   unsigned long long seen_ctx = ~0ull;  // (context, m) of the previous solve
   int seen_m = -1;
   int g_m = -1;
+  bool g_loop = false;      // gexec is the WHILE-loop graph (device-decided restarts)
+  bool loop_broken = false; // the loop graph could not be built on this driver: flat graph
+  int host_syncs = 0;       // host synchronisations of the last solve's cycle loop
+  int used_loop = 0;        // the last solve's cycles ran under the device-side loop
   // profiling
   bool prof = false;
   double prof_ms[PC_COUNT] = {0};
@@ -750,6 +754,67 @@ int read_state(dk_op* op) {
   return DK_OK;
 }
 
+// One GMRES cycle recorded into the capturing stream (restart, m Arnoldi steps, cycle end).
+static void issue_cycle(dk_op* op, dk_defl* c, int m) {
+  issue_restart(op, c);
+  if (op->small) issue_cycle_small(op, c, m);
+  else
+    for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
+  issue_cycle_end(op);
+}
+
+static int end_capture(dk_op* op, cudaGraph_t* g) {
+  const cudaError_t le = launch_error();
+  launch_error() = cudaSuccess;
+  const cudaError_t ce = cudaStreamEndCapture(op->stream, g);
+  if (le != cudaSuccess) return cuda_fail(le, "kernel launch during graph capture");
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+  return DK_OK;
+}
+
+// The restart loop on the device (krylov.py:127): a graph holding one conditional WHILE node
+// whose body is the cycle followed by k_loop_cond.  One launch runs every remaining cycle; the
+// host reads the state once, after the loop.  Returns a cuda error when the driver rejects
+// any step (the caller then builds the flat one-cycle graph).
+static cudaError_t build_loop_graph(dk_op* op, dk_defl* c, int m, cudaGraphExec_t* out) {
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaGraphCreate(&g, 0);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h;
+  e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  cudaGraphNode_t node;
+  cudaGraphNodeParams cp = {};
+  if (e == cudaSuccess) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  }
+  if (e == cudaSuccess) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    launch_error() = cudaSuccess;
+    e = cudaStreamBeginCaptureToGraph(op->stream, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      pdl_skip_next() = true;
+      const int l0 = op->launches;
+      issue_cycle(op, c, m);
+      launch_loop_cond(op->sc, h, op->stream);
+      op->launches = l0;
+      const cudaError_t le = launch_error();
+      launch_error() = cudaSuccess;
+      cudaGraph_t got = nullptr;
+      e = cudaStreamEndCapture(op->stream, &got);
+      if (e == cudaSuccess) e = le;
+    }
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(out, g, 0);
+  if (g) cudaGraphDestroy(g);
+  if (e != cudaSuccess) cudaGetLastError();  // clear the sticky-free error for the fallback
+  return e;
+}
+
 int build_graph(dk_op* op, dk_defl* c, int m) {
   const unsigned long long key =
       (c ? c->serial : 0ull) * 4 + (op->split ? 1 : 0) + (op->small ? 2 : 0);
@@ -758,29 +823,38 @@ int build_graph(dk_op* op, dk_defl* c, int m) {
     cudaGraphExecDestroy(op->gexec);
     op->gexec = nullptr;
   }
+  static const bool loop_off = getenv("DK_NO_LOOP_GRAPH") != nullptr;
+  if (!loop_off && !op->loop_broken && !op->split) {
+    const cudaError_t le = build_loop_graph(op, c, m, &op->gexec);
+    if (le == cudaSuccess) {
+      op->g_m = m;
+      op->g_ctx = key;
+      op->g_loop = true;
+      return DK_OK;
+    }
+    op->gexec = nullptr;
+    op->loop_broken = true;
+    if (getenv("DK_TRACE"))
+      fprintf(stderr, "dk: WHILE-loop graph rejected (%s); one graph launch per cycle\n",
+              cudaGetErrorString(le));
+  }
   cudaGraph_t g;
   launch_error() = cudaSuccess;
   DK_TRY(cudaStreamBeginCapture(op->stream, cudaStreamCaptureModeThreadLocal));
   pdl_skip_next() = true;
   const int l0 = op->launches;
-  issue_restart(op, c);
-  if (op->small) issue_cycle_small(op, c, m);
-  else
-    for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
-  issue_cycle_end(op);
+  issue_cycle(op, c, m);
   op->launches = l0;
   {
-    const cudaError_t le = launch_error();
-    launch_error() = cudaSuccess;
-    const cudaError_t ce = cudaStreamEndCapture(op->stream, &g);
-    if (le != cudaSuccess) return cuda_fail(le, "kernel launch during graph capture");
-    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+    const int rc = end_capture(op, &g);
+    if (rc) return rc;
   }
   cudaError_t e = cudaGraphInstantiate(&op->gexec, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   op->g_m = m;
   op->g_ctx = key;
+  op->g_loop = false;
   return DK_OK;
 }
 
@@ -1886,24 +1960,47 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
                       m * (coarse_launches + (op->gs_fuse ? 2 : 4) + (op->split ? 1 : 0)) + 2;
   long long guard_cycles = run_cycles ? (long long)max_iters + 2 : 0;
   if (max_cycles > 0 && guard_cycles > max_cycles) guard_cycles = max_cycles;
+  op->host_syncs = 0;
+  op->used_loop = 0;
   for (long long cyc = 0; cyc < guard_cycles; ++cyc) {
+    if (use_graph && op->g_loop) {
+      // every remaining cycle in one launch: the WHILE node's condition is set on the device
+      const long long left = guard_cycles - cyc;
+      launch_loop_arm(op->sc, (int)std::min<long long>(left, INT_MAX), op->stream);
+      DK_TRY(cudaGraphLaunch(op->gexec, op->stream));
+      if ((rc = read_state(op))) return rc;
+      op->host_syncs += 1;
+      op->used_loop = 1;
+      const long long ran = left - op->st_host->loop_left;
+      op->launches += 1 + (int)ran * (per_cycle_launches + 1);
+      break;
+    }
     if (use_graph) {
       DK_TRY(cudaGraphLaunch(op->gexec, op->stream));
       op->launches += per_cycle_launches;
     } else if (!op->prof) {
       const int l0 = op->launches;
-      issue_restart(op, c);
-      if (op->small) issue_cycle_small(op, c, m);
-      else
-        for (int j = 0; j < m; ++j) issue_iteration(op, c, j);
-      issue_cycle_end(op);
+      issue_cycle(op, c, m);
       op->launches = l0 + per_cycle_launches;
       DK_TRY(launch_error());
       if (cyc == 0 && guard_cycles > 1 && !late_graph_off) {
-        // the stream still holds this cycle's work; capture records only what follows
+        // the stream still holds this cycle's work; capture records only what follows.  The
+        // state copy queued behind the cycle is polled, never waited for: a solve that ended
+        // in its first cycle while the host was building the graph stops here.
+        cudaEvent_t es;
+        DK_TRY(cudaEventCreateWithFlags(&es, cudaEventDisableTiming));
+        DK_TRY(cudaMemcpyAsync(op->st_host, op->st, sizeof(State), cudaMemcpyDeviceToHost,
+                               op->stream));
+        DK_TRY(cudaEventRecord(es, op->stream));
         rc = build_graph(op, c, m);
+        const bool landed = cudaEventQuery(es) == cudaSuccess;
+        cudaEventDestroy(es);
         if (rc) return rc;
         use_graph = true;  // from the next cycle on
+        if (op->g_loop) {
+          if (landed && !op->st_host->running) break;
+          continue;  // no host wait in between: a finished solve's loop body is gated off
+        }
       }
     } else {
       issue_restart(op, c);
@@ -1916,6 +2013,7 @@ int dk_gmres_ex(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_
       prof_collect(op);
     }
     if ((rc = read_state(op))) return rc;
+    op->host_syncs += 1;
     if (!op->st_host->running) break;
   }
   cudaEventRecord(e1, op->stream);
@@ -2018,6 +2116,13 @@ int dk_gmres(dk_op* op, dk_defl* c, const double* b, const double* x0, int32_t m
              int32_t* restart_of, double* hbar, dk_solve_info* info) {
   return dk_gmres_ex(op, c, b, x0, m, tol, max_iters, min_iters, x_out, hist, restart_of, hbar,
                      nullptr, info, nullptr, nullptr);
+}
+
+int dk_op_solve_stats(dk_op* op, int32_t* host_syncs, int32_t* device_loop) {
+  if (!op || !host_syncs || !device_loop) return fail(DK_EINVAL, "null argument");
+  *host_syncs = op->host_syncs;
+  *device_loop = op->used_loop;
+  return DK_OK;
 }
 
 int dk_last_basis_vector(dk_op* op, int32_t i, double* out) {

@@ -59,6 +59,7 @@ struct State {
   int xupdate;     // cycle end produced an x update (gates k_xupdate)
   int cycle_cols;  // columns of the last cycle before the dependent-column drop
   int last_broke;  // the last iteration ended its cycle by convergence or breakdown
+  int loop_left;   // cycles the device-side restart loop (WHILE graph) may still start
   int m, max_iters, min_iters;
   double tol, denom, beta, prev_beta, wnorm0;
   unsigned int ticket[4];

@@ -2512,7 +2512,12 @@ __global__ void __launch_bounds__(32) k_cycle_end(Scal sc) {
   State* st = sc.st;
   if (sc.post != nullptr)  // re-arm the early-start flags (the last iteration's is still set)
     for (int i = threadIdx.x; i < 2 * (sc.m + 1); i += 32) sc.post[i] = 0u;
-  if (!st->cycle_open) return;
+  if (!st->cycle_open) {
+    // no cycle ran (a finished solve's gated pass through the restart loop's body): the
+    // previous cycle's x update must not be applied again
+    if (threadIdx.x == 0) st->xupdate = 0;
+    return;
+  }
   extern __shared__ double sm[];
   const int m = sc.m;
   const int lane = threadIdx.x;
@@ -2702,6 +2707,7 @@ __global__ void k_init_state(Scal sc, double tol, int m, int max_iters, int min_
   st->xupdate = 0;
   st->cycle_cols = 0;
   st->last_broke = 0;
+  st->loop_left = 0;
   for (int i = 0; i < 4; ++i) st->ticket[i] = 0u;
 }
 
@@ -2727,6 +2733,23 @@ __global__ void k_resume_state(Scal sc, int iterations, int cycles, int warning,
 void launch_resume_state(const Scal& sc, int iterations, int cycles, int warning, int has_prev,
                          double denom, double prev_beta, cudaStream_t s) {
   k_resume_state<<<1, 1, 0, s>>>(sc, iterations, cycles, warning, has_prev, denom, prev_beta);
+}
+
+// ---- device-decided restart loop (krylov.py:127 `while not converged and it < max_iters`) --
+// The cycle graph is the body of a conditional WHILE node; its last kernel decides whether
+// another cycle starts: the solve is still running and the caller's cycle budget is not spent.
+__global__ void k_loop_arm(State* st, int cycles) { st->loop_left = cycles; }
+__global__ void k_loop_cond(State* st, cudaGraphConditionalHandle h) {
+  pdl_wait();
+  const int left = st->loop_left - 1;
+  st->loop_left = left;
+  cudaGraphSetConditional(h, (st->running && left > 0) ? 1u : 0u);
+}
+void launch_loop_arm(const Scal& sc, int cycles, cudaStream_t s) {
+  k_loop_arm<<<1, 1, 0, s>>>(sc.st, cycles);
+}
+void launch_loop_cond(const Scal& sc, cudaGraphConditionalHandle h, cudaStream_t s) {
+  launch_pdl(k_loop_cond, dim3(1), dim3(1), 0, s, sc.st, h);
 }
 
 DK_TL_SETTER(tl_set_kernels)

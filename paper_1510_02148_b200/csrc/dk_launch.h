@@ -138,6 +138,10 @@ void launch_init_state(const Scal& sc, double tol, int m, int max_iters, int min
                        cudaStream_t s);
 void launch_resume_state(const Scal& sc, int iterations, int cycles, int warning, int has_prev,
                          double denom, double prev_beta, cudaStream_t s);
+// device-decided restart loop: arm the cycle budget; the WHILE body's last kernel sets the
+// loop condition (another cycle: still running and budget left)
+void launch_loop_arm(const Scal& sc, int cycles, cudaStream_t s);
+void launch_loop_cond(const Scal& sc, cudaGraphConditionalHandle h, cudaStream_t s);
 
 // ---- set-up on the device (dk_setup.cu) ----
 int device_levelset_labels(long long nx, long long ny, long long nz, const long long* band_in,

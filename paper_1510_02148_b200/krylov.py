@@ -108,6 +108,8 @@ class SolveReport:
     solve_seconds: float = 0.0
     kernel_launches: int = 0
     reorthogonalisations: int = 0
+    host_syncs: int = 0       # host synchronisations inside the cycle loop (dk_op_solve_stats)
+    device_loop: bool = False  # restarts decided on the device (conditional WHILE graph)
 
 
 def ritz_values(data: ArnoldiData) -> np.ndarray:
@@ -136,6 +138,8 @@ class _Cycles:
         self.solve_seconds = 0.0
         self.launches = 0
         self.reorths = 0
+        self.host_syncs = 0
+        self.device_loop = False
 
     def run(self, ctx, max_cycles: int = 0, warning: int | None = None):
         """Cycles until convergence / max_iters (or max_cycles of this call) on the current
@@ -166,6 +170,10 @@ class _Cycles:
         self.solve_seconds += float(info.solve_seconds)
         self.launches += int(info.kernel_launches)
         self.reorths += int(info.reorths)
+        hs, dl = C.c_int32(0), C.c_int32(0)
+        _lib.check(op._lib.dk_op_solve_stats(op.h, C.byref(hs), C.byref(dl)), "dk_op_solve_stats")
+        self.host_syncs += int(hs.value)
+        self.device_loop = bool(dl.value)
         cols = int(info.last_cols)
         self.hbar_full = hbar.T.copy()  # (m+1) x m, the cycle's columns before any drop
         if info.cycles > 0:
@@ -190,7 +198,8 @@ class _Cycles:
             warning=warning if warning is not None else ("breakdown" if info.warning == 1
                                                          else None),
             deflated_from_cycle=deflated_from, solve_seconds=self.solve_seconds,
-            kernel_launches=self.launches, reorthogonalisations=self.reorths)
+            kernel_launches=self.launches, reorthogonalisations=self.reorths,
+            host_syncs=self.host_syncs, device_loop=self.device_loop)
 
 
 def _ritz_of_cycle(H: np.ndarray, cols: int, n_iters: int):

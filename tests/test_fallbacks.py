@@ -9,6 +9,8 @@ environment switches (read once per process, so each variant runs in a subproces
   DK_NO_EARLY    no early start of the stencil / k_gs on published partials
   DK_NO_COOP     the spinning grids launched without the cooperative attribute (by default
                  they are cooperative: all blocks co-resident or the launch fails)
+  DK_NO_LOOP_GRAPH     one graph launch and one host read of the state per cycle instead of
+                       the conditional WHILE graph (restarts decided on the device)
   DK_FUSE_RESTRICT     (opt-in variant) the column sums inside tile pass 1, behind a grid
                        barrier of the cooperative pass
 Config 3 uses the nested-dissection tile streams (the spinning finisher) and its x is
@@ -40,7 +42,8 @@ M = dk.Preconditioner.jacobi(A)
 basis = dk.partition_to_basis(case.partition())
 rep = dk.pdgmres(A, b, M=M, m=case.m, basis=basis, tol=case.tol, max_iters=case.max_iters)
 print(json.dumps({{"iters": rep.iterations, "relres": rep.final_relres,
-                  "launches": rep.kernel_launches,
+                  "launches": rep.kernel_launches, "syncs": rep.host_syncs,
+                  "loop": rep.device_loop,
                   "x": hashlib.sha256(np.ascontiguousarray(rep.x).tobytes()).hexdigest(),
                   "hist": hashlib.sha256(np.asarray(rep.residual_history).tobytes()).hexdigest()}}))
 """
@@ -59,11 +62,16 @@ def _run(cfg, env_extra):
 def test_fallbacks_bitwise(gpu, cfg):
     ref = _run(cfg, {})
     launches = ref.pop("launches")
+    # the default path decides its restarts on the device: one host read for the whole loop
+    assert ref.pop("loop") is True and ref.pop("syncs") == 1
     for extra in ({"DK_NO_SPIN": "1"},
                   {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"},
-                  {"DK_NO_COOP": "1"}, {"DK_FUSE_RESTRICT": "1"}):
+                  {"DK_NO_COOP": "1"}, {"DK_FUSE_RESTRICT": "1"}, {"DK_NO_LOOP_GRAPH": "1"}):
         got = _run(cfg, extra)
         got_launches = got.pop("launches")
+        loop, syncs = got.pop("loop"), got.pop("syncs")
+        if "DK_NO_LOOP_GRAPH" in extra:  # the host reads the state after every cycle
+            assert loop is False and syncs >= (16 if cfg == 3 else 2), (loop, syncs)
         assert got == ref, (extra, got, ref)
         if cfg == 3 and "DK_NO_SPIN" in extra:  # the default path spins (one launch a pass)
             assert got_launches > launches, (extra, got_launches, launches)
