@@ -399,6 +399,8 @@ def run_ours(args, world, rank, local, pg):
                          max_iters=case.max_iters)
         sec = time.perf_counter() - t
         A_host.release_device()
+        if os.environ.get("DK_TRACE"):
+            print(f"e2e call {s}: {sec:.4f}s", file=sys.stderr, flush=True)
         if s > 0:  # first call warms the library / allocator
             e2e_its += rep.iterations
             e2e_sec += sec

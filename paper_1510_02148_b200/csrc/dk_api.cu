@@ -1304,7 +1304,7 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   DKD(cudaMallocAsync(&c->lab_run_ptr, ptr.size() * sizeof(int), s));
   DKD(cudaMemcpyAsync(c->lab_run_ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
-  DKD(cudaMallocAsync(&c->run_slot, slot.size() * sizeof(int), s));
+  DKD(cudaMallocAsync(&c->run_slot, (slot.size() + 4) * sizeof(int), s));
   DKD(cudaMemcpyAsync(c->run_slot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice,
                       s));
   tr.mark("run map uploaded");

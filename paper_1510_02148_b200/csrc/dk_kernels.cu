@@ -31,8 +31,17 @@ namespace dk {
 __device__ __forceinline__ int pidx(int c) { return c + (c >> 3); }
 constexpr int kTilePad = kTile + kTile / 8;
 
-__device__ void tile_restrict(const double* sw, const int* sl, double* out,
-                              const int* __restrict__ slot) {
+// RING: called by the 256 compute threads of a larger block (named barrier 1) with the
+// tile's slot list in shared memory; otherwise by a whole 256-thread block, slots in global
+template <bool RING>
+__device__ __forceinline__ void tile_sync() {
+  if (RING) asm volatile("bar.sync 1, 256;" ::: "memory");
+  else __syncthreads();
+}
+
+template <bool RING, class SlotFn>
+__device__ __forceinline__ void tile_restrict(const double* sw, const int* sl, double* out,
+                                              SlotFn slot) {
   __shared__ int wf[kWarps];
   __shared__ double ws[kWarps];
   __shared__ int wc[kWarps];
@@ -88,7 +97,7 @@ __device__ void tile_restrict(const double* sw, const int* sl, double* out,
     se = 0.0;
     ce = 0;
   }
-  __syncthreads();
+  tile_sync<RING>();
   double ps = 0.0;
   int pc = 0;
   for (int w = 0; w < warp; ++w) {
@@ -106,50 +115,57 @@ __device__ void tile_restrict(const double* sw, const int* sl, double* out,
     run = __dadd_rn(run, val[e]);
     const bool is_tail = (e < 7) ? ((heads >> (e + 1)) & 1u) != 0
                                  : (c0 + 8 >= kTile || next != lb[7]);
-    if (is_tail) out[__ldg(slot + ridx)] = run;
+    if (is_tail) out[slot(ridx)] = run;
   }
 }
 
 // Run sums of a stencil tile's outputs rr (8 per thread: cells 2t + 512k, +1) with labels lb.
+// slot(r): the slot of the tile's r-th run
+template <bool RING, class SlotFn>
+__device__ __forceinline__ void restrict_tail_runs(const double (&rr)[8], const int2 (&lb)[4],
+                                                   double* sw, int* sl, double* wsum, int nruns,
+                                                   SlotFn slot,
+                                                   double* __restrict__ run_part) {
+  // a tile inside one region is a single run: plain block sum instead of the segmented scan
+  const bool one_run = nruns == 1;
+  double tsum = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (one_run) {
+      tsum = __dadd_rn(tsum, __dadd_rn(rr[2 * k], rr[2 * k + 1]));
+    } else {
+      const int p = pidx(2 * threadIdx.x + 512 * k);
+      sw[p] = rr[2 * k];
+      sw[p + 1] = rr[2 * k + 1];
+      sl[p] = lb[k].x;
+      sl[p + 1] = lb[k].y;
+    }
+  }
+  if (one_run) {
+    tsum = warp_sum(tsum);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tsum;
+    tile_sync<RING>();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
+      run_part[slot(0)] = s;
+    }
+  } else {
+    tile_sync<RING>();
+    tile_restrict<RING>(sw, sl, run_part, slot);
+  }
+}
+
 __device__ __forceinline__ void stencil_restrict_tail(const double (&rr)[8], const int2 (&lb)[4],
                                                       double* sw, int* sl, double* wsum,
                                                       const int* __restrict__ tile_run_off,
                                                       const int* __restrict__ run_slot,
-                                                      double* __restrict__ run_part) {
-  constexpr bool RESTRICT = true;  // (the body is shared by both stencil kernels)
-  // a tile inside one region is a single run: plain block sum instead of the segmented scan
-  const bool one_run =
-      RESTRICT && (tile_run_off[blockIdx.x + 1] - tile_run_off[blockIdx.x] == 1);
-  double tsum = 0.0;
-  if (RESTRICT) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (one_run) {
-        tsum = __dadd_rn(tsum, __dadd_rn(rr[2 * k], rr[2 * k + 1]));
-      } else {
-        const int p = pidx(2 * threadIdx.x + 512 * k);
-        sw[p] = rr[2 * k];
-        sw[p + 1] = rr[2 * k + 1];
-        sl[p] = lb[k].x;
-        sl[p + 1] = lb[k].y;
-      }
-    }
-  }
-  if (RESTRICT) {
-    if (one_run) {
-      tsum = warp_sum(tsum);
-      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tsum;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
-        run_part[run_slot[tile_run_off[blockIdx.x]]] = s;
-      }
-    } else {
-      __syncthreads();
-      tile_restrict(sw, sl, run_part, run_slot + tile_run_off[blockIdx.x]);
-    }
-  }
+                                                      double* __restrict__ run_part,
+                                                      int tile) {
+  const int r0 = tile_run_off[tile];
+  const int* rs = run_slot + r0;
+  restrict_tail_runs<false>(rr, lb, sw, sl, wsum, tile_run_off[tile + 1] - r0,
+                            [rs](int r) { return __ldg(rs + r); }, run_part);
 }
 
 // Early start of an iteration's stencil (wait != nullptr): the grid is launched while k_gs of
@@ -302,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil(Dia A, const double* __res
     rr[2 * k + 1] = r1;
     if (RESTRICT) lb[k] = *reinterpret_cast<const int2*>(lab + i);
   }
-  if (RESTRICT) stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  if (RESTRICT) stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part, blockIdx.x);
   if (wait != nullptr) pdl_wait();
 }
 
@@ -438,7 +454,298 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
     for (int k = 0; k < 4; ++k)
       st2_vec(out + base + 2 * threadIdx.x + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
   if (RESTRICT)
-    stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+    stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part, blockIdx.x);
+  DK_TL(TL_STENCIL, 3);
+  if (wait != nullptr) pdl_wait();
+  DK_TL(TL_STENCIL, 4);
+}
+
+// K1 as a persistent grid fed by a bulk-copy ring (one CTA per SM; the default for the
+// symmetric 7-point operator): the same arithmetic and the same per-thread cell mapping as
+// k_stencil_sym7 (bit-identical results), but every input of a 512-cell sub-tile — the four
+// coefficient streams and their shifted re-reads, the z-planes of v and M^-1 above and below,
+// the in-plane input with its halo — lands in one shared-memory stage through cp.async.bulk
+// (one elected thread issues; an mbarrier per stage counts the bytes).  S stages keep
+// S-1 sub-tiles (~47 KB each at nx <= 62) in flight per SM while the threads work on one and
+// while a tile's restriction tail runs, so DRAM never waits for a dependent load round.
+// Early start: the coefficient, M^-1 copies of the first stages are issued, and the later
+// tiles' constants prefetched into L2, before the start flag; only v waits for it.
+struct RingLayout {
+  int c, u1, ux, uz, uzm, v, vm, vp, iv, im, ip, stage;  // offsets in doubles
+};
+constexpr int kSub = 512;       // cells per sub-tile (2 per thread)
+constexpr int kRingMax = 8;     // stages (mbarriers)
+__host__ __device__ inline RingLayout ring_layout(int H, bool pre) {
+  RingLayout L;
+  L.c = 0;
+  L.u1 = L.c + kSub;
+  L.ux = L.u1 + kSub + 2;
+  L.uz = L.ux + kSub + H;
+  L.uzm = L.uz + kSub;
+  L.v = L.uzm + kSub;
+  L.vm = L.v + kSub + 2 * H;
+  L.vp = L.vm + kSub;
+  L.iv = L.vp + kSub;
+  L.im = L.iv + (pre ? kSub + 2 * H : 0);
+  L.ip = L.im + (pre ? kSub : 0);
+  L.stage = L.ip + (pre ? kSub : 0);
+  return L;
+}
+
+constexpr int kSlotCap = kTile + 8;  // ints per slot-list buffer (aligned-down start + runs)
+constexpr int kRingThreads = kThreads + 32;  // 8 compute warps + the copy warp
+
+__device__ __forceinline__ void mbar_init_n(unsigned long long* bar, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
+template <bool PRE, bool RESTRICT, bool WRITE>
+__global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
+    Dia A, const double* __restrict__ v, const double* __restrict__ scale,
+    double* __restrict__ out, const int* __restrict__ lab, const int* __restrict__ tile_run_off,
+    const int* __restrict__ run_slot, double* __restrict__ run_part,
+    const int* __restrict__ gate, int H, int S, int ntiles, const unsigned* wait,
+    const double* gsig, int ng) {
+  DK_TL(TL_STENCIL, 0);
+  extern __shared__ __align__(16) double ring[];  // S stages
+  __shared__ __align__(8) unsigned long long full[kRingMax], empty[kRingMax];
+  __shared__ double sw[RESTRICT ? kTilePad : 2];
+  __shared__ int sl[RESTRICT ? kTilePad : 2];
+  __shared__ __align__(16) int sslot[RESTRICT ? 2 * kSlotCap : 4];  // two tiles' slot lists
+  __shared__ double wsum[2 * kWarps];  // by tile parity: no barrier separates two tiles' sums
+  __shared__ double s_sig;
+  __shared__ int s_go;
+  const int t = threadIdx.x;
+  const bool producer = t >= kThreads;
+  const long long nx = A.off[5], nz = A.off[6];
+  const RingLayout L = ring_layout(H, PRE);
+  const int nmine = ((int)blockIdx.x < ntiles)
+                        ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                        : 0;
+  const int nq = 4 * nmine;
+  const int npro = nq < S ? nq : S;
+  const bool has_scale = scale != nullptr;
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init1(&full[s]);
+      mbar_init_n(&empty[s], kWarps);
+    }
+    mbar_init_fence();
+  }
+  if (wait != nullptr) {
+    if (t == 0) s_go = gate == nullptr || *reinterpret_cast<const volatile int*>(gate) != 0;
+    __syncthreads();
+    if (!s_go) {  // the producer kernel did not run
+      pdl_wait();
+      return;
+    }
+  } else {
+    pdl_wait();
+    if (gate != nullptr && *gate == 0) return;
+    __syncthreads();
+  }
+  if (producer) {
+    // ---- copy warp: one lane issues every bulk copy of the block ----
+    const int lane = t - kThreads;
+    if (wait != nullptr && lane >= 1 && lane <= 6) {
+      // later tiles' constants into L2 while the start flag is awaited
+      for (int j = 1; j < nmine; ++j) {
+        const long long b0 = ((long long)blockIdx.x + (long long)j * gridDim.x) * kTile;
+        if (lane <= 4) l2_prefetch(A.co[2 + lane] + b0, kTile * 8);
+        if (PRE && lane == 5) l2_prefetch(A.inv + b0, kTile * 8);
+        if (RESTRICT && lane == 6) l2_prefetch(lab + b0, kTile * 4);
+      }
+    }
+    if (lane != 0) return;
+    const unsigned long long pol = l2_evict_first();
+    const unsigned bytes_stage =
+        8u * (unsigned)(kSub + (kSub + 2) + (kSub + nx) + 2 * kSub +
+                        (PRE ? 3 * kSub + 2 * H : 0) + 3 * kSub + 2 * H);
+    auto cell0 = [&](int q) {
+      return ((long long)blockIdx.x + (long long)(q >> 2) * gridDim.x) * kTile + (q & 3) * kSub;
+    };
+    // run offsets of the tile whose first sub-tile is issued next (loaded one tile ahead)
+    int r0 = 0, r1 = 0;
+    if (RESTRICT && nmine > 0) {
+      r0 = __ldg(tile_run_off + blockIdx.x);
+      r1 = __ldg(tile_run_off + blockIdx.x + 1);
+    }
+    // final data (operator, M^-1, the tile's slot list): may precede the start flag
+    auto issue_const = [&](int q) {
+      const int s = q % S;
+      double* st = ring + (size_t)s * L.stage;
+      unsigned long long* bar = &full[s];
+      const long long g = cell0(q);
+      unsigned bytes = bytes_stage;
+      unsigned sbytes = 0;
+      int a0 = 0;
+      if (RESTRICT && (q & 3) == 0) {
+        a0 = r0 & ~3;
+        sbytes = 4u * (unsigned)((r1 - a0 + 3) & ~3);
+        bytes += sbytes;
+      }
+      mbar_arrive_expect(bar, bytes);
+      if (RESTRICT && (q & 3) == 0) {
+        bulk_g2s(sslot + ((q >> 2) & 1) * kSlotCap, run_slot + a0, sbytes, bar, pol);
+        const int jn = (q >> 2) + 1;  // next tile's offsets for its own first sub-tile
+        if (jn < nmine) {
+          const long long tn = (long long)blockIdx.x + (long long)jn * gridDim.x;
+          r0 = __ldg(tile_run_off + tn);
+          r1 = __ldg(tile_run_off + tn + 1);
+        }
+      }
+      bulk_g2s(st + L.c, A.co[3] + g, 8u * kSub, bar, pol);
+      bulk_g2s(st + L.u1, A.co[4] + g - 2, 8u * (kSub + 2), bar, pol);
+      bulk_g2s(st + L.ux, A.co[5] + g - nx, 8u * (unsigned)(kSub + nx), bar, pol);
+      bulk_g2s(st + L.uz, A.co[6] + g, 8u * kSub, bar, pol);
+      bulk_g2s(st + L.uzm, A.co[6] + g - nz, 8u * kSub, bar, pol);
+      if (PRE) {
+        bulk_g2s(st + L.iv, A.inv + g - H, 8u * (unsigned)(kSub + 2 * H), bar, pol);
+        bulk_g2s(st + L.im, A.inv + g - nz, 8u * kSub, bar, pol);
+        bulk_g2s(st + L.ip, A.inv + g + nz, 8u * kSub, bar, pol);
+      }
+    };
+    // the iteration's input vector: after the start flag / the predecessor's completion
+    auto issue_vec = [&](int q) {
+      const int s = q % S;
+      double* st = ring + (size_t)s * L.stage;
+      unsigned long long* bar = &full[s];
+      const long long g = cell0(q);
+      bulk_g2s(st + L.v, v + g - H, 8u * (unsigned)(kSub + 2 * H), bar);
+      bulk_g2s(st + L.vm, v + g - nz, 8u * kSub, bar);
+      bulk_g2s(st + L.vp, v + g + nz, 8u * kSub, bar);
+    };
+    for (int q = 0; q < npro; ++q) issue_const(q);
+    if (wait != nullptr) {
+      while (ld_flag(wait) < (unsigned)ng) __nanosleep(64);
+      __threadfence();
+      fence_async_global();
+    }
+    for (int q = 0; q < npro; ++q) issue_vec(q);
+    for (int q = npro; q < nq; ++q) {
+      mbar_wait_parity(&empty[q % S], (unsigned)(q / S - 1) & 1u);
+      issue_const(q);
+      issue_vec(q);
+    }
+    return;
+  }
+  // ---- compute warps ----
+  double sc = 1.0;
+  if (has_scale) {
+    if (wait != nullptr) {
+      // sigma from k_gs's group partials once they are all posted (early_sigma's arithmetic)
+      if (t == 0) {
+        while (ld_flag(wait) < (unsigned)ng) __nanosleep(64);
+        __threadfence();
+        s_sig = 1.0 / sqrt(grouped_total(gsig, 0, ng));
+      }
+      tile_sync<true>();
+      sc = s_sig;
+    } else {
+      sc = __ldcg(scale);
+    }
+  }
+  DK_TL(TL_STENCIL, 1);
+  pdl_trigger();  // the next grid launches while this one runs (it still waits for it)
+  const unsigned long long pol = l2_evict_first();
+  const int lane = t & 31;
+  for (int j = 0; j < nmine; ++j) {
+    const int tile = (int)blockIdx.x + j * (int)gridDim.x;
+    const long long base = (long long)tile * kTile;
+    int2 lb[4];
+    int r0 = 0, r1 = 0;
+    if (RESTRICT) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) lb[k] = ldi2_stream(lab + base + 2 * t + 512 * k, pol);
+      r0 = __ldg(tile_run_off + tile);
+      r1 = __ldg(tile_run_off + tile + 1);
+    }
+    double rr[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int q = 4 * j + k;
+      const int s = q % S;
+      double* st = ring + (size_t)s * L.stage;
+      mbar_wait_parity(&full[s], (unsigned)(q / S) & 1u);
+      // no block barrier inside a tile's four sub-tiles: p = (sigma v) M^-1 is formed on use
+      // from the staged v and M^-1 (the same two roundings as the staged product)
+      const double* sv = st + L.v + H + 2 * t;
+      const double* si = st + L.iv + H + 2 * t;
+      auto P2 = [&](int o) {  // p at cells i + o, i + o + 1 (o even)
+        double2 x = *reinterpret_cast<const double2*>(sv + o);
+        if (has_scale) {
+          x.x = __dmul_rn(x.x, sc);
+          x.y = __dmul_rn(x.y, sc);
+        }
+        if (PRE) {
+          const double2 m = *reinterpret_cast<const double2*>(si + o);
+          x.x = __dmul_rn(x.x, m.x);
+          x.y = __dmul_rn(x.y, m.y);
+        }
+        return x;
+      };
+      const double2 pa = P2(-2), pb = P2(0), pc = P2(2), pd = P2(-(int)nx), pe = P2((int)nx);
+      const double2 c = *reinterpret_cast<const double2*>(st + L.c + 2 * t);
+      const double2 u1m = *reinterpret_cast<const double2*>(st + L.u1 + 2 * t);
+      const double2 u1 = *reinterpret_cast<const double2*>(st + L.u1 + 2 * t + 2);
+      const double2 uxm = *reinterpret_cast<const double2*>(st + L.ux + 2 * t);
+      const double2 ux = *reinterpret_cast<const double2*>(st + L.ux + 2 * t + nx);
+      const double2 uz = *reinterpret_cast<const double2*>(st + L.uz + 2 * t);
+      const double2 uzm = *reinterpret_cast<const double2*>(st + L.uzm + 2 * t);
+      double2 zm = *reinterpret_cast<const double2*>(st + L.vm + 2 * t);
+      double2 zp = *reinterpret_cast<const double2*>(st + L.vp + 2 * t);
+      if (has_scale) {
+        zm.x = __dmul_rn(zm.x, sc);
+        zm.y = __dmul_rn(zm.y, sc);
+        zp.x = __dmul_rn(zp.x, sc);
+        zp.y = __dmul_rn(zp.y, sc);
+      }
+      if (PRE) {
+        const double2 im = *reinterpret_cast<const double2*>(st + L.im + 2 * t);
+        const double2 ip = *reinterpret_cast<const double2*>(st + L.ip + 2 * t);
+        zm.x = __dmul_rn(zm.x, im.x);
+        zm.y = __dmul_rn(zm.y, im.y);
+        zp.x = __dmul_rn(zp.x, ip.x);
+        zp.y = __dmul_rn(zp.y, ip.y);
+      }
+      // sym7_apply's sums (ascending offsets): cell i, then cell i + 1
+      double r0 = __dmul_rn(uzm.x, zm.x);
+      r0 = __dadd_rn(r0, __dmul_rn(uxm.x, pd.x));
+      r0 = __dadd_rn(r0, __dmul_rn(u1m.y, pa.y));
+      r0 = __dadd_rn(r0, __dmul_rn(c.x, pb.x));
+      r0 = __dadd_rn(r0, __dmul_rn(u1.x, pb.y));
+      r0 = __dadd_rn(r0, __dmul_rn(ux.x, pe.x));
+      r0 = __dadd_rn(r0, __dmul_rn(uz.x, zp.x));
+      double r1 = __dmul_rn(uzm.y, zm.y);
+      r1 = __dadd_rn(r1, __dmul_rn(uxm.y, pd.y));
+      r1 = __dadd_rn(r1, __dmul_rn(u1.x, pb.x));
+      r1 = __dadd_rn(r1, __dmul_rn(c.y, pb.y));
+      r1 = __dadd_rn(r1, __dmul_rn(u1.y, pc.x));
+      r1 = __dadd_rn(r1, __dmul_rn(ux.y, pe.y));
+      r1 = __dadd_rn(r1, __dmul_rn(uz.y, zp.y));
+      rr[2 * k] = r0;
+      rr[2 * k + 1] = r1;
+      // this warp is done with the stage: the copy warp may refill it once all eight are
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (WRITE)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        st2_vec(out + base + 2 * t + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
+    DK_TL(TL_STENCIL, 8);
+    {
+      const int* ss = sslot + (j & 1) * kSlotCap + (r0 & 3);
+      if (RESTRICT)
+        restrict_tail_runs<true>(rr, lb, sw, sl, wsum + (j & 1) * kWarps, r1 - r0,
+                                 [ss](int r) { return ss[r]; }, run_part);
+    }
+    DK_TL(TL_STENCIL, 9);
+  }
   DK_TL(TL_STENCIL, 3);
   if (wait != nullptr) pdl_wait();
   DK_TL(TL_STENCIL, 4);
@@ -547,9 +854,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7_split(
   __syncthreads();  // the staging area becomes the restriction scratch
   double* sw = sp;
   int* sl = reinterpret_cast<int*>(sp + kTilePad);
-  stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part);
+  stencil_restrict_tail(rr, lb, sw, sl, wsum, tile_run_off, run_slot, run_part, blockIdx.x);
   __syncthreads();
-  stencil_restrict_tail(aa, lb, sw, sl, wsum, tile_run_off, run_slot, run_part2);
+  stencil_restrict_tail(aa, lb, sw, sl, wsum, tile_run_off, run_slot, run_part2, blockIdx.x);
   DK_TL(TL_STENCIL, 3);
   if (wait != nullptr) pdl_wait();
   DK_TL(TL_STENCIL, 4);
@@ -592,11 +899,43 @@ void launch_stencil_split(bool pre, bool am, const Dia& A, long long n_pad, cons
   }
 }
 
+// stages of the bulk-copy ring that fit beside the kernel's static shared memory (0: use the
+// register-load kernel; DK_NO_RING forces that)
+template <bool PRE, bool R, bool W>
+static int ring_stages(int H, size_t* stage_bytes) {
+  static const bool off = getenv("DK_NO_RING") != nullptr;
+  if (off) return 0;
+  static const int want = getenv("DK_RING_STAGES") ? atoi(getenv("DK_RING_STAGES")) : 4;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, (const void*)k_stencil_sym7_ring<PRE, R, W>) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, current_device());
+  *stage_bytes = (size_t)ring_layout(H, PRE).stage * sizeof(double);
+  const long long room = (long long)optin - (long long)fa.sharedSizeBytes - 256;
+  int S = (int)(room / (long long)*stage_bytes);
+  if (S > want) S = want;
+  if (S > kRingMax) S = kRingMax;
+  return S >= 2 ? S : 0;
+}
+
 template <bool PRE, bool R, bool W>
 static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, const double* scale,
                        double* out, const RunMap* rm, const int* gate, cudaStream_t s,
                        const unsigned* wait, const double* gsig, int ng) {
   const unsigned grid = (unsigned)(n_pad / kTile);
+  size_t stage_bytes = 0;
+  const int S = ring_stages<PRE, R, W>(H, &stage_bytes);
+  if (S > 0 && smem_optin((const void*)k_stencil_sym7_ring<PRE, R, W>, S * stage_bytes) == 0) {
+    const unsigned sms = (unsigned)num_sms();
+    launch_pdl(k_stencil_sym7_ring<PRE, R, W>, dim3(grid < sms ? grid : sms), dim3(kRingThreads),
+               S * stage_bytes, s, A, v, scale, out, rm ? rm->lab : nullptr,
+               rm ? rm->tile_run_off : nullptr, rm ? rm->run_slot : nullptr,
+               rm ? rm->run_part : nullptr, gate, H, S, (int)grid, wait, gsig, ng);
+    return;
+  }
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
   // static + dynamic above 48 KB needs the opt-in (wide grids: nx = 512)
   smem_optin((const void*)k_stencil_sym7<PRE, R, W>, smem);

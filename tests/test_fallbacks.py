@@ -11,6 +11,8 @@ environment switches (read once per process, so each variant runs in a subproces
                  they are cooperative: all blocks co-resident or the launch fails)
   DK_NO_LOOP_GRAPH     one graph launch and one host read of the state per cycle instead of
                        the conditional WHILE graph (restarts decided on the device)
+  DK_NO_RING           the register-load stencil (k_stencil_sym7) instead of the persistent
+                       bulk-copy ring (k_stencil_sym7_ring); DK_RING_STAGES=2: a 2-stage ring
   DK_FUSE_RESTRICT     (opt-in variant) the column sums inside tile pass 1, behind a grid
                        barrier of the cooperative pass
 Config 3 uses the nested-dissection tile streams (the spinning finisher) and its x is
@@ -66,7 +68,8 @@ def test_fallbacks_bitwise(gpu, cfg):
     assert ref.pop("loop") is True and ref.pop("syncs") == 1
     for extra in ({"DK_NO_SPIN": "1"},
                   {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"},
-                  {"DK_NO_COOP": "1"}, {"DK_FUSE_RESTRICT": "1"}, {"DK_NO_LOOP_GRAPH": "1"}):
+                  {"DK_NO_COOP": "1"}, {"DK_FUSE_RESTRICT": "1"}, {"DK_NO_LOOP_GRAPH": "1"},
+                  {"DK_NO_RING": "1"}, {"DK_RING_STAGES": "2"}):
         got = _run(cfg, extra)
         got_launches = got.pop("launches")
         loop, syncs = got.pop("loop"), got.pop("syncs")

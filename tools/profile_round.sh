@@ -16,5 +16,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python tools/kprof.py 3 > gpurun_out/${TAG}_launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none \
   -k regex:"k_project|k_gs|k_stencil_sym7|k_tgemv|k_restrict" --launch-skip 3000 -c 6 \
-  -o gpurun_out/${TAG}_full python tools/variant_probe.py 3 --steps 1 > gpurun_out/${TAG}_full.log 2>&1
+  -o gpurun_out/${TAG}_full env DK_NO_LOOP_GRAPH=1 python tools/variant_probe.py 3 --steps 1 > gpurun_out/${TAG}_full.log 2>&1
 echo done
