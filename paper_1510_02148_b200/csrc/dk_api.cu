@@ -1470,6 +1470,34 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
         cudaEventDestroy(p1);
         c->prof = 1;
         c->rm.s_pos = c->iperm;
+        // opt-in L2 prefetches riding on the latency-bound kernels (measured slower, DESIGN.md
+        // §5): DK_WPF=1 — the ring stencil prefetches the tile store for the coarse kernels
+        // that follow it; DK_PF2=1|2 — that tile pass prefetches the projection's per-cell
+        // prolongation constants (DK_PF2_N of its five streams)
+        if (getenv("DK_WPF")) {
+          c->rm.pf_base = c->T1;
+          c->rm.pf_bytes = (unsigned long long)h1.nt * 1024ull * sizeof(double);
+        }
+        {
+          const int which = getenv("DK_PF2") ? atoi(getenv("DK_PF2")) : 0;
+          TileGemv* tg = which == 1 ? &c->tg1 : which == 2 ? &c->tg2 : nullptr;
+          if (tg != nullptr) {
+            const unsigned long long np = (unsigned long long)op->n_pad;
+            const char* ptr[5] = {(const char*)c->pro.fco, (const char*)c->pro.flab,
+                                  (const char*)c->pro.own, (const char*)c->pro.lab,
+                                  (const char*)c->pro.mask};
+            const unsigned long long by[5] = {16 * np, 8 * np, 8 * np, 4 * np, np};
+            const int lim = getenv("DK_PF2_N") ? atoi(getenv("DK_PF2_N")) : 5;
+            tg->npf = 0;
+            for (int k = 0; k < 5 && k < lim; ++k) {
+              if (((unsigned long long)(uintptr_t)ptr[k] & 15ull) != 0 || (by[k] & 15ull) != 0)
+                break;
+              tg->pf[k] = ptr[k];
+              tg->pf_bytes[k] = by[k];
+              tg->npf = k + 1;
+            }
+          }
+        }
         inverted = true;
         tr.mark("W tile streams");
       } else {

@@ -509,7 +509,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
     double* __restrict__ out, const int* __restrict__ lab, const int* __restrict__ tile_run_off,
     const int* __restrict__ run_slot, double* __restrict__ run_part,
     const int* __restrict__ gate, int H, int S, int ntiles, const unsigned* wait,
-    const double* gsig, int ng) {
+    const double* gsig, int ng, const char* __restrict__ pf, unsigned long long pf_bytes,
+    int pf_early) {
   DK_TL(TL_STENCIL, 0);
   extern __shared__ __align__(16) double ring[];  // S stages
   __shared__ __align__(8) unsigned long long full[kRingMax], empty[kRingMax];
@@ -619,17 +620,40 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
       bulk_g2s(st + L.vm, v + g - nz, 8u * kSub, bar);
       bulk_g2s(st + L.vp, v + g + nz, 8u * kSub, bar);
     };
+    // L2 prefetch of the block's slice of the constant stream the coarse kernels read next
+    // (the W tile store): the stencil leaves more than half of the DRAM bandwidth unused, so
+    // one piece per issued stage rides along and the tile GEMV's first pass finds W in L2
+    unsigned long long pf_off = 0, pf_end = 0;
+    unsigned pf_piece = 0;
+    if (pf != nullptr && nq > 0) {
+      const unsigned long long slice =
+          ((pf_bytes + gridDim.x - 1) / gridDim.x + 127ull) & ~127ull;
+      pf_off = slice * blockIdx.x;
+      pf_end = pf_off + slice < pf_bytes ? pf_off + slice : pf_bytes;
+      pf_piece = (unsigned)(((slice + nq - 1) / nq + 127ull) & ~127ull);
+    }
+    auto issue_pf = [&]() {
+      if (pf_off < pf_end) {
+        const unsigned long long left = pf_end - pf_off;
+        const unsigned len = left < pf_piece ? (unsigned)left : pf_piece;
+        l2_prefetch(pf + pf_off, len);
+        pf_off += len;
+      }
+    };
     for (int q = 0; q < npro; ++q) issue_const(q);
+    for (int q = 0; q < pf_early && q < nq; ++q) issue_pf();
     if (wait != nullptr) {
       while (ld_flag(wait) < (unsigned)ng) __nanosleep(64);
       __threadfence();
       fence_async_global();
     }
     for (int q = 0; q < npro; ++q) issue_vec(q);
+    for (int q = pf_early; q < npro; ++q) issue_pf();
     for (int q = npro; q < nq; ++q) {
       mbar_wait_parity(&empty[q % S], (unsigned)(q / S - 1) & 1u);
       issue_const(q);
       issue_vec(q);
+      if (q >= pf_early) issue_pf();
     }
     return;
   }
@@ -928,12 +952,17 @@ static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, co
   const unsigned grid = (unsigned)(n_pad / kTile);
   size_t stage_bytes = 0;
   const int S = ring_stages<PRE, R, W>(H, &stage_bytes);
+  // pieces of the L2 prefetch issued before the early-start flag (DK_WPF_EARLY; default: the
+  // ring's prologue stages)
+  static const int pf_early = getenv("DK_WPF_EARLY") ? atoi(getenv("DK_WPF_EARLY")) : S;
   if (S > 0 && smem_optin((const void*)k_stencil_sym7_ring<PRE, R, W>, S * stage_bytes) == 0) {
     const unsigned sms = (unsigned)num_sms();
     launch_pdl(k_stencil_sym7_ring<PRE, R, W>, dim3(grid < sms ? grid : sms), dim3(kRingThreads),
                S * stage_bytes, s, A, v, scale, out, rm ? rm->lab : nullptr,
                rm ? rm->tile_run_off : nullptr, rm ? rm->run_slot : nullptr,
-               rm ? rm->run_part : nullptr, gate, H, S, (int)grid, wait, gsig, ng);
+               rm ? rm->run_part : nullptr, gate, H, S, (int)grid, wait, gsig, ng,
+               rm ? (const char*)rm->pf_base : (const char*)nullptr,
+               rm ? rm->pf_bytes : 0ull, pf_early);
     return;
   }
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);

@@ -37,6 +37,8 @@ struct RunMap {            // label-segmented restriction metadata (see DESIGN.m
   const int* long_ids;     // columns with more than kShortRuns runs (summed by a warp)
   int nlong;
   const int* s_pos;        // nullptr, or the position of label L in s (coarse ordering)
+  const void* pf_base;     // nullptr, or a constant stream the next kernels read (the W tile
+  unsigned long long pf_bytes;  // store): the ring stencil prefetches it into L2 as it goes
 };
 constexpr int kShortRuns = 16;
 
@@ -225,6 +227,11 @@ struct TileGemv {
   const int* split_rows = nullptr;  // output blocks split across warps (NOSPIN finish)
   int nsplit = 0;
   unsigned* bar = nullptr;  // [count, generation] of the in-kernel grid barrier (fused pass 1)
+  // constant streams of the kernel that follows the coarse solve (the projection's per-cell
+  // prolongation inputs): this pass prefetches them into L2 while DRAM is otherwise idle
+  const char* pf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  unsigned long long pf_bytes[5] = {0, 0, 0, 0, 0};
+  int npf = 0;
 };
 struct TileGemvHost {
   long long nt = 0;

@@ -277,6 +277,14 @@ __global__ void __launch_bounds__(KW * 32, 1) k_tgemv(TileGemv g, const double* 
   if (lane == 0)
     for (int s = 0; s < nfirst; ++s)
       tg_issue(wbuf + s * kPTileBytes, tile_ptr(t0 + s), &bars[wl][s], pol);
+  // each warp prefetches its slice of the next kernel's constant streams into L2
+  if (g.npf > 0 && lane < g.npf) {
+    const unsigned long long nwarp = (unsigned long long)gridDim.x * KW;
+    const unsigned long long tot = g.pf_bytes[lane];
+    const unsigned long long slice = ((tot + nwarp - 1) / nwarp + 127ull) & ~127ull;
+    const unsigned long long o = slice * (unsigned long long)(blockIdx.x * KW + wl);
+    if (o < tot) l2_prefetch(g.pf[lane] + o, (unsigned)(o + slice < tot ? slice : tot - o));
+  }
   // the next grid may launch now (its griddepcontrol.wait still waits for this one)
   pdl_trigger();
   pdl_wait();

@@ -17,6 +17,7 @@ BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 # (a class launch of coarse_gemv is the two tile passes: twice the per-kernel bytes)
 CLASSES = {"void dk::k_project<0,": ("prolong_dots", 1), "void dk::k_gs<0>": ("gs_update", 1),
            "void dk::k_stencil_sym7<1, 1, 1>": ("stencil_restrict", 1),
+           "void dk::k_stencil_sym7_ring<1, 1, 1>": ("stencil_restrict", 1),
            "void dk::k_stencil<0, 1, 1, 1>": ("stencil_restrict", 1),
            "dk::k_restrict_final": ("restrict_final", 1),
            "void dk::<unnamed>::k_tgemv": ("coarse_gemv", 2)}

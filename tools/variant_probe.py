@@ -23,9 +23,12 @@ ap.add_argument("config", type=int)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--tag", default="")
 ap.add_argument("--plain", action="store_true")
+ap.add_argument("--max-iters", type=int, default=0)
 a = ap.parse_args()
 lib = _lib.load()
 case = configs.make_case(a.config)
+if a.max_iters:
+    case.max_iters = a.max_iters
 A, b = case.problem()
 M = dk.Preconditioner.jacobi(A)
 op = A.device()
