@@ -460,8 +460,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_sym7(Dia A, const doubl
   DK_TL(TL_STENCIL, 4);
 }
 
-// K1 as a persistent grid fed by a bulk-copy ring (one CTA per SM; the default for the
-// symmetric 7-point operator): the same arithmetic and the same per-thread cell mapping as
+// K1 as a persistent grid fed by a bulk-copy ring (one CTA per SM; opt-in, DK_RING=1): the same arithmetic and the same per-thread cell mapping as
 // k_stencil_sym7 (bit-identical results), but every input of a 512-cell sub-tile — the four
 // coefficient streams and their shifted re-reads, the z-planes of v and M^-1 above and below,
 // the in-plane input with its halo — lands in one shared-memory stage through cp.async.bulk
@@ -924,11 +923,13 @@ void launch_stencil_split(bool pre, bool am, const Dia& A, long long n_pad, cons
 }
 
 // stages of the bulk-copy ring that fit beside the kernel's static shared memory (0: use the
-// register-load kernel; DK_NO_RING forces that)
+// register-load kernel, the default: the ring is opt-in with DK_RING=1 — at parity at config 3,
+// 4 % / 11 % slower at configs 2 / 4, where its one 288-thread block per SM delays the early
+// start against the previous kernel's draining blocks, profiles/r02f_ab_loop_ring.log)
 template <bool PRE, bool R, bool W>
 static int ring_stages(int H, size_t* stage_bytes) {
-  static const bool off = getenv("DK_NO_RING") != nullptr;
-  if (off) return 0;
+  static const bool on = getenv("DK_RING") != nullptr && getenv("DK_NO_RING") == nullptr;
+  if (!on) return 0;
   static const int want = getenv("DK_RING_STAGES") ? atoi(getenv("DK_RING_STAGES")) : 4;
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, (const void*)k_stencil_sym7_ring<PRE, R, W>) != cudaSuccess) {

@@ -8,9 +8,11 @@ mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.log 2>&1
 echo "bench rc=$?" >> gpurun_out/${TAG}_bench.log
 timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_reference.log 2>&1
-for c in 1 2 4 5; do
-  timeout 900 python bench.py --config $c --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_config$c.log 2>&1
-done
+# config 1 solves take 1.7 ms: enough steps that the clock sampler's start-up does not weigh
+timeout 600 python bench.py --config 1 --steps 100 --warmup 10 > gpurun_out/${TAG}_bench_config1.log 2>&1
+timeout 600 python bench.py --config 2 --steps 20 --warmup 3 > gpurun_out/${TAG}_bench_config2.log 2>&1
+timeout 900 python bench.py --config 4 --steps 2 --warmup 3 > gpurun_out/${TAG}_bench_config4.log 2>&1
+timeout 1500 python bench.py --config 5 --steps 2 --warmup 3 --e2e-steps 1 > gpurun_out/${TAG}_bench_config5.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
   python tools/kprof.py 3 > gpurun_out/${TAG}_launches.log 2>&1
