@@ -136,6 +136,27 @@ def test_config3_parity(gpu):
     assert np.abs(zr).max() <= 1e-6 * np.linalg.norm(b)
 
 
+def test_long_cycle_on_a_million_cells(gpu):
+    """GMRES(400) at config 3 (1.12 M cells, 548 blocks, 18 reduction groups): the
+    Gram-Schmidt update's early-start staging needs (m + 1) x groups doubles of shared memory
+    (58 KB: the opt-in path); the reference accepts any m >= 1 (krylov.py:107-125).  The first
+    50 steps of the long cycle are the Arnoldi process of GMRES(50)'s first cycle."""
+    case = configs.make_case(3)
+    A, b = case.problem()
+    M = dk.Preconditioner.jacobi(A)
+    basis = dk.partition_to_basis(case.partition())
+    short = dk.pdgmres(A, b, M=M, m=50, basis=basis, tol=case.tol, max_iters=50)
+    long_ = dk.pdgmres(A, b, M=M, m=400, basis=basis, tol=case.tol, max_iters=120)
+    assert short.iterations == 50 and long_.iterations == 120
+    np.testing.assert_allclose(long_.residual_history[:51], short.residual_history[:51],
+                               rtol=1e-9)
+    # no restart inside the long cycle: the estimate keeps decreasing past step 50
+    h = long_.residual_history
+    assert np.all(np.diff(h[:121]) <= 1e-12 * h[0])
+    plain = dk.gmres(A, b, M=M, m=400, tol=case.tol, max_iters=120)
+    assert plain.iterations == 120 and np.isfinite(plain.final_relres)
+
+
 @pytest.mark.parametrize("d_boxes", [(2, 2, 2), (8, 8, 6)])
 def test_nonsymmetric_operator_matches_oracle(gpu, d_boxes):
     """Upwinded convection-diffusion 7-point operator (non-symmetric DIA storage, E
