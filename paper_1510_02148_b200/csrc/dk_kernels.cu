@@ -31,21 +31,35 @@ namespace dk {
 __device__ __forceinline__ int pidx(int c) { return c + (c >> 3); }
 constexpr int kTilePad = kTile + kTile / 8;
 
-// RING: called by the 256 compute threads of a larger block (named barrier 1) with the
-// tile's slot list in shared memory; otherwise by a whole 256-thread block, slots in global
+// RING: called by one 256-thread compute group of a larger block (threads [256 g, 256 g + 256),
+// named barrier 1 + g) with the tile's slot list in shared memory; otherwise by a whole
+// 256-thread block, slots in global
 template <bool RING>
 __device__ __forceinline__ void tile_sync() {
-  if (RING) asm volatile("bar.sync 1, 256;" ::: "memory");
+  if (RING) asm volatile("bar.sync %0, 256;" ::"r"(1 + (int)(threadIdx.x >> 8)) : "memory");
   else __syncthreads();
 }
+// thread index within the tile's 256 threads, and the compute group
+template <bool RING>
+__device__ __forceinline__ int tile_tid() {
+  return RING ? (int)(threadIdx.x & 255) : (int)threadIdx.x;
+}
+template <bool RING>
+__device__ __forceinline__ int tile_grp() {
+  return RING ? (int)(threadIdx.x >> 8) : 0;
+}
+constexpr int kRingGroupsMax = 2;
 
 template <bool RING, class SlotFn>
 __device__ __forceinline__ void tile_restrict(const double* sw, const int* sl, double* out,
                                               SlotFn slot) {
-  __shared__ int wf[kWarps];
-  __shared__ double ws[kWarps];
-  __shared__ int wc[kWarps];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ int wf_[(RING ? kRingGroupsMax : 1) * kWarps];
+  __shared__ double ws_[(RING ? kRingGroupsMax : 1) * kWarps];
+  __shared__ int wc_[(RING ? kRingGroupsMax : 1) * kWarps];
+  int* wf = wf_ + tile_grp<RING>() * kWarps;
+  double* ws = ws_ + tile_grp<RING>() * kWarps;
+  int* wc = wc_ + tile_grp<RING>() * kWarps;
+  const int t = tile_tid<RING>(), lane = t & 31, warp = t >> 5;
   const int c0 = 8 * t;
   double val[8];
   int lb[8];
@@ -128,13 +142,14 @@ __device__ __forceinline__ void restrict_tail_runs(const double (&rr)[8], const 
                                                    double* __restrict__ run_part) {
   // a tile inside one region is a single run: plain block sum instead of the segmented scan
   const bool one_run = nruns == 1;
+  const int tl = tile_tid<RING>();
   double tsum = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (one_run) {
       tsum = __dadd_rn(tsum, __dadd_rn(rr[2 * k], rr[2 * k + 1]));
     } else {
-      const int p = pidx(2 * threadIdx.x + 512 * k);
+      const int p = pidx(2 * tl + 512 * k);
       sw[p] = rr[2 * k];
       sw[p + 1] = rr[2 * k + 1];
       sl[p] = lb[k].x;
@@ -143,9 +158,9 @@ __device__ __forceinline__ void restrict_tail_runs(const double (&rr)[8], const 
   }
   if (one_run) {
     tsum = warp_sum(tsum);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = tsum;
+    if ((tl & 31) == 0) wsum[tl >> 5] = tsum;
     tile_sync<RING>();
-    if (threadIdx.x == 0) {
+    if (tl == 0) {
       double s = 0.0;
       for (int w = 0; w < kWarps; ++w) s = __dadd_rn(s, wsum[w]);
       run_part[slot(0)] = s;
@@ -492,7 +507,16 @@ __host__ __device__ inline RingLayout ring_layout(int H, bool pre) {
 }
 
 constexpr int kSlotCap = kTile + 8;  // ints per slot-list buffer (aligned-down start + runs)
-constexpr int kRingThreads = kThreads + 32;  // 8 compute warps + the copy warp
+// NG compute groups of 8 warps (alternate tiles: one group's restriction tail overlaps the
+// other's stencil phase) + the copy warp.  Each group has its own full / empty barrier per
+// stage, so it sees every phase of the barriers it waits on (a group skipping the other
+// group's phases could not follow a shared barrier's parity).
+constexpr int ring_threads(int ng) { return ng * kThreads + 32; }
+// dynamic shared memory ahead of the stages (bytes; a multiple of 16): the restriction's
+// staging per group and NG + 1 tiles' slot lists
+constexpr size_t ring_extra(int ng, bool restrict_) {
+  return restrict_ ? (size_t)ng * kTilePad * 12 + (size_t)(ng + 1) * kSlotCap * 4 : 0;
+}
 
 __device__ __forceinline__ void mbar_init_n(unsigned long long* bar, unsigned n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n));
@@ -502,8 +526,8 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
                : "memory");
 }
 
-template <bool PRE, bool RESTRICT, bool WRITE>
-__global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
+template <bool PRE, bool RESTRICT, bool WRITE, int NG>
+__global__ void __launch_bounds__(ring_threads(NG), 1) k_stencil_sym7_ring(
     Dia A, const double* __restrict__ v, const double* __restrict__ scale,
     double* __restrict__ out, const int* __restrict__ lab, const int* __restrict__ tile_run_off,
     const int* __restrict__ run_slot, double* __restrict__ run_part,
@@ -511,16 +535,24 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
     const double* gsig, int ng, const char* __restrict__ pf, unsigned long long pf_bytes,
     int pf_early) {
   DK_TL(TL_STENCIL, 0);
-  extern __shared__ __align__(16) double ring[];  // S stages
-  __shared__ __align__(8) unsigned long long full[kRingMax], empty[kRingMax];
-  __shared__ double sw[RESTRICT ? kTilePad : 2];
-  __shared__ int sl[RESTRICT ? kTilePad : 2];
-  __shared__ __align__(16) int sslot[RESTRICT ? 2 * kSlotCap : 4];  // two tiles' slot lists
-  __shared__ double wsum[2 * kWarps];  // by tile parity: no barrier separates two tiles' sums
+  // dynamic shared memory: the restriction's staging (per group), NB tiles' slot lists,
+  // then the S stages
+  extern __shared__ __align__(16) double ring_smem[];
+  __shared__ __align__(8) unsigned long long full[NG * kRingMax], empty[NG * kRingMax];
+  constexpr int NB = NG + 1;  // slot-list buffers: tile j's is refilled for tile j + NB
+  double* sw_ = ring_smem;
+  int* sl_ = reinterpret_cast<int*>(sw_ + (RESTRICT ? NG * kTilePad : 0));
+  int* sslot = sl_ + (RESTRICT ? NG * kTilePad : 0);
+  double* ring = reinterpret_cast<double*>(sslot + (RESTRICT ? NB * kSlotCap : 0));
+  __shared__ double wsum[NG * 2 * kWarps];  // by group and by the parity of its tile count
   __shared__ double s_sig;
   __shared__ int s_go;
-  const int t = threadIdx.x;
-  const bool producer = t >= kThreads;
+  const int tid = threadIdx.x;
+  const bool producer = tid >= NG * kThreads;
+  const int grp = tid >> 8;  // compute group
+  const int t = tid & 255;   // thread of the group (the cell mapping of k_stencil_sym7)
+  double* sw = sw_ + (RESTRICT ? grp * kTilePad : 0);
+  int* sl = sl_ + (RESTRICT ? grp * kTilePad : 0);
   const long long nx = A.off[5], nz = A.off[6];
   const RingLayout L = ring_layout(H, PRE);
   const int nmine = ((int)blockIdx.x < ntiles)
@@ -529,15 +561,16 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
   const int nq = 4 * nmine;
   const int npro = nq < S ? nq : S;
   const bool has_scale = scale != nullptr;
-  if (t == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init1(&full[s]);
-      mbar_init_n(&empty[s], kWarps);
-    }
+  if (tid == 0) {
+    for (int g = 0; g < NG; ++g)
+      for (int s = 0; s < S; ++s) {
+        mbar_init1(&full[g * kRingMax + s]);
+        mbar_init_n(&empty[g * kRingMax + s], kWarps);
+      }
     mbar_init_fence();
   }
   if (wait != nullptr) {
-    if (t == 0) s_go = gate == nullptr || *reinterpret_cast<const volatile int*>(gate) != 0;
+    if (tid == 0) s_go = gate == nullptr || *reinterpret_cast<const volatile int*>(gate) != 0;
     __syncthreads();
     if (!s_go) {  // the producer kernel did not run
       pdl_wait();
@@ -550,7 +583,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
   }
   if (producer) {
     // ---- copy warp: one lane issues every bulk copy of the block ----
-    const int lane = t - kThreads;
+    const int lane = tid - NG * kThreads;
     if (wait != nullptr && lane >= 1 && lane <= 6) {
       // later tiles' constants into L2 while the start flag is awaited
       for (int j = 1; j < nmine; ++j) {
@@ -578,7 +611,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
     auto issue_const = [&](int q) {
       const int s = q % S;
       double* st = ring + (size_t)s * L.stage;
-      unsigned long long* bar = &full[s];
+      unsigned long long* bar = &full[((q >> 2) % NG) * kRingMax + s];
       const long long g = cell0(q);
       unsigned bytes = bytes_stage;
       unsigned sbytes = 0;
@@ -590,7 +623,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
       }
       mbar_arrive_expect(bar, bytes);
       if (RESTRICT && (q & 3) == 0) {
-        bulk_g2s(sslot + ((q >> 2) & 1) * kSlotCap, run_slot + a0, sbytes, bar, pol);
+        bulk_g2s(sslot + ((q >> 2) % NB) * kSlotCap, run_slot + a0, sbytes, bar, pol);
         const int jn = (q >> 2) + 1;  // next tile's offsets for its own first sub-tile
         if (jn < nmine) {
           const long long tn = (long long)blockIdx.x + (long long)jn * gridDim.x;
@@ -613,7 +646,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
     auto issue_vec = [&](int q) {
       const int s = q % S;
       double* st = ring + (size_t)s * L.stage;
-      unsigned long long* bar = &full[s];
+      unsigned long long* bar = &full[((q >> 2) % NG) * kRingMax + s];
       const long long g = cell0(q);
       bulk_g2s(st + L.v, v + g - H, 8u * (unsigned)(kSub + 2 * H), bar);
       bulk_g2s(st + L.vm, v + g - nz, 8u * kSub, bar);
@@ -639,6 +672,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
         pf_off += len;
       }
     };
+    unsigned epar[kRingGroupsMax] = {0u, 0u};  // per group: phase parity of each stage's empty
     for (int q = 0; q < npro; ++q) issue_const(q);
     for (int q = 0; q < pf_early && q < nq; ++q) issue_pf();
     if (wait != nullptr) {
@@ -649,7 +683,14 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
     for (int q = 0; q < npro; ++q) issue_vec(q);
     for (int q = pf_early; q < npro; ++q) issue_pf();
     for (int q = npro; q < nq; ++q) {
-      mbar_wait_parity(&empty[q % S], (unsigned)(q / S - 1) & 1u);
+      // stage q % S was last filled for sub-tile q - S: wait for its owner group's release
+      // (the producer sees every phase of every empty barrier, in order)
+      {
+        const int s = q % S;
+        const int go = ((q - S) >> 2) % NG;
+        mbar_wait_parity(&empty[go * kRingMax + s], (epar[go] >> s) & 1u);
+        epar[go] ^= 1u << s;
+      }
       issue_const(q);
       issue_vec(q);
       if (q >= pf_early) issue_pf();
@@ -661,12 +702,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
   if (has_scale) {
     if (wait != nullptr) {
       // sigma from k_gs's group partials once they are all posted (early_sigma's arithmetic)
-      if (t == 0) {
+      if (tid == 0) {
         while (ld_flag(wait) < (unsigned)ng) __nanosleep(64);
         __threadfence();
         s_sig = 1.0 / sqrt(grouped_total(gsig, 0, ng));
       }
-      tile_sync<true>();
+      asm volatile("bar.sync 3, %0;" ::"r"(NG * kThreads) : "memory");  // the compute threads
       sc = s_sig;
     } else {
       sc = __ldcg(scale);
@@ -676,7 +717,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
   pdl_trigger();  // the next grid launches while this one runs (it still waits for it)
   const unsigned long long pol = l2_evict_first();
   const int lane = t & 31;
-  for (int j = 0; j < nmine; ++j) {
+  unsigned fpar = 0u;  // phase parity of each stage's full barrier of this group
+  for (int j = grp; j < nmine; j += NG) {
     const int tile = (int)blockIdx.x + j * (int)gridDim.x;
     const long long base = (long long)tile * kTile;
     int2 lb[4];
@@ -693,7 +735,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
       const int q = 4 * j + k;
       const int s = q % S;
       double* st = ring + (size_t)s * L.stage;
-      mbar_wait_parity(&full[s], (unsigned)(q / S) & 1u);
+      mbar_wait_parity(&full[grp * kRingMax + s], (fpar >> s) & 1u);
+      fpar ^= 1u << s;
       // no block barrier inside a tile's four sub-tiles: p = (sigma v) M^-1 is formed on use
       // from the staged v and M^-1 (the same two roundings as the staged product)
       const double* sv = st + L.v + H + 2 * t;
@@ -754,7 +797,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
       rr[2 * k + 1] = r1;
       // this warp is done with the stage: the copy warp may refill it once all eight are
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&empty[grp * kRingMax + s]);
     }
     if (WRITE)
 #pragma unroll
@@ -762,9 +805,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_stencil_sym7_ring(
         st2_vec(out + base + 2 * t + 512 * k, make_double2(rr[2 * k], rr[2 * k + 1]));
     DK_TL(TL_STENCIL, 8);
     {
-      const int* ss = sslot + (j & 1) * kSlotCap + (r0 & 3);
+      const int* ss = sslot + (j % NB) * kSlotCap + (r0 & 3);
       if (RESTRICT)
-        restrict_tail_runs<true>(rr, lb, sw, sl, wsum + (j & 1) * kWarps, r1 - r0,
+        restrict_tail_runs<true>(rr, lb, sw, sl,
+                                 wsum + (2 * grp + ((j / NG) & 1)) * kWarps, r1 - r0,
                                  [ss](int r) { return ss[r]; }, run_part);
     }
     DK_TL(TL_STENCIL, 9);
@@ -926,24 +970,50 @@ void launch_stencil_split(bool pre, bool am, const Dia& A, long long n_pad, cons
 // register-load kernel, the default: the ring is opt-in with DK_RING=1 — at parity at config 3,
 // 4 % / 11 % slower at configs 2 / 4, where its one 288-thread block per SM delays the early
 // start against the previous kernel's draining blocks, profiles/r02f_ab_loop_ring.log)
-template <bool PRE, bool R, bool W>
+template <bool PRE, bool R, bool W, int NG>
 static int ring_stages(int H, size_t* stage_bytes) {
   static const bool on = getenv("DK_RING") != nullptr && getenv("DK_NO_RING") == nullptr;
   if (!on) return 0;
   static const int want = getenv("DK_RING_STAGES") ? atoi(getenv("DK_RING_STAGES")) : 4;
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, (const void*)k_stencil_sym7_ring<PRE, R, W>) != cudaSuccess) {
+  if (cudaFuncGetAttributes(&fa, (const void*)k_stencil_sym7_ring<PRE, R, W, NG>) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, current_device());
   *stage_bytes = (size_t)ring_layout(H, PRE).stage * sizeof(double);
-  const long long room = (long long)optin - (long long)fa.sharedSizeBytes - 256;
+  const long long room = (long long)optin - (long long)fa.sharedSizeBytes - 256 -
+                         (long long)ring_extra(NG, R);
   int S = (int)(room / (long long)*stage_bytes);
   if (S > want) S = want;
-  if (S > kRingMax) S = kRingMax;
+  if (S > 4) S = 4;  // a tile's slot list is refilled NG + 1 tiles later: needs S <= 4
   return S >= 2 ? S : 0;
+}
+
+// launches the ring kernel with NG compute groups when at least two stages fit
+template <bool PRE, bool R, bool W, int NG>
+static bool stencil7_ring(const Dia& A, int H, long long n_pad, const double* v,
+                          const double* scale, double* out, const RunMap* rm, const int* gate,
+                          cudaStream_t s, const unsigned* wait, const double* gsig, int ng) {
+  const unsigned grid = (unsigned)(n_pad / kTile);
+  size_t stage_bytes = 0;
+  const int S = ring_stages<PRE, R, W, NG>(H, &stage_bytes);
+  // pieces of the L2 prefetch issued before the early-start flag (DK_WPF_EARLY; default: the
+  // ring's prologue stages)
+  static const int pf_early = getenv("DK_WPF_EARLY") ? atoi(getenv("DK_WPF_EARLY")) : S;
+  if (S <= 0 ||
+      smem_optin((const void*)k_stencil_sym7_ring<PRE, R, W, NG>,
+                 S * stage_bytes + ring_extra(NG, R)) != 0)
+    return false;
+  const unsigned sms = (unsigned)num_sms();
+  launch_pdl(k_stencil_sym7_ring<PRE, R, W, NG>, dim3(grid < sms ? grid : sms),
+             dim3(ring_threads(NG)), S * stage_bytes + ring_extra(NG, R), s, A, v, scale, out,
+             rm ? rm->lab : nullptr, rm ? rm->tile_run_off : nullptr,
+             rm ? rm->run_slot : nullptr, rm ? rm->run_part : nullptr, gate, H, S, (int)grid,
+             wait, gsig, ng, rm ? (const char*)rm->pf_base : (const char*)nullptr,
+             rm ? rm->pf_bytes : 0ull, pf_early);
+  return true;
 }
 
 template <bool PRE, bool R, bool W>
@@ -951,21 +1021,13 @@ static void stencil7_t(const Dia& A, int H, long long n_pad, const double* v, co
                        double* out, const RunMap* rm, const int* gate, cudaStream_t s,
                        const unsigned* wait, const double* gsig, int ng) {
   const unsigned grid = (unsigned)(n_pad / kTile);
-  size_t stage_bytes = 0;
-  const int S = ring_stages<PRE, R, W>(H, &stage_bytes);
-  // pieces of the L2 prefetch issued before the early-start flag (DK_WPF_EARLY; default: the
-  // ring's prologue stages)
-  static const int pf_early = getenv("DK_WPF_EARLY") ? atoi(getenv("DK_WPF_EARLY")) : S;
-  if (S > 0 && smem_optin((const void*)k_stencil_sym7_ring<PRE, R, W>, S * stage_bytes) == 0) {
-    const unsigned sms = (unsigned)num_sms();
-    launch_pdl(k_stencil_sym7_ring<PRE, R, W>, dim3(grid < sms ? grid : sms), dim3(kRingThreads),
-               S * stage_bytes, s, A, v, scale, out, rm ? rm->lab : nullptr,
-               rm ? rm->tile_run_off : nullptr, rm ? rm->run_slot : nullptr,
-               rm ? rm->run_part : nullptr, gate, H, S, (int)grid, wait, gsig, ng,
-               rm ? (const char*)rm->pf_base : (const char*)nullptr,
-               rm ? rm->pf_bytes : 0ull, pf_early);
+  // the opt-in ring (DK_RING=1): DK_RING_GROUPS=2 runs two compute groups per block
+  static const int groups = getenv("DK_RING_GROUPS") ? atoi(getenv("DK_RING_GROUPS")) : 1;
+  if (groups >= 2 &&
+      stencil7_ring<PRE, R, W, 2>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng))
     return;
-  }
+  if (stencil7_ring<PRE, R, W, 1>(A, H, n_pad, v, scale, out, rm, gate, s, wait, gsig, ng))
+    return;
   const size_t smem = (size_t)(kTile + 2 * H) * sizeof(double);
   // static + dynamic above 48 KB needs the opt-in (wide grids: nx = 512)
   smem_optin((const void*)k_stencil_sym7<PRE, R, W>, smem);

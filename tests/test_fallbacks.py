@@ -13,7 +13,8 @@ environment switches (read once per process, so each variant runs in a subproces
                        the conditional WHILE graph (restarts decided on the device)
   DK_RING              (opt-in variant) the persistent bulk-copy ring stencil
                        (k_stencil_sym7_ring) instead of the register-load stencil
-                       (k_stencil_sym7); DK_RING_STAGES=2: a 2-stage ring
+                       (k_stencil_sym7); DK_RING_STAGES=2: a 2-stage ring; DK_RING_GROUPS=2: two
+                       compute groups per block on alternate tiles
   DK_WPF / DK_PF2      (opt-in) L2 prefetches issued by the ring stencil (W tile store) and a
                        tile pass (the projection's constants): hints only, results unchanged
   DK_FUSE_RESTRICT     (opt-in variant) the column sums inside tile pass 1, behind a grid
@@ -73,6 +74,7 @@ def test_fallbacks_bitwise(gpu, cfg):
                   {"DK_NO_SPIN": "1", "DK_NO_GS_FUSE": "1", "DK_NO_EARLY": "1"},
                   {"DK_NO_COOP": "1"}, {"DK_FUSE_RESTRICT": "1"}, {"DK_NO_LOOP_GRAPH": "1"},
                   {"DK_RING": "1"}, {"DK_RING": "1", "DK_RING_STAGES": "2"},
+                  {"DK_RING": "1", "DK_RING_GROUPS": "2"},
                   {"DK_WPF": "1", "DK_PF2": "1"}, {"DK_WPF": "1", "DK_PF2": "2", "DK_WPF_EARLY": "0"}):
         got = _run(cfg, extra)
         got_launches = got.pop("launches")
