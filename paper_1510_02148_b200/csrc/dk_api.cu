@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dk_launch.h"
@@ -1235,22 +1236,70 @@ int dk_defl_create(dk_defl** out, dk_op* op, const int32_t* col_of_cell, int32_t
   const long long ntiles = n_pad / kTile;
   std::vector<int> tile_off(ntiles + 1, 0);
   std::vector<int> run_label;
-  run_label.reserve(n_pad / 8 + 16);
-  for (long long t = 0; t < ntiles; ++t) {
-    tile_off[t] = (int)run_label.size();
-    const long long i0 = t * kTile;
-    int prev = lab[i0];
-    if (prev < -1 || prev >= d) return fail(DK_EINVAL, "column label out of range");
-    run_label.push_back(prev);
-    if (prev >= 0) count[prev]++;
-    for (long long i = i0 + 1; i < i0 + kTile; ++i) {
-      const int L = lab[i];
-      if (L != prev) {
-        if (L < -1 || L >= d) return fail(DK_EINVAL, "column label out of range");
-        run_label.push_back(L);
-        prev = L;
+  {
+    // host threads scan disjoint tile ranges; their runs are concatenated in tile order, so
+    // the result does not depend on the thread count
+    struct Part {
+      std::vector<int> runs, off;  // runs of the range; first run of each of its tiles
+      std::vector<long long> count;
+      bool bad = false;
+    };
+    unsigned hw = std::thread::hardware_concurrency();
+    int nthr = (int)std::min<long long>(std::min<unsigned>(hw ? hw : 1u, 8u), ntiles / 64);
+    if (nthr < 1) nthr = 1;
+    std::vector<Part> parts(nthr);
+    auto scan = [&](int p) {
+      Part& P = parts[p];
+      const long long t0 = ntiles * p / nthr, t1 = ntiles * (p + 1) / nthr;
+      P.count.assign(d, 0);
+      P.off.reserve(t1 - t0);
+      P.runs.reserve((t1 - t0) * kTile / 8 + 16);
+      const int* lb = lab.data();
+      for (long long t = t0; t < t1; ++t) {
+        P.off.push_back((int)P.runs.size());
+        const long long i0 = t * kTile;
+        int prev = lb[i0];
+        if (prev < -1 || prev >= d) {
+          P.bad = true;
+          return;
+        }
+        P.runs.push_back(prev);
+        if (prev >= 0) P.count[prev]++;
+        for (long long i = i0 + 1; i < i0 + kTile; ++i) {
+          const int L = lb[i];
+          if (L != prev) {
+            if (L < -1 || L >= d) {
+              P.bad = true;
+              return;
+            }
+            P.runs.push_back(L);
+            prev = L;
+          }
+          if (L >= 0) P.count[L]++;
+        }
       }
-      if (L >= 0) count[L]++;
+    };
+    if (nthr == 1) {
+      scan(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int p = 1; p < nthr; ++p) th.emplace_back(scan, p);
+      scan(0);
+      for (auto& t : th) t.join();
+    }
+    size_t total = 0;
+    for (const Part& P : parts) {
+      if (P.bad) return fail(DK_EINVAL, "column label out of range");
+      total += P.runs.size();
+    }
+    run_label.reserve(total + 16);
+    for (int p = 0; p < nthr; ++p) {
+      const Part& P = parts[p];
+      const long long t0 = ntiles * p / nthr;
+      const int base = (int)run_label.size();
+      for (size_t k = 0; k < P.off.size(); ++k) tile_off[t0 + (long long)k] = base + P.off[k];
+      run_label.insert(run_label.end(), P.runs.begin(), P.runs.end());
+      for (int L = 0; L < d; ++L) count[L] += P.count[L];
     }
   }
   tile_off[ntiles] = (int)run_label.size();
